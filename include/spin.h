@@ -1,0 +1,197 @@
+/*
+ * spin.h — C ABI of libspin, the B200 (sm_100a) spin-image engine.
+ *
+ * The hot path is the DOALL spin-image loop of the paper (Eleliemy, Mohammed,
+ * Ciorba, "Efficient Generation of Parallel Spin-images Using Dynamic Loop
+ * Scheduling", arXiv 1811.00901): Algorithm 1 `calculateSpinImages(W, B, S, OP, N)`
+ * (`algo:spin`) and its per-chunk form Algorithm 2
+ * `adCalculateSpinImages(..., spinImages, start, end)` (PAPER.md:286-319,
+ * `algo:adaptedcalc`), with its iterations dealt by the paper's STATIC / SS / GSS /
+ * FAC loop schedules (§2.2; `getChunk`).
+ *
+ * Naming follows BASELINE.json: N = number of oriented points (the paper's M,
+ * PAPER.md:109), M = number of spin images (the paper's N),
+ * b = bin size (the paper's B), A_s = support angle (the paper's S).
+ *
+ * Conventions for every entry point
+ *   - d_* arguments are CUDA DEVICE pointers, h_* arguments are HOST pointers.
+ *     spin_create / spin_load_cloud accept either (the copy uses cudaMemcpyDefault).
+ *   - Arrays are dense, row-major, little-endian, 4-byte aligned.
+ *   - No C++ exception crosses this boundary.  Every call returns a spin_status;
+ *     spin_last_error() then holds a thread-local message naming the offending
+ *     argument or index.
+ *   - `stream` is a cudaStream_t (NULL = the legacy default stream).  Calls are
+ *     asynchronous with respect to the host unless stated otherwise.
+ */
+#ifndef SPIN_H_
+#define SPIN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPIN_ABI_VERSION 1
+
+typedef struct spin_ctx* spin_handle;
+typedef struct CUstream_st* spin_stream; /* identical to cudaStream_t */
+
+typedef enum {
+  SPIN_OK = 0,
+  SPIN_E_INVAL = 1,    /* a synchronous argument check failed                        */
+  SPIN_E_RANGE = 2,    /* a centre index outside [0, N) (detected on the device)     */
+  SPIN_E_INPUT = 3,    /* non-finite coordinate, or |normal| outside [0.999, 1.001] */
+  SPIN_E_NOMEM = 4,    /* device or host allocation failed                           */
+  SPIN_E_CUDA = 5,     /* a CUDA runtime error (message carries cudaGetErrorString) */
+  SPIN_E_OVERFLOW = 6  /* an accumulator could not hold a bin (see spin_generate)   */
+} spin_status;
+
+/* Loop schedules of PAPER.md §2.2.  STATIC = PSIA's fixed blocks
+ * (P:476-477); SS = one unit per request; GSS = ceil(R/P) per request
+ * (P:224-228); FAC = batches of P equal chunks, size ceil(R_batch/(2P))
+ * (the FAC2 reading). */
+typedef enum { SPIN_STATIC = 0, SPIN_SS = 1, SPIN_GSS = 2, SPIN_FAC = 3 } spin_schedule;
+
+/* NEAREST: the paper's integer count tempSpinImage[k,l]++ (P:173-174).
+ * BILINEAR: weight 1 split over the 4 bins around (u, v) (north star; not in the
+ * paper — SURVEY.md §8(c) #12). */
+typedef enum { SPIN_NEAREST = 0, SPIN_BILINEAR = 1 } spin_mode;
+
+/* BRUTE: every (centre, point) pair, as Alg. 1's inner loop.
+ * CELLS: exact uniform-grid pruning — only points in cells that intersect the
+ * bounding box of a centre group grown by the region radius are visited. */
+typedef enum { SPIN_BRUTE = 0, SPIN_CELLS = 1 } spin_prune;
+
+/* flags */
+#define SPIN_F_LITERAL_HALF_WIDTH 0x1u /* u = (W/2 - beta)/b exactly as printed; default u = W/2 - beta/b (#2) */
+#define SPIN_F_FLOOR_BINS         0x2u /* NEAREST: k = floor(u), l = floor(v) (Johnson) instead of ceil */
+#define SPIN_F_NO_SORT            0x4u /* CELLS: keep the caller's centre order (control run)    */
+#define SPIN_F_NO_FAST_CERT       0x8u /* testing: send every candidate through the fp64 / exact decision stages   */
+
+/* Scheduling parameters.  All-zero = defaults. */
+typedef struct {
+  int32_t P;             /* "processing elements" (P:230, P:338 workersCount) = resident CTAs
+                            of the persistent launch; 0 -> occupancy x SM count           */
+  int32_t unit;          /* images per scheduling iteration; 0 -> the kernel group size G;
+                            1 = the paper's one-image iteration            */
+  int32_t gss_min_chunk; /* GSS minimum chunk in units; 0 -> 1 (#16)                      */
+  int32_t fac_divisor;   /* FAC: chunk = ceil(R_batch / (fac_divisor * P)); 0 -> 2 (#15)   */
+  uint32_t flags;        /* SPIN_F_* */
+} spin_chunk_params;
+
+/* Optional per-call statistics.  Passing non-NULL makes spin_generate synchronise
+ * `stream` before it returns (the counters are read back). */
+typedef struct {
+  double elapsed_ms;        /* device time of the persistent kernel (CUDA events)          */
+  double grid_build_ms;     /* CELLS: device time of a grid (re)build in this call, else 0 */
+  int64_t pairs_visited;    /* (centre, point) pairs evaluated by the pair test            */
+  int64_t pairs_candidate;  /* pairs that passed the fp32 conservative region test         */
+  int64_t pairs_accepted;   /* pairs that contributed (NEAREST: sum of all counts)         */
+  int64_t fp64_fallbacks;   /* decisions the fp32 stage could not certify                  */
+  int64_t exact_fallbacks;  /* decisions the fp64 stage could not certify (exact stage)    */
+  int32_t P;                /* resident CTAs used                                          */
+  int32_t G;                /* images per CTA group                                        */
+  int32_t n_units;          /* scheduling units                                            */
+  int32_t n_chunks;         /* chunks in the schedule                                      */
+  uint64_t* h_cta_start_ns; /* caller array [P] or NULL: %globaltimer at CTA start         */
+  uint64_t* h_cta_end_ns;   /* caller array [P] or NULL: %globaltimer at CTA finish        */
+  int32_t* h_cta_units;     /* caller array [P] or NULL: units processed per CTA           */
+  int32_t cta_capacity;     /* length of the three arrays above                            */
+} spin_stats;
+
+/*
+ * spin_create — make a handle that owns a device copy of the oriented point cloud.
+ *   points, normals: fp32 [N][3] (x,y,z) — the set OP of PAPER.md:115 with normals
+ *                    np_i.  Host or device pointers (cudaMemcpyDefault).
+ *   N: number of oriented points, 1 <= N < 2^31.
+ * Copies and re-lays the cloud out as SoA float4 {x,y,z,|x|^2} + {nx,ny,nz,0} in
+ * HBM (the input "replicated to every worker", P:256 / P:333, is resident once).
+ * Validates: every coordinate finite, every |normal| in [0.999, 1.001]
+ * (SPIN_E_INPUT names the first bad index).  Normals are NOT renormalised (#7).
+ * Synchronises `stream`.  The caller may free its arrays when it returns.
+ */
+spin_status spin_create(const float* points, const float* normals, int64_t N,
+                        spin_stream stream, spin_handle* out);
+
+/*
+ * spin_load_cloud — replace the handle's cloud (same rules as spin_create).
+ * Reuses the device buffers when N fits the current capacity; cached cell grids
+ * are invalidated.  Synchronises `stream`.
+ */
+spin_status spin_load_cloud(spin_handle h, const float* points, const float* normals,
+                            int64_t N, spin_stream stream);
+
+/*
+ * spin_generate — the hot path: M spin images, one per centre (Alg. 1 / Alg. 2).
+ *   d_centre_idx: int32 [M] device; image m spins around point d_centre_idx[m]
+ *                 (duplicates allowed; the paper's case is iota(0, paper-N)).
+ *   M: number of images, M >= 0 (M = 0 is a no-op).
+ *   W: image width in bins, 1 <= W <= 64 (BILINEAR: W >= 2).
+ *   b: bin size in cloud length units, finite, 1e-30 <= b <= 1e30.
+ *   cos_As: cosine of the support angle: a point contributes only if
+ *           n . n_x >= cos_As (inclusive, #5).  -INFINITY disables the test (the
+ *           paper's S = 2 pi).  Otherwise must lie in [-1, 1].
+ *   sched, cp: loop schedule and its parameters (cp may be NULL = defaults).
+ *   mode, prune: see the enums.
+ *   d_out: fp32 [M][W][W] device, fully overwritten; out[m][k][l], row k = beta bin,
+ *          column l = alpha bin, as tempSpinImage[k,l].  NEAREST counts are
+ *          exact integers in fp32 (counts <= N < 2^24 required, else SPIN_E_INVAL).
+ *   stats: optional (see spin_stats).
+ * Results equal the EXACT-arithmetic evaluation of Alg. 1 on the fp32 inputs
+ * (b and cos_As as exact doubles): NEAREST bit-exact; BILINEAR to fp32 weight
+ * rounding (2^-24 per corner).  Every decision the fp32 stage cannot certify is
+ * re-taken in fp64 and, if still uncertain, exactly.
+ * Schedule, P and unit never change the result (NEAREST and BILINEAR both
+ * bit-reproducible).  Asynchronous on `stream` (unless stats != NULL).
+ * A centre index outside [0, N) zeroes that image and latches SPIN_E_RANGE, which
+ * this call returns if stats != NULL, else the next call on the handle returns.
+ * d_centre_idx and d_out must not alias each other or handle memory.  A handle is
+ * not safe for concurrent spin_generate calls (shared scratch): serialise per handle.
+ */
+spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M, int32_t W,
+                          double b, double cos_As, spin_schedule sched,
+                          const spin_chunk_params* cp, spin_mode mode, spin_prune prune,
+                          float* d_out, spin_stats* stats, spin_stream stream);
+
+/*
+ * spin_generate_host — spin_generate with HOST buffers: copies h_centre_idx [M]
+ * to the device, runs, copies the images to h_out [M][W][W] (pinned memory is
+ * fastest; pageable works) and synchronises `stream`.  Device scratch for the
+ * centres and images is owned by the handle and grown on demand.
+ */
+spin_status spin_generate_host(spin_handle h, const int32_t* h_centre_idx, int64_t M,
+                               int32_t W, double b, double cos_As, spin_schedule sched,
+                               const spin_chunk_params* cp, spin_mode mode, spin_prune prune,
+                               float* h_out, spin_stats* stats, spin_stream stream);
+
+/*
+ * spin_chunk_sequence — host-only trace of a schedule (SPEC getChunk traces):
+ * writes the chunk boundaries b_0 = 0 < b_1 < ... < b_n = n_units into h_bounds
+ * (capacity `cap` entries, n_chunks + 1 needed) and the chunk count into *n_chunks.
+ * SPIN_E_RANGE if cap is too small (*n_chunks still set).  P >= 1, n_units >= 0.
+ */
+spin_status spin_chunk_sequence(spin_schedule sched, int64_t n_units, int32_t P,
+                                const spin_chunk_params* cp, int64_t* h_bounds, int64_t cap,
+                                int64_t* n_chunks);
+
+/* spin_region_radius — upper bound on |X - P| of any contributing pair for (W, b,
+ * mode, flags): sqrt(alpha_max^2 + |beta|_max^2).  Host-only. */
+double spin_region_radius(int32_t W, double b, spin_mode mode, uint32_t flags);
+
+/* spin_cos_from_degrees — cos of an angle in degrees, exact at 0, 60, 90, 120, 180
+ * (1, 0.5, 0, -0.5, -1); >= 180 degrees returns -INFINITY (test disabled). */
+double spin_cos_from_degrees(double deg);
+
+/* spin_default_P — the resident-CTA count the persistent launch would use for
+ * (W, mode, prune) on the current device (occupancy x SMs); <= 0 on error. */
+int32_t spin_default_P(int32_t W, spin_mode mode, spin_prune prune);
+
+void spin_destroy(spin_handle h);
+const char* spin_last_error(void);
+int32_t spin_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPIN_H_ */

@@ -1,0 +1,61 @@
+"""Build libspin.so in-tree for sm_100a (called by __graft_entry__.build()).
+
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo; cudart linked
+statically so the library does not depend on the process's libcudart.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "libspin.so")
+BUILD = os.path.join(HERE, "..", "build", "spin")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr"]
+SOURCES = ["spin_kernels.cu", "spin_api.cpp"]
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("build failed:\n" + " ".join(cmd) + "\n" + r.stdout)
+    return r.stdout
+
+
+def _stale(objs):
+    if not os.path.exists(OUT):
+        return True
+    t = os.path.getmtime(OUT)
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    deps.append(os.path.join(HERE, "..", "include", "spin.h"))
+    deps.append(os.path.abspath(__file__))
+    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    objs = [os.path.join(BUILD, s + ".o") for s in SOURCES]
+    if not force and not _stale(objs):
+        return OUT
+    def comp(src, obj):
+        extra = ["-Xptxas", "-v"] if (verbose and src.endswith(".cu")) else []
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", os.path.join(HERE, "..", "include"),
+               "-c", os.path.join(CSRC, src), "-o", obj]
+        return _run(cmd)
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        logs = list(ex.map(comp, SOURCES, objs))
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", OUT + ".tmp", *objs])
+    os.replace(OUT + ".tmp", OUT)
+    if verbose:
+        print("".join(logs))
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,654 @@
+// spin_api.cpp — the C ABI of include/spin.h and the host planner.
+//
+// Planner duties per spin_generate call: validate (§8(b)),
+// region constants and certified fp32 thresholds (a2), the chunk-boundary table of
+// the schedule (a3, §2.2), the CELLS grid (a4, cached per cell size) and
+// the centre ordering (a5), then one launch of the persistent kernel (a6-a13).
+#include "../../include/spin.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "spin_internal.h"
+
+using namespace spin;
+
+namespace {
+
+thread_local std::string g_err;
+
+spin_status fail(spin_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+spin_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(SPIN_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+#define CK(call, what)                                   \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what);   \
+  } while (0)
+
+constexpr int TILE_POINTS = 256 * 4;  // NT * KP of the kernel
+constexpr double U32 = 5.9604644775390625e-08;  // 2^-24
+
+template <typename T>
+spin_status ensure(T*& ptr, int64_t& cap, int64_t need, const char* what) {
+  if (need <= cap && ptr) return SPIN_OK;
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  cap = 0;
+  int64_t n = std::max<int64_t>(need, 1);
+  if (cudaMalloc((void**)&ptr, (size_t)n * sizeof(T)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SPIN_E_NOMEM, "cudaMalloc failed for %s (%lld elements)", what, (long long)n);
+  }
+  cap = n;
+  return SPIN_OK;
+}
+
+float f32_up(double x) {
+  float f = (float)x;
+  if ((double)f < x) f = std::nextafter(f, INFINITY);
+  return f;
+}
+float f32_down(double x) {
+  float f = (float)x;
+  if ((double)f > x) f = std::nextafter(f, -INFINITY);
+  return f;
+}
+
+// The set of (u, v) that contributes, per mode and flags:
+//   NEAREST ceil : k = ceil(u) in [0,W)  <=> u in (-1, W-1];  l = ceil(v) <= W-1  <=> v <= W-1
+//   NEAREST floor: k = floor(u) in [0,W) <=> u in [0, W);     v < W
+//   BILINEAR     : floor(u) in [0,W-2]   <=> u in [0, W-1);   v < W-1
+// and beta = (W/2 - u) b (scaled) or W/2 - u b (literal).
+struct Region {
+  double ulo, uhi, vmax;
+  double beta_lo, beta_hi, Qmax, mid, h, R;
+};
+Region region_of(int W, double b, int mode, uint32_t flags) {
+  Region r;
+  if (mode == SPIN_NEAREST && !(flags & SPIN_F_FLOOR_BINS)) {
+    r.ulo = -1.0; r.uhi = W - 1.0; r.vmax = W - 1.0;
+  } else if (mode == SPIN_NEAREST) {
+    r.ulo = 0.0; r.uhi = (double)W; r.vmax = (double)W;
+  } else {
+    r.ulo = 0.0; r.uhi = W - 1.0; r.vmax = W - 1.0;
+  }
+  const double A = 0.5 * W;
+  auto beta_of = [&](double u) { return (flags & SPIN_F_LITERAL_HALF_WIDTH) ? A - u * b : (A - u) * b; };
+  const double b1 = beta_of(r.uhi), b2 = beta_of(r.ulo);
+  r.beta_lo = std::min(b1, b2);
+  r.beta_hi = std::max(b1, b2);
+  r.Qmax = (r.vmax * b) * (r.vmax * b);
+  r.mid = 0.5 * (r.beta_lo + r.beta_hi);
+  r.h = 0.5 * (r.beta_hi - r.beta_lo);
+  const double bm = std::max(std::fabs(r.beta_lo), std::fabs(r.beta_hi));
+  r.R = std::sqrt(r.Qmax + bm * bm);
+  return r;
+}
+
+void build_bounds(spin_schedule sched, int64_t n, int32_t P, int32_t gss_min, int32_t fac_div,
+                  std::vector<int64_t>& out) {
+  out.clear();
+  out.push_back(0);
+  if (n <= 0) return;
+  int64_t R = n;
+  switch (sched) {
+    case SPIN_STATIC: {  // P near-equal blocks, the first n mod P one larger (#17)
+      const int64_t q = n / P, r = n % P;
+      const int64_t nb = std::min<int64_t>(P, n);
+      for (int64_t i = 0; i < nb; ++i) out.push_back(out.back() + q + (i < r ? 1 : 0));
+      break;
+    }
+    case SPIN_SS:        // one iteration per request
+      for (int64_t i = 1; i <= n; ++i) out.push_back(i);
+      break;
+    case SPIN_GSS:       // ceil(remaining / P), at least gss_min (#16)
+      while (R > 0) {
+        int64_t c = std::min(R, std::max<int64_t>(gss_min, (R + P - 1) / P));
+        out.push_back(out.back() + c);
+        R -= c;
+      }
+      break;
+    case SPIN_FAC:       // batches of P equal chunks ceil(R / (fac_div P)) (#15)
+      while (R > 0) {
+        const int64_t c = std::max<int64_t>(1, (R + (int64_t)fac_div * P - 1) / ((int64_t)fac_div * P));
+        for (int i = 0; i < P && R > 0; ++i) {
+          const int64_t t = std::min(c, R);
+          out.push_back(out.back() + t);
+          R -= t;
+        }
+      }
+      break;
+  }
+}
+
+}  // namespace
+
+struct spin_ctx {
+  int dev = 0, sms = 0;
+  int64_t N = 0, Npad = 0, cap = 0;
+  float4* pos = nullptr;
+  float4* nrm = nullptr;
+  float absmax = 0.f;
+  float aabb[6] = {0, 0, 0, 0, 0, 0};
+  uint64_t cloud_version = 0;
+  // CELLS grid cache
+  bool grid_valid = false;
+  uint64_t grid_version = 0;
+  float grid_h = 0.f;
+  int dx = 0, dy = 0, dz = 0;
+  float ox = 0, oy = 0, oz = 0, inv_h = 0;
+  int32_t* cell_start = nullptr; int64_t cell_start_cap = 0;
+  float4* spos = nullptr; int64_t spos_cap = 0;
+  float4* snrm = nullptr; int64_t snrm_cap = 0;
+  int32_t* keys = nullptr; int64_t keys_cap = 0;
+  int32_t* counts = nullptr; int64_t counts_cap = 0;
+  int32_t* cursor = nullptr; int64_t cursor_cap = 0;
+  int32_t* scan_tmp = nullptr; int64_t scan_tmp_cap = 0;
+  // centre ordering scratch
+  int32_t* ckeys = nullptr; int64_t ckeys_cap = 0;
+  int32_t* cstarts = nullptr; int64_t cstarts_cap = 0;
+  int32_t* order = nullptr; int64_t order_cap = 0;
+  // dealing
+  int32_t* bounds = nullptr; int64_t bounds_cap = 0;
+  std::vector<int64_t> bounds_h;
+  long long bounds_key[6] = {-1, -1, -1, -1, -1, -1};
+  unsigned* counter = nullptr;
+  unsigned long long* stats = nullptr;
+  int32_t* err = nullptr;
+  int32_t* h_err = nullptr;  // pinned copy of the previous call's flags
+  cudaEvent_t ev_err = nullptr, ev0 = nullptr, ev1 = nullptr, evg0 = nullptr, evg1 = nullptr;
+  bool err_pending = false;
+  unsigned long long* cta_t0 = nullptr; unsigned long long* cta_t1 = nullptr;
+  int32_t* cta_units = nullptr; int64_t cta_cap = 0;
+  // cloud staging (AoS input) and reductions
+  float* stage_p = nullptr; int64_t stage_p_cap = 0;
+  float* stage_n = nullptr; int64_t stage_n_cap = 0;
+  int32_t* red = nullptr;     // [0] bad index, [1] absmax bits, [2..7] aabb bits
+  int32_t* h_red = nullptr;   // pinned
+  // host-buffer path scratch
+  int32_t* cidx = nullptr; int64_t cidx_cap = 0;
+  float* outbuf = nullptr; int64_t outbuf_cap = 0;
+};
+
+namespace {
+
+spin_status load_cloud(spin_ctx* h, const float* points, const float* normals, int64_t N,
+                       cudaStream_t s) {
+  if (!points || !normals) return fail(SPIN_E_INVAL, "points/normals must be non-null");
+  if (N < 1 || N >= ((int64_t)1 << 31) - 2 * TILE_POINTS)
+    return fail(SPIN_E_INVAL, "N=%lld outside [1, 2^31)", (long long)N);
+  const int64_t Npad = ((N + 1 + TILE_POINTS - 1) / TILE_POINTS) * TILE_POINTS;  // >= 1 sentinel
+  if (Npad > h->cap) {
+    if (h->pos) cudaFree(h->pos);
+    if (h->nrm) cudaFree(h->nrm);
+    h->pos = h->nrm = nullptr;
+    h->cap = 0;
+    if (cudaMalloc((void**)&h->pos, Npad * sizeof(float4)) != cudaSuccess ||
+        cudaMalloc((void**)&h->nrm, Npad * sizeof(float4)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(SPIN_E_NOMEM, "cudaMalloc of the cloud (%lld points) failed", (long long)N);
+    }
+    h->cap = Npad;
+  }
+  // stage AoS input on the device (host or device source: cudaMemcpyDefault)
+  spin_status st;
+  if ((st = ensure(h->stage_p, h->stage_p_cap, N * 3, "staging")) != SPIN_OK) return st;
+  if ((st = ensure(h->stage_n, h->stage_n_cap, N * 3, "staging")) != SPIN_OK) return st;
+  CK(cudaMemcpyAsync(h->stage_p, points, N * 3 * sizeof(float), cudaMemcpyDefault, s), "copy points");
+  CK(cudaMemcpyAsync(h->stage_n, normals, N * 3 * sizeof(float), cudaMemcpyDefault, s), "copy normals");
+  const int32_t big = 0x7fffffff;
+  // [0] first bad index; [1] absmax bits 0; aabb min as flipped +max, max as flipped -max
+  const int32_t init[8] = {big, 0, 0x7fffffff, 0x7fffffff, 0x7fffffff, (int32_t)0x80000000,
+                           (int32_t)0x80000000, (int32_t)0x80000000};
+  std::memcpy(h->h_red, init, sizeof init);
+  CK(cudaMemcpyAsync(h->red, h->h_red, sizeof init, cudaMemcpyHostToDevice, s), "init");
+  CK(launch_relayout(h->stage_p, h->stage_n, N, Npad, h->pos, h->nrm, h->red,
+                     reinterpret_cast<float*>(h->red + 1), reinterpret_cast<float*>(h->red + 2), s),
+     "relayout");
+  CK(cudaMemcpyAsync(h->h_red, h->red, sizeof init, cudaMemcpyDeviceToHost, s), "readback");
+  CK(cudaStreamSynchronize(s), "spin_create sync");
+  int32_t red[8];
+  std::memcpy(red, h->h_red, sizeof red);
+  const int32_t bad = red[0];
+  if (bad != big)
+    return fail(SPIN_E_INPUT, "point %d: non-finite coordinate or |normal| outside [0.999, 1.001]", bad);
+  auto unflip = [](int32_t i) { int32_t v = i >= 0 ? i : i ^ 0x7fffffff; float f; std::memcpy(&f, &v, 4); return f; };
+  std::memcpy(&h->absmax, &red[1], 4);
+  for (int a = 0; a < 6; ++a) h->aabb[a] = unflip(red[2 + a]);
+  h->N = N;
+  h->Npad = Npad;
+  h->cloud_version++;
+  h->grid_valid = false;
+  return SPIN_OK;
+}
+
+spin_status ensure_grid(spin_ctx* h, float R, cudaStream_t s, double* build_ms) {
+  // cell edge R/2; grow it if the grid would exceed 2^24 cells
+  double hh = 0.5 * R;
+  const double ex = std::max(1e-30, (double)h->aabb[3] - h->aabb[0]);
+  const double ey = std::max(1e-30, (double)h->aabb[4] - h->aabb[1]);
+  const double ez = std::max(1e-30, (double)h->aabb[5] - h->aabb[2]);
+  while ((ex / hh + 2) * (ey / hh + 2) * (ez / hh + 2) > (double)(1 << 24)) hh *= 1.25;
+  const float hf = (float)hh;
+  if (h->grid_valid && h->grid_version == h->cloud_version && h->grid_h == hf) {
+    *build_ms = 0.0;
+    return SPIN_OK;
+  }
+  h->ox = h->aabb[0];
+  h->oy = h->aabb[1];
+  h->oz = h->aabb[2];
+  h->inv_h = (float)(1.0 / hh);
+  auto dim = [&](float lo, float hi) {
+    const float t = (hi - lo) * h->inv_h;  // same rounding as the device cell_coord
+    return (int)std::floor(t) + 1;
+  };
+  h->dx = dim(h->aabb[0], h->aabb[3]);
+  h->dy = dim(h->aabb[1], h->aabb[4]);
+  h->dz = dim(h->aabb[2], h->aabb[5]);
+  const int64_t ncells = (int64_t)h->dx * h->dy * h->dz;
+  spin_status st;
+  if ((st = ensure(h->cell_start, h->cell_start_cap, ncells + 1, "cell_start")) != SPIN_OK) return st;
+  if ((st = ensure(h->counts, h->counts_cap, std::max<int64_t>(ncells, 1 << 18), "counts")) != SPIN_OK) return st;
+  if ((st = ensure(h->cursor, h->cursor_cap, std::max<int64_t>(ncells, 1 << 18), "cursor")) != SPIN_OK) return st;
+  if ((st = ensure(h->scan_tmp, h->scan_tmp_cap, (int64_t)scan_tmp_elems(std::max<int64_t>(ncells, 1 << 18)) + 1, "scan_tmp")) != SPIN_OK) return st;
+  if ((st = ensure(h->keys, h->keys_cap, h->N, "keys")) != SPIN_OK) return st;
+  if ((st = ensure(h->spos, h->spos_cap, h->Npad, "spos")) != SPIN_OK) return st;
+  if ((st = ensure(h->snrm, h->snrm_cap, h->Npad, "snrm")) != SPIN_OK) return st;
+  CK(cudaEventRecord(h->evg0, s), "event");
+  CK(launch_cell_build(h->pos, h->nrm, (int32_t)h->N, (int32_t)h->Npad, h->ox, h->oy, h->oz,
+                       h->inv_h, h->dx, h->dy, h->dz, h->keys, h->counts, h->cell_start,
+                       h->cursor, h->scan_tmp, h->spos, h->snrm, s),
+     "cell build");
+  CK(cudaEventRecord(h->evg1, s), "event");
+  *build_ms = -1.0;  // measured later if stats are requested
+  h->grid_valid = true;
+  h->grid_version = h->cloud_version;
+  h->grid_h = hf;
+  return SPIN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t spin_abi_version(void) { return SPIN_ABI_VERSION; }
+const char* spin_last_error(void) { return g_err.c_str(); }
+
+double spin_cos_from_degrees(double deg) {
+  if (deg >= 180.0) return -INFINITY;
+  if (deg == 0.0) return 1.0;
+  if (deg == 60.0) return 0.5;
+  if (deg == 90.0) return 0.0;
+  if (deg == 120.0) return -0.5;
+  return std::cos(deg * (M_PI / 180.0));
+}
+
+double spin_region_radius(int32_t W, double b, spin_mode mode, uint32_t flags) {
+  return region_of(W, b, (int)mode, flags).R;
+}
+
+spin_status spin_chunk_sequence(spin_schedule sched, int64_t n_units, int32_t P,
+                                const spin_chunk_params* cp, int64_t* h_bounds, int64_t cap,
+                                int64_t* n_chunks) {
+  if (P < 1) return fail(SPIN_E_INVAL, "P=%d must be >= 1", P);
+  if (n_units < 0) return fail(SPIN_E_INVAL, "n_units must be >= 0");
+  if (sched < SPIN_STATIC || sched > SPIN_FAC) return fail(SPIN_E_INVAL, "bad schedule %d", (int)sched);
+  spin_chunk_params d{};
+  if (cp) d = *cp;
+  if (d.gss_min_chunk < 0 || d.fac_divisor < 0) return fail(SPIN_E_INVAL, "negative chunk parameter");
+  std::vector<int64_t> b;
+  build_bounds(sched, n_units, P, d.gss_min_chunk ? d.gss_min_chunk : 1,
+               d.fac_divisor ? d.fac_divisor : 2, b);
+  if (n_chunks) *n_chunks = (int64_t)b.size() - 1;
+  if ((int64_t)b.size() > cap || !h_bounds)
+    return fail(SPIN_E_RANGE, "need %lld bound entries, cap is %lld", (long long)b.size(), (long long)cap);
+  std::memcpy(h_bounds, b.data(), b.size() * sizeof(int64_t));
+  return SPIN_OK;
+}
+
+int32_t spin_default_P(int32_t W, spin_mode mode, spin_prune prune) {
+  if (W < 1 || W > 64) return -1;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const LaunchCfg lc = choose_launch(W, (int)mode, (int)prune);
+  return occupancy_blocks(lc, W, (int)mode, (int)prune) * sms;
+}
+
+spin_status spin_create(const float* points, const float* normals, int64_t N, spin_stream stream,
+                        spin_handle* out) {
+  if (!out) return fail(SPIN_E_INVAL, "out handle pointer is null");
+  *out = nullptr;
+  spin_ctx* h = new (std::nothrow) spin_ctx();
+  if (!h) return fail(SPIN_E_NOMEM, "host allocation failed");
+  cudaStream_t s = (cudaStream_t)stream;
+  auto bail = [&](spin_status st) { spin_destroy(h); return st; };
+  if (cudaGetDevice(&h->dev) != cudaSuccess) return bail(fail(SPIN_E_CUDA, "no CUDA device"));
+  cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->dev);
+  if (cudaMalloc((void**)&h->counter, sizeof(unsigned)) != cudaSuccess ||
+      cudaMalloc((void**)&h->stats, ST_NSLOTS * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMalloc((void**)&h->err, 4 * sizeof(int32_t)) != cudaSuccess ||
+      cudaMallocHost((void**)&h->h_err, 4 * sizeof(int32_t)) != cudaSuccess ||
+      cudaMalloc((void**)&h->red, 8 * sizeof(int32_t)) != cudaSuccess ||
+      cudaMallocHost((void**)&h->h_red, 8 * sizeof(int32_t)) != cudaSuccess) {
+    cudaGetLastError();
+    return bail(fail(SPIN_E_NOMEM, "handle allocation failed"));
+  }
+  if (cudaMemset(h->err, 0, 4 * sizeof(int32_t)) != cudaSuccess)
+    return bail(fail(SPIN_E_CUDA, "memset failed"));
+  std::memset(h->h_err, 0, 4 * sizeof(int32_t));
+  cudaEventCreateWithFlags(&h->ev_err, cudaEventDisableTiming);
+  cudaEventCreate(&h->ev0);
+  cudaEventCreate(&h->ev1);
+  cudaEventCreate(&h->evg0);
+  cudaEventCreate(&h->evg1);
+  spin_status st = load_cloud(h, points, normals, N, s);
+  if (st != SPIN_OK) return bail(st);
+  *out = h;
+  return SPIN_OK;
+}
+
+spin_status spin_load_cloud(spin_handle h, const float* points, const float* normals, int64_t N,
+                            spin_stream stream) {
+  if (!h) return fail(SPIN_E_INVAL, "null handle");
+  return load_cloud(h, points, normals, N, (cudaStream_t)stream);
+}
+
+void spin_destroy(spin_handle h) {
+  if (!h) return;
+  void* ptrs[] = {h->pos, h->nrm, h->cell_start, h->spos, h->snrm, h->keys, h->counts,
+                  h->cursor, h->scan_tmp, h->ckeys, h->cstarts, h->order, h->bounds,
+                  h->counter, h->stats, h->err, h->cta_t0, h->cta_t1, h->cta_units, h->cidx,
+                  h->outbuf, h->stage_p, h->stage_n, h->red};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (h->h_err) cudaFreeHost(h->h_err);
+  if (h->h_red) cudaFreeHost(h->h_red);
+  cudaEvent_t evs[] = {h->ev_err, h->ev0, h->ev1, h->evg0, h->evg1};
+  for (cudaEvent_t e : evs)
+    if (e) cudaEventDestroy(e);
+  delete h;
+}
+
+spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M, int32_t W,
+                          double b, double cos_As, spin_schedule sched,
+                          const spin_chunk_params* cp, spin_mode mode, spin_prune prune,
+                          float* d_out, spin_stats* stats, spin_stream stream) {
+  if (!h) return fail(SPIN_E_INVAL, "null handle");
+  cudaStream_t s = (cudaStream_t)stream;
+  // ---- a deferred SPIN_E_RANGE / overflow from an earlier asynchronous call
+  if (h->err_pending && cudaEventQuery(h->ev_err) == cudaSuccess) {
+    h->err_pending = false;
+    if (h->h_err[0]) { h->h_err[0] = 0; return fail(SPIN_E_RANGE, "an earlier call saw a centre index outside [0, N)"); }
+    if (h->h_err[1]) { h->h_err[1] = 0; return fail(SPIN_E_OVERFLOW, "an earlier call overflowed a bin accumulator"); }
+  }
+  // ---- synchronous argument checks (§8(b) SPIN_E_INVAL)
+  if (M < 0) return fail(SPIN_E_INVAL, "M=%lld must be >= 0", (long long)M);
+  if (M >= ((int64_t)1 << 31)) return fail(SPIN_E_INVAL, "M=%lld must be < 2^31", (long long)M);
+  if (W < 1 || W > 64) return fail(SPIN_E_INVAL, "W=%d outside [1, 64]", W);
+  if (mode != SPIN_NEAREST && mode != SPIN_BILINEAR) return fail(SPIN_E_INVAL, "bad mode %d", (int)mode);
+  if (mode == SPIN_BILINEAR && W < 2) return fail(SPIN_E_INVAL, "BILINEAR needs W >= 2");
+  if (prune != SPIN_BRUTE && prune != SPIN_CELLS) return fail(SPIN_E_INVAL, "bad prune %d", (int)prune);
+  if (sched < SPIN_STATIC || sched > SPIN_FAC) return fail(SPIN_E_INVAL, "bad schedule %d", (int)sched);
+  if (!std::isfinite(b) || b < 1e-30 || b > 1e30) return fail(SPIN_E_INVAL, "b=%g must be finite in [1e-30, 1e30]", b);
+  const bool has_support = !(std::isinf(cos_As) && cos_As < 0);
+  if (has_support && !(cos_As >= -1.0 && cos_As <= 1.0))
+    return fail(SPIN_E_INVAL, "cos_As=%g must be in [-1, 1] or -inf", cos_As);
+  spin_chunk_params cpar{};
+  if (cp) cpar = *cp;
+  if (cpar.P < 0 || cpar.unit < 0 || cpar.gss_min_chunk < 0 || cpar.fac_divisor < 0)
+    return fail(SPIN_E_INVAL, "negative chunk parameter");
+  if (cpar.flags & ~0xfu) return fail(SPIN_E_INVAL, "unknown flag bits 0x%x", cpar.flags);
+  if (M > 0 && (!d_centre_idx || !d_out)) return fail(SPIN_E_INVAL, "null d_centre_idx or d_out with M > 0");
+  if (stats) {
+    stats->elapsed_ms = stats->grid_build_ms = 0.0;
+    stats->pairs_visited = stats->pairs_candidate = stats->pairs_accepted = 0;
+    stats->fp64_fallbacks = stats->exact_fallbacks = 0;
+    stats->P = stats->G = stats->n_units = stats->n_chunks = 0;
+  }
+  if (M == 0) return SPIN_OK;
+
+  // ---- launch shape, P, units, chunk table (a3)
+  const LaunchCfg lc = choose_launch(W, (int)mode, (int)prune);
+  const int occ = occupancy_blocks(lc, W, (int)mode, (int)prune);
+  if (occ <= 0) return fail(SPIN_E_CUDA, "kernel does not fit on the device (smem %zu)", lc.smem);
+  const int P = cpar.P > 0 ? cpar.P : occ * h->sms;
+  if (P > 1 << 20) return fail(SPIN_E_INVAL, "P=%d too large", P);
+  const int unit = cpar.unit > 0 ? cpar.unit : lc.G;
+  const int64_t n_units = (M + unit - 1) / unit;
+  const int gmin = cpar.gss_min_chunk ? cpar.gss_min_chunk : 1;
+  const int fdiv = cpar.fac_divisor ? cpar.fac_divisor : 2;
+  const long long key[6] = {(long long)sched, (long long)n_units, P, gmin, fdiv, 1};
+  if (!std::equal(key, key + 6, h->bounds_key)) {
+    build_bounds(sched, n_units, P, gmin, fdiv, h->bounds_h);
+    std::vector<int32_t> b32(h->bounds_h.begin(), h->bounds_h.end());
+    spin_status st = ensure(h->bounds, h->bounds_cap, (int64_t)b32.size(), "chunk table");
+    if (st != SPIN_OK) return st;
+    CK(cudaMemcpyAsync(h->bounds, b32.data(), b32.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s), "chunk table");
+    CK(cudaStreamSynchronize(s), "chunk table");  // b32 is a temporary
+    std::copy(key, key + 6, h->bounds_key);
+  }
+  const int n_chunks = (int)h->bounds_h.size() - 1;
+  if (h->cta_cap < P) {
+    if (h->cta_t0) cudaFree(h->cta_t0);
+    if (h->cta_t1) cudaFree(h->cta_t1);
+    if (h->cta_units) cudaFree(h->cta_units);
+    h->cta_t0 = h->cta_t1 = nullptr;
+    h->cta_units = nullptr;
+    h->cta_cap = 0;
+    if (cudaMalloc((void**)&h->cta_t0, P * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc((void**)&h->cta_t1, P * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc((void**)&h->cta_units, P * sizeof(int32_t)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(SPIN_E_NOMEM, "per-CTA instrumentation allocation failed");
+    }
+    h->cta_cap = P;
+  }
+
+  // ---- a2: region constants and certified thresholds
+  const uint32_t flags = cpar.flags;
+  const Region rg = region_of(W, b, (int)mode, flags);
+  const double X = std::max((double)h->absmax, 1e-30) * (1.0 + 1e-6);
+  const double u = U32;
+  const double amid = std::fabs(rg.mid);
+  // hot loop (fp32, expanded forms; bounds hold for any pair inside the region)
+  const double Eb_h = 8.0 * u * (X + amid) * 1.01;
+  const double Et_h = 16.0 * u * (X + amid) * (X + amid) * 1.01;
+  const double Eq_h = Et_h + Eb_h * (2.0 * rg.h + Eb_h) + 2.0 * u * (rg.Qmax + 2.0 * (X + amid) * (X + amid));
+  const double Es_h = 4.0 * u * 1.01;
+  KParams p{};
+  p.b = b;
+  p.cos_As = has_support ? cos_As : -INFINITY;
+  p.A = 0.5 * W;
+  p.mid = rg.mid;
+  p.Qmax = rg.Qmax;
+  p.Eq_hot = Eq_h;
+  p.c_test = has_support ? f32_down(cos_As - Es_h) : -INFINITY;
+  p.h_test = f32_up(rg.h + Eb_h);
+  p.has_support = has_support ? 1 : 0;
+  // candidates satisfy |d| <= D: q <= Qmax + 2Eq, |beta| <= |mid| + h_test + Eb
+  const double Cmax = (X + amid) * (X + amid) * 1.01;
+  const double bmax = amid + (double)p.h_test + Eb_h;
+  const double D2 = (rg.Qmax + 2.0 * Eq_h + 4.0 * u * (rg.Qmax + Cmax) + bmax * bmax) * 1.001 + 1e-30;
+  const double D = std::sqrt(D2);
+  // accept path, fp32 direct forms, valid while |d| <= D
+  const double Es_a = 5.5 * u * 1.01;
+  const double Eb_a = 4.2 * u * D * 1.002;
+  const double Edd_a = 5.2 * u * D2;
+  const double Eq_a = Edd_a + Eb_a * (2.0 * D + Eb_a) + 1.01 * u * D2;
+  double Eu_a;
+  if (!(flags & SPIN_F_LITERAL_HALF_WIDTH))
+    Eu_a = ((Eb_a + 1.01 * u * D) / b + u * (p.A + D / b)) * 1.01;
+  else
+    Eu_a = (Eb_a + 3.01 * u * (p.A + D)) / b * 1.01;
+  const double Ew_a = (Eq_a + 2.01 * u * D2) / (b * b) * 1.01;
+  p.c_f = has_support ? (float)cos_As : -INFINITY;
+  p.inv_b = (float)(1.0 / b);
+  p.inv_b2 = (float)(1.0 / (b * b));
+  p.Af = (float)p.A;
+  p.Es_a = f32_up(Es_a);
+  p.Eu_a = f32_up(Eu_a);
+  p.Ew_a = f32_up(Ew_a);
+  p.D2g = f32_down(D2);
+  p.literal = (flags & SPIN_F_LITERAL_HALF_WIDTH) ? 1 : 0;
+  p.floor_bins = (flags & SPIN_F_FLOOR_BINS) ? 1 : 0;
+  p.no_fast_cert = (flags & SPIN_F_NO_FAST_CERT) ? 1 : 0;
+  // self pair (d = 0): beta = q = 0 exactly, u = W/2 (scaled reading only)
+  p.self_fast = p.literal ? 0 : 1;
+  if (mode == SPIN_NEAREST) {
+    const int k = p.floor_bins ? (int)std::floor(p.A) : (int)std::ceil(p.A);
+    p.self_k = (k >= 0 && k < W) ? k : -1;
+    p.self_l = 0;
+    p.self_a = 0.f;
+  } else {
+    const double i0 = std::floor(p.A);
+    const bool in = p.A >= 0.0 && p.A < W - 1.0;
+    p.self_k = in ? (int)i0 : -1;
+    p.self_l = 0;
+    p.self_a = (float)(p.A - i0);
+  }
+  if (!(Eu_a < 0.25 && Ew_a < 0.25)) p.no_fast_cert = 1;  // fp32 cannot resolve bins: skip it
+
+  // ---- cloud, centres, dealing, outputs
+  p.cpos = h->pos;
+  p.cnrm = h->nrm;
+  p.N = (int32_t)h->N;
+  p.centre_idx = d_centre_idx;
+  p.order = nullptr;
+  p.M = M;
+  p.W = W;
+  p.out = d_out;
+  p.bounds = h->bounds;
+  p.n_chunks = n_chunks;
+  p.unit_images = unit;
+  p.is_static = sched == SPIN_STATIC ? 1 : 0;
+  p.counter = h->counter;
+  p.stats = h->stats;
+  p.cta_t0 = h->cta_t0;
+  p.cta_t1 = h->cta_t1;
+  p.cta_units = h->cta_units;
+  p.err_flags = h->err;
+  p.row_cap = 256;
+  double grid_ms = 0.0;
+  if (prune == SPIN_BRUTE) {
+    p.pos = h->pos;
+    p.nrm = h->nrm;
+    p.n_tiles = (int32_t)(((h->N + TILE_POINTS - 1) / TILE_POINTS));
+  } else {
+    const float R = f32_up(rg.R * (1.0 + 1e-6) + 1e-30);
+    spin_status st = ensure_grid(h, R, s, &grid_ms);
+    if (st != SPIN_OK) return st;
+    p.pos = h->spos;
+    p.nrm = h->snrm;
+    p.cell_start = h->cell_start;
+    p.dimx = h->dx; p.dimy = h->dy; p.dimz = h->dz;
+    p.ox = h->ox; p.oy = h->oy; p.oz = h->oz;
+    p.inv_h = h->inv_h;
+    p.R_up = R;
+    if (!(flags & SPIN_F_NO_SORT)) {
+      int shift = 0;
+      const int dmax = std::max(h->dx, std::max(h->dy, h->dz));
+      while ((dmax >> shift) > 64) ++shift;
+      int bits = 0;
+      while ((1 << bits) < ((dmax - 1) >> shift) + 1) ++bits;
+      bits = std::max(bits, 1);
+      const int64_t nb = (int64_t)1 << (3 * bits);
+      if ((st = ensure(h->ckeys, h->ckeys_cap, M, "centre keys")) != SPIN_OK) return st;
+      if ((st = ensure(h->order, h->order_cap, M, "centre order")) != SPIN_OK) return st;
+      if ((st = ensure(h->cstarts, h->cstarts_cap, nb + 1, "centre buckets")) != SPIN_OK) return st;
+      if ((st = ensure(h->counts, h->counts_cap, nb, "counts")) != SPIN_OK) return st;
+      if ((st = ensure(h->cursor, h->cursor_cap, nb, "cursor")) != SPIN_OK) return st;
+      if ((st = ensure(h->scan_tmp, h->scan_tmp_cap, (int64_t)scan_tmp_elems(nb) + 1, "scan_tmp")) != SPIN_OK) return st;
+      CK(launch_centre_order(d_centre_idx, M, h->pos, (int32_t)h->N, h->ox, h->oy, h->oz,
+                             h->inv_h, h->dx, h->dy, h->dz, shift, bits, h->ckeys, h->counts,
+                             h->cstarts, h->cursor, h->scan_tmp, h->order, s),
+         "centre order");
+      p.order = h->order;
+    }
+  }
+
+  // ---- a6-a13: the persistent launch
+  CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned), s), "memset");
+  CK(cudaMemsetAsync(h->stats, 0, ST_NSLOTS * sizeof(unsigned long long), s), "memset");
+  CK(cudaEventRecord(h->ev0, s), "event");
+  CK(launch_spin(lc, (int)mode, (int)prune, P, p, s), "spin kernel launch");
+  CK(cudaEventRecord(h->ev1, s), "event");
+  CK(cudaMemcpyAsync(h->h_err, h->err, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "err readback");
+  CK(cudaMemsetAsync(h->err, 0, 2 * sizeof(int32_t), s), "memset");
+  CK(cudaEventRecord(h->ev_err, s), "event");
+  h->err_pending = true;
+
+  if (stats) {
+    CK(cudaStreamSynchronize(s), "stats sync");
+    unsigned long long sv[ST_NSLOTS];
+    CK(cudaMemcpy(sv, h->stats, sizeof sv, cudaMemcpyDeviceToHost), "stats");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+    stats->elapsed_ms = ms;
+    if (grid_ms < 0.0) {
+      float gm = 0.f;
+      cudaEventElapsedTime(&gm, h->evg0, h->evg1);
+      stats->grid_build_ms = gm;
+    }
+    stats->pairs_visited = prune == SPIN_BRUTE ? M * h->N : (int64_t)sv[ST_VISITED];
+    stats->pairs_candidate = (int64_t)sv[ST_CAND];
+    stats->pairs_accepted = (int64_t)sv[ST_ACC];
+    stats->fp64_fallbacks = (int64_t)sv[ST_F64];
+    stats->exact_fallbacks = (int64_t)sv[ST_EXACT];
+    stats->P = P;
+    stats->G = lc.G;
+    stats->n_units = (int32_t)n_units;
+    stats->n_chunks = n_chunks;
+    const int nc = std::min(P, stats->cta_capacity);
+    if (nc > 0) {
+      if (stats->h_cta_start_ns) CK(cudaMemcpy(stats->h_cta_start_ns, h->cta_t0, nc * 8, cudaMemcpyDeviceToHost), "cta");
+      if (stats->h_cta_end_ns) CK(cudaMemcpy(stats->h_cta_end_ns, h->cta_t1, nc * 8, cudaMemcpyDeviceToHost), "cta");
+      if (stats->h_cta_units) CK(cudaMemcpy(stats->h_cta_units, h->cta_units, nc * 4, cudaMemcpyDeviceToHost), "cta");
+    }
+    h->err_pending = false;
+    if (h->h_err[0]) { h->h_err[0] = 0; return fail(SPIN_E_RANGE, "a centre index is outside [0, N); its image is zero"); }
+    if (h->h_err[1]) { h->h_err[1] = 0; return fail(SPIN_E_OVERFLOW, "a bin accumulator overflowed"); }
+  }
+  return SPIN_OK;
+}
+
+spin_status spin_generate_host(spin_handle h, const int32_t* h_centre_idx, int64_t M, int32_t W,
+                               double b, double cos_As, spin_schedule sched,
+                               const spin_chunk_params* cp, spin_mode mode, spin_prune prune,
+                               float* h_out, spin_stats* stats, spin_stream stream) {
+  if (!h) return fail(SPIN_E_INVAL, "null handle");
+  if (M < 0) return fail(SPIN_E_INVAL, "M must be >= 0");
+  if (M == 0) return spin_generate(h, nullptr, 0, W, b, cos_As, sched, cp, mode, prune, nullptr, stats, stream);
+  if (!h_centre_idx || !h_out) return fail(SPIN_E_INVAL, "null host buffer");
+  if (W < 1 || W > 64) return fail(SPIN_E_INVAL, "W=%d outside [1, 64]", W);
+  cudaStream_t s = (cudaStream_t)stream;
+  spin_status st;
+  if ((st = ensure(h->cidx, h->cidx_cap, M, "centre scratch")) != SPIN_OK) return st;
+  if ((st = ensure(h->outbuf, h->outbuf_cap, M * W * W, "image scratch")) != SPIN_OK) return st;
+  CK(cudaMemcpyAsync(h->cidx, h_centre_idx, M * sizeof(int32_t), cudaMemcpyHostToDevice, s), "H2D centres");
+  st = spin_generate(h, h->cidx, M, W, b, cos_As, sched, cp, mode, prune, h->outbuf, stats, stream);
+  if (st != SPIN_OK) return st;
+  CK(cudaMemcpyAsync(h_out, h->outbuf, (size_t)M * W * W * sizeof(float), cudaMemcpyDeviceToHost, s), "D2H images");
+  CK(cudaStreamSynchronize(s), "sync");
+  return SPIN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// spin_internal.h — structures shared by the host planner (spin_api.cpp) and the
+// sm_100a kernels (spin_kernels.cu).  Not part of the ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace spin {
+
+// Per-launch parameters of the persistent spin kernel (passed __grid_constant__).
+struct KParams {
+  // ---- cloud (a1).  BRUTE: original order; CELLS: cell-sorted copy.  Both have
+  // N real points followed by sentinel padding (|x|^2 = +inf never passes).
+  const float4* __restrict__ pos;   // {x, y, z, |x|^2}
+  const float4* __restrict__ nrm;   // {nx, ny, nz, 0}
+  const float4* __restrict__ cpos;  // original-order copies, indexed by centre index
+  const float4* __restrict__ cnrm;
+  int32_t N;
+  int32_t n_tiles;                  // BRUTE: padded length / (NT*K)
+
+  // ---- centres and output (a5, a12)
+  const int32_t* __restrict__ centre_idx;  // [M]
+  const int32_t* __restrict__ order;       // [M] processing position -> m, or nullptr
+  int64_t M;
+  int32_t W;
+  float* __restrict__ out;                 // [M][W][W]
+
+  // ---- dealing (a3, a6)
+  const int32_t* __restrict__ bounds;      // chunk boundaries in units, [n_chunks + 1]
+  int32_t n_chunks;
+  int32_t unit_images;                     // images per unit
+  int32_t is_static;                       // chunk = blockIdx.x, no atomics
+  unsigned int* counter;                   // the "master": one u32 in global memory
+
+  // ---- region constants (a2).  Doubles are exact host values; floats are the
+  // conservative fp32 thresholds of the hot loop.
+  double b, cos_As;          // cos_As = -inf disables the support test
+  double A;                  // W/2
+  double mid, Qmax;          // beta window centre, alpha^2 bound: region is |beta-mid|<=h, q<=Qmax
+  double Eq_hot;             // hot-loop bound on |q''_fp32 - q''| (added to Qmax - C per centre)
+  float c_test, h_test;      // hot loop: s >= c_test, |beta''| <= h_test
+  int32_t has_support;
+  // accept path, fp32 stage
+  float c_f;                 // (float)cos_As, its rounding is inside Es_a
+  float inv_b, inv_b2, Af;
+  float Es_a, Eu_a, Ew_a, D2g;
+  int32_t literal, floor_bins, no_fast_cert;
+  int32_t self_fast;         // d == 0 pairs can be decided exactly without arithmetic
+  int32_t self_k, self_l;    // their (k, l) (NEAREST) or (i0, -) ; self_k = -1: no contribution
+  float self_a;              // BILINEAR: a for the self pair
+
+  // ---- CELLS (a4)
+  const int32_t* __restrict__ cell_start;  // [ncells + 1]
+  int32_t dimx, dimy, dimz;
+  float ox, oy, oz, inv_h;                 // cell = floor((x - o) * inv_h)
+  float R_up;                              // region radius rounded up
+  int32_t row_cap;
+
+  // ---- instrumentation (a13) and errors
+  unsigned long long* stats;               // [8] global counters
+  unsigned long long* cta_t0;              // [P]
+  unsigned long long* cta_t1;              // [P]
+  int32_t* cta_units;                      // [P]
+  int32_t* err_flags;                      // [0]: bad centre index seen; [1]: overflow
+};
+
+enum StatSlot {
+  ST_VISITED = 0, ST_CAND = 1, ST_ACC = 2, ST_F64 = 3, ST_EXACT = 4, ST_NSLOTS = 8
+};
+
+// Launch configuration chosen by the planner.
+struct LaunchCfg {
+  int G;           // images per group (8, 16, 32)
+  int threads;     // NT
+  size_t smem;     // dynamic shared memory bytes
+};
+
+// ---- launchers implemented in spin_kernels.cu
+LaunchCfg choose_launch(int W, int mode, int prune);
+int occupancy_blocks(const LaunchCfg& lc, int W, int mode, int prune);
+cudaError_t launch_spin(const LaunchCfg& lc, int mode, int prune, int grid, const KParams& p,
+                        cudaStream_t s);
+
+// cloud relayout + validation (a1)
+cudaError_t launch_relayout(const float* pts, const float* nrm, int64_t N, int64_t Npad,
+                            float4* pos, float4* nrm4, int32_t* bad, float* absmax,
+                            float* aabb, cudaStream_t s);
+
+// CELLS grid build (a4): keys + histogram, exclusive scan, scatter
+cudaError_t launch_cell_build(const float4* pos, const float4* nrm, int32_t N, int32_t Npad,
+                              float ox, float oy, float oz, float inv_h, int dx, int dy, int dz,
+                              int32_t* keys, int32_t* counts, int32_t* cell_start,
+                              int32_t* cursor, int32_t* scan_tmp, float4* spos, float4* snrm,
+                              cudaStream_t s);
+// centre ordering (a5): coarse Morton bucket counting sort
+cudaError_t launch_centre_order(const int32_t* centre_idx, int64_t M, const float4* cpos,
+                                int32_t N, float ox, float oy, float oz, float inv_h, int dx,
+                                int dy, int dz, int shift, int bits, int32_t* keys,
+                                int32_t* counts, int32_t* starts, int32_t* cursor,
+                                int32_t* scan_tmp, int32_t* order, cudaStream_t s);
+cudaError_t launch_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, int32_t* tmp,
+                                  cudaStream_t s);
+size_t scan_tmp_elems(int64_t n);
+
+}  // namespace spin

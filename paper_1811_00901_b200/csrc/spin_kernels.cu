@@ -1,0 +1,793 @@
+// spin_kernels.cu — sm_100a kernels of the spin-image hot path.
+//
+// Persistent spin kernel: P resident CTAs; each CTA
+// asks the device "master" (one u32 in global memory) for the next chunk of the
+// schedule (the five-step protocol of PAPER.md:262-267 collapsed to one atomicAdd;
+// STATIC takes chunk blockIdx.x), and for every group of G images in the chunk:
+//   a7  loads the G centres (p, n) and folds them into per-centre fp32 constants,
+//       zeroes G images in shared memory (tempSpinImage + init),
+//   a8  streams the cloud through registers (BRUTE: all N points, Alg. 1's inner
+//       loop P:161; CELLS: the grid rows around the group), each thread holding K
+//       points that are reused against all G centres (n-body blocking),
+//   a9  runs the conservative fp32 pair test — support n.nx >= cos_As,
+//       beta window and alpha^2 bound — packing pass bits into a mask,
+//   a10 compacts candidates into a per-warp shared-memory queue and processes them
+//       32 at a time: exact-certified bin decision, shared-memory u32 atomics
+//       (NEAREST ++) or 2^-23 fixed point (BILINEAR),
+//   a11 re-takes any decision fp32 cannot certify in fp64 and then exactly
+//       (spin_exact.cuh),
+//   a12 writes the G images to out[m] in the caller's order (add(spinImages)),
+//   a13 records %globaltimer start/finish and units per CTA (fig:loadim).
+// No tensor cores: the pair test is not a contraction.
+#include <cstdint>
+#include <cfloat>
+#include <cmath>
+
+#include "spin_internal.h"
+#include "spin_exact.cuh"
+
+namespace spin {
+
+constexpr int NT = 256;           // threads per CTA
+constexpr int NWARP = NT / 32;
+constexpr int KP = 4;             // points per thread (register blocking)
+constexpr int CB = 8;             // centres per mask batch: CB * KP = 32 bits
+constexpr int QCAP = 64;          // per-warp candidate ring (power of two, >= 2*32)
+constexpr int ROWCAP = NT;        // CELLS: grid rows staged per batch
+
+static_assert(CB * KP == 32, "mask is one u32");
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// The ONE cell-coordinate function used for binning points and for bounding the
+// visited rows: monotone non-decreasing in x (IEEE sub/mul by a positive constant
+// and floor are monotone), clamped to [0, dim).
+__device__ __forceinline__ int cell_coord(float x, float o, float inv_h, int dim) {
+  float t = __fmul_rn(__fsub_rn(x, o), inv_h);
+  t = fminf(fmaxf(t, 0.0f), (float)(dim - 1));
+  return (int)floorf(t);
+}
+
+// ------------------------------------------------------------------ smem layout
+struct Layout {
+  size_t oA, oB, oP, oN, oM, oImg, oHi, oQ, oRowS, oRowO, total;
+};
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+__host__ __device__ inline Layout make_layout(int G, int W, int mode, int prune) {
+  Layout L;
+  size_t o = 0;
+  L.oA = o; o += 16 * (size_t)G;
+  L.oB = o; o += 16 * (size_t)G;
+  L.oP = o; o += 16 * (size_t)G;
+  L.oN = o; o += 16 * (size_t)G;
+  L.oM = o; o = align16(o + 4 * (size_t)G);
+  const size_t WW = (size_t)W * W;
+  L.oImg = o; o = align16(o + 4 * WW * G);
+  L.oHi = o;
+  if (mode == 1) o = align16(o + 4 * ((WW + 1) / 2) * G);
+  L.oQ = o; o += 8 * (size_t)QCAP * NWARP;
+  L.oRowS = o;
+  L.oRowO = o;
+  if (prune == 1) {
+    o += 4 * ROWCAP;
+    L.oRowO = o;
+    o += 4 * (ROWCAP + 1);
+    o = align16(o);
+  }
+  L.total = o;
+  return L;
+}
+
+// ------------------------------------------------------------------ counters
+struct Ctr {
+  unsigned cand, acc, f64, exact;
+};
+
+// BILINEAR accumulator: 2^-23 fixed point, 32-bit low word + 16-bit carry word
+// packed two bins per u32.  round(w * 2^23) for w in [0,1] is the mantissa of 1 + w.
+__device__ __forceinline__ void add_fixed(uint32_t* lo, uint32_t* hi, int bin, float w,
+                                          int32_t* err) {
+  uint32_t v = __float_as_uint(w + 1.0f) - 0x3f800000u;
+  if (v == 0u) return;
+  uint32_t old = atomicAdd(&lo[bin], v);
+  if (old + v < old) {
+    uint32_t sh = (uint32_t)(bin & 1) * 16u;
+    uint32_t prev = atomicAdd(&hi[bin >> 1], 1u << sh);
+    if (((prev >> sh) & 0xffffu) == 0xffffu) atomicOr(&err[1], 1);
+  }
+}
+
+// ------------------------------------------------------------------ accept path
+// One candidate (centre slot g, point X): certified fp32 decision, fallbacks, splat.
+template <int MODE>
+__device__ __forceinline__ void accept_pair(const KParams& p, const float4 P4, const float4 N4,
+                                            const float4 X4, const float4 NX4, uint32_t* img,
+                                            uint32_t* hi, Ctr& ct) {
+  const int W = p.W;
+  ++ct.cand;
+  const float d0 = X4.x - P4.x, d1 = X4.y - P4.y, d2 = X4.z - P4.z;
+  bool unc = p.no_fast_cert != 0;
+  // support test, inclusive, cosine form (#5)
+  if (p.has_support) {
+    const float s = fmaf(N4.x, NX4.x, fmaf(N4.y, NX4.y, N4.z * NX4.z));
+    const float ds = s - p.c_f;
+    if (ds < -p.Es_a) return;            // certainly rejected
+    if (!(ds > p.Es_a)) unc = true;
+  }
+  int k = 0, l = 0;
+  float uval = 0.f, wval = 0.f;
+  if (p.self_fast && d0 == 0.f && d1 == 0.f && d2 == 0.f && !unc) {
+    // the self pair (and exact duplicates): beta = 0 and q = 0 exactly (#8)
+    if (p.self_k < 0) return;
+    if (MODE == 0) {
+      atomicAdd(&img[p.self_k * W], 1u);
+    } else {
+      add_fixed(img, hi, p.self_k * W, 1.0f - p.self_a, p.err_flags);
+      if (p.self_a > 0.f) add_fixed(img, hi, (p.self_k + 1) * W, p.self_a, p.err_flags);
+    }
+    ++ct.acc;
+    return;
+  }
+  const float be = fmaf(N4.x, d0, fmaf(N4.y, d1, N4.z * d2));       // np_i.(X-P)
+  const float dd = fmaf(d0, d0, fmaf(d1, d1, d2 * d2));              // ||X-P||^2
+  const float q = fmaf(-be, be, dd);                                 // alpha^2
+  uval = p.literal ? (p.Af - be) * p.inv_b : fmaf(-be, p.inv_b, p.Af);
+  wval = q * p.inv_b2;                                               // (alpha/b)^2
+  const float Wm1 = (float)(W - 1);
+  if (!(dd <= p.D2g)) {
+    unc = true;                     // outside the domain of the fp32 bounds: no fp32 verdicts
+  } else if (MODE == 0) {
+    // row k = ceil(u) (or floor): certified when u is farther than Eu from an integer
+    const float uc = fminf(fmaxf(uval, -4.0f), (float)W + 4.0f);
+    const float rr = rintf(uc);
+    const bool ku = !(fabsf(uc - rr) > p.Eu_a);
+    if (!ku) {
+      k = p.floor_bins ? (int)floorf(uc) : (int)ceilf(uc);
+      if (k < 0 || k >= W) return;
+    }
+    // column l = ceil(sqrt(w)) (or floor): certified when w is farther than Ew from
+    // every perfect square (squares are exact in fp32 here)
+    const float v = sqrtf(fmaxf(wval, 0.0f));
+    const float fl = floorf(v);
+    const float dlo = wval - fl * fl, dhi = (fl + 1.0f) * (fl + 1.0f) - wval;
+    bool lu = false;
+    if (wval < -p.Ew_a) l = 0;
+    else if (dlo > p.Ew_a && dhi > p.Ew_a) l = p.floor_bins ? (int)fl : (int)fl + 1;
+    else lu = true;
+    if (!lu && l >= W) return;
+    unc = unc || ku || lu;
+  } else {
+    // BILINEAR region 0 <= u < W-1, w < (W-1)^2  (#12)
+    const bool uu = !(fabsf(uval) > p.Eu_a && fabsf(uval - Wm1) > p.Eu_a);
+    if (!uu && !(uval > 0.f && uval < Wm1)) return;
+    const float lim = Wm1 * Wm1;
+    const bool wu = !(fabsf(wval - lim) > p.Ew_a);
+    if (!wu && !(wval < lim)) return;
+    unc = unc || uu || wu;
+  }
+  if (unc) {
+    ++ct.f64;
+    PairD D;
+    D.p[0] = P4.x; D.p[1] = P4.y; D.p[2] = P4.z;
+    D.n[0] = N4.x; D.n[1] = N4.y; D.n[2] = N4.z;
+    D.x[0] = X4.x; D.x[1] = X4.y; D.x[2] = X4.z;
+    D.nx[0] = NX4.x; D.nx[1] = NX4.y; D.nx[2] = NX4.z;
+    SlowOut r = slow_decide(D, W, p.A, p.b, p.cos_As, p.has_support, p.literal, p.floor_bins,
+                            MODE, ct.exact);
+    if (!r.accept) return;
+    k = r.k;
+    l = r.l;
+  }
+  ++ct.acc;
+  if (MODE == 0) {
+    atomicAdd(&img[k * W + l], 1u);                                  // tempSpinImage[k,l]++
+  } else {
+    const float v = sqrtf(fmaxf(wval, 0.0f));
+    const float fi = fminf(fmaxf(floorf(uval), 0.0f), Wm1 - 1.0f);
+    const float fj = fminf(fmaxf(floorf(v), 0.0f), Wm1 - 1.0f);
+    const float a = fminf(fmaxf(uval - fi, 0.0f), 1.0f);
+    const float c = fminf(fmaxf(v - fj, 0.0f), 1.0f);
+    const int bin = (int)fi * W + (int)fj;
+    add_fixed(img, hi, bin, (1.0f - a) * (1.0f - c), p.err_flags);
+    add_fixed(img, hi, bin + W, a * (1.0f - c), p.err_flags);
+    add_fixed(img, hi, bin + 1, (1.0f - a) * c, p.err_flags);
+    add_fixed(img, hi, bin + W + 1, a * c, p.err_flags);
+  }
+}
+
+// ------------------------------------------------------------------ the kernel
+template <int MODE, int PRUNE, int G>
+__global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__ KParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_chunk;
+  __shared__ int s_nrows, s_total, s_live;
+  __shared__ int s_rng[6];
+  __shared__ unsigned long long s_ctr[5];
+
+  const int W = p.W;
+  const int WW = W * W;
+  const Layout L = make_layout(G, W, MODE, PRUNE);
+  float4* sA = reinterpret_cast<float4*>(smem + L.oA);
+  float4* sB = reinterpret_cast<float4*>(smem + L.oB);
+  float4* sP = reinterpret_cast<float4*>(smem + L.oP);
+  float4* sN = reinterpret_cast<float4*>(smem + L.oN);
+  int* sM = reinterpret_cast<int*>(smem + L.oM);
+  uint32_t* sImg = reinterpret_cast<uint32_t*>(smem + L.oImg);
+  uint32_t* sHi = reinterpret_cast<uint32_t*>(smem + L.oHi);
+  int* sRowS = reinterpret_cast<int*>(smem + L.oRowS);
+  int* sRowO = reinterpret_cast<int*>(smem + L.oRowO);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int2* sQ = reinterpret_cast<int2*>(smem + L.oQ) + warp * QCAP;
+  const int hiWords = (WW + 1) / 2;
+
+  if (tid < 5) s_ctr[tid] = 0ull;
+  const unsigned long long t0 = gtimer();
+  Ctr ct{0, 0, 0, 0};
+  int units_done = 0;
+  unsigned long long visited = 0;
+  bool first = true;
+
+  for (;;) {
+    // ---- a6: request a chunk (PAPER.md:336-342 / 372-377)
+    if (tid == 0) s_chunk = p.is_static ? (first ? (int)blockIdx.x : p.n_chunks)
+                                        : (int)atomicAdd(p.counter, 1u);
+    __syncthreads();
+    const int u = s_chunk;
+    first = false;
+    if (u >= p.n_chunks) break;
+    const int u0 = p.bounds[u], u1 = p.bounds[u + 1];
+    const long long i0 = (long long)u0 * p.unit_images;
+    const long long i1 = min((long long)u1 * p.unit_images, (long long)p.M);
+
+    for (long long g0 = i0; g0 < i1; g0 += G) {
+      const int gcount = (int)min((long long)G, i1 - g0);
+      // ---- a7: group setup (tempSpinImage, init, P = OP[i])
+      if (tid < G) {
+        const int slot = tid;
+        float4 A4 = make_float4(0.f, 0.f, 0.f, 0.f), B4 = make_float4(0.f, 0.f, 0.f, -INFINITY);
+        float4 P4 = make_float4(0.f, 0.f, 0.f, 0.f), N4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        int mm = -1;
+        if (slot < gcount) {
+          const long long ip = g0 + slot;
+          const int m = p.order ? p.order[ip] : (int)ip;
+          const int c = p.centre_idx[m];
+          if (c >= 0 && c < p.N) {
+            P4 = __ldg(&p.cpos[c]);
+            N4 = __ldg(&p.cnrm[c]);
+            const double px = P4.x, py = P4.y, pz = P4.z, nx = N4.x, ny = N4.y, nz = N4.z;
+            const double np = nx * px + ny * py + nz * pz;
+            const double mid = p.mid;
+            const double C = (px * px + py * py + pz * pz) + 2.0 * mid * np + mid * mid;
+            const double Qt = p.Qmax - C + p.Eq_hot + 1e-12 * (fabs(C) + p.Qmax);
+            A4 = make_float4(N4.x, N4.y, N4.z, __double2float_rn(-np - mid));
+            B4 = make_float4(__double2float_rn(-2.0 * (px + mid * nx)),
+                             __double2float_rn(-2.0 * (py + mid * ny)),
+                             __double2float_rn(-2.0 * (pz + mid * nz)), __double2float_ru(Qt));
+            mm = m;
+          } else {
+            atomicOr(&p.err_flags[0], 1);
+            mm = -(m + 2);  // image written as zeros
+          }
+        }
+        sA[slot] = A4;
+        sB[slot] = B4;
+        sP[slot] = P4;
+        sN[slot] = N4;
+        sM[slot] = mm;
+      }
+      for (int i = tid; i < G * WW; i += NT) sImg[i] = 0u;
+      if (MODE == 1)
+        for (int i = tid; i < G * hiWords; i += NT) sHi[i] = 0u;
+      int nrows = 0;
+      if (PRUNE == 1) {
+        __syncthreads();
+        // bounding box of the live centres, grown by R (rounded outward)
+        if (warp == 0) {
+          float lo[3], hi3[3];
+          const bool live = lane < G && sM[lane] >= 0;
+          const float4 P4 = live ? sP[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+          lo[0] = live ? P4.x : INFINITY; lo[1] = live ? P4.y : INFINITY; lo[2] = live ? P4.z : INFINITY;
+          hi3[0] = live ? P4.x : -INFINITY; hi3[1] = live ? P4.y : -INFINITY; hi3[2] = live ? P4.z : -INFINITY;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+              hi3[a] = fmaxf(hi3[a], __shfl_xor_sync(0xffffffffu, hi3[a], o));
+            }
+          }
+          const int anyl = __any_sync(0xffffffffu, live);
+          if (lane == 0) {
+            s_live = anyl;
+            if (anyl) {
+              s_rng[0] = cell_coord(__fsub_rd(lo[0], p.R_up), p.ox, p.inv_h, p.dimx);
+              s_rng[1] = cell_coord(__fadd_ru(hi3[0], p.R_up), p.ox, p.inv_h, p.dimx);
+              s_rng[2] = cell_coord(__fsub_rd(lo[1], p.R_up), p.oy, p.inv_h, p.dimy);
+              s_rng[3] = cell_coord(__fadd_ru(hi3[1], p.R_up), p.oy, p.inv_h, p.dimy);
+              s_rng[4] = cell_coord(__fsub_rd(lo[2], p.R_up), p.oz, p.inv_h, p.dimz);
+              s_rng[5] = cell_coord(__fadd_ru(hi3[2], p.R_up), p.oz, p.inv_h, p.dimz);
+            }
+          }
+        }
+        __syncthreads();
+        if (s_live) nrows = (s_rng[3] - s_rng[2] + 1) * (s_rng[5] - s_rng[4] + 1);
+      }
+      __syncthreads();
+
+      // ---- a8-a10: stream points, pair test, compact, accept
+      unsigned qhead = 0, qtail = 0;
+      uint32_t* img_base = sImg;
+      auto process_entry = [&](int2 e) {
+        const int gs = e.y;
+        const float4 P4 = sP[gs], N4 = sN[gs];
+        const float4 X4 = __ldg(&p.pos[e.x]), NX4 = __ldg(&p.nrm[e.x]);
+        accept_pair<MODE>(p, P4, N4, X4, NX4, img_base + gs * WW, sHi + gs * hiWords, ct);
+      };
+      auto run_tile = [&](const int (&j)[KP]) {
+        float x[KP], y[KP], z[KP], xx[KP], nx[KP], ny[KP], nz[KP];
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          const float4 a = __ldg(&p.pos[j[k]]);
+          const float4 b = __ldg(&p.nrm[j[k]]);
+          x[k] = a.x; y[k] = a.y; z[k] = a.z; xx[k] = a.w;
+          nx[k] = b.x; ny[k] = b.y; nz[k] = b.z;
+        }
+        const float c_test = p.c_test, h_test = p.h_test;
+#pragma unroll 1
+        for (int cb = 0; cb < G; cb += CB) {
+          unsigned mask = 0u;
+#pragma unroll
+          for (int c = 0; c < CB; ++c) {
+            const float4 A4 = sA[cb + c];
+            const float4 B4 = sB[cb + c];
+#pragma unroll
+            for (int k = 0; k < KP; ++k) {
+              // support n.nx; beta'' = n.x - n.p - mid;
+              // q'' = |x|^2 - 2(p + mid n).x - beta''^2 = q - C
+              const float s = fmaf(A4.x, nx[k], fmaf(A4.y, ny[k], A4.z * nz[k]));
+              const float be = fmaf(A4.x, x[k], fmaf(A4.y, y[k], fmaf(A4.z, z[k], A4.w)));
+              const float t = fmaf(B4.x, x[k], fmaf(B4.y, y[k], fmaf(B4.z, z[k], xx[k])));
+              const float q = fmaf(-be, be, t);
+              const bool pass = (s >= c_test) & (fabsf(be) <= h_test) & (q <= B4.w);
+              if (pass) mask |= 1u << (c * KP + k);
+            }
+          }
+          // compaction: each round every lane with bits left enqueues its lowest one
+          unsigned m = mask;
+          while (__any_sync(0xffffffffu, m != 0u)) {
+            const unsigned ball = __ballot_sync(0xffffffffu, m != 0u);
+            if (m) {
+              const int bit = __ffs(m) - 1;
+              m &= m - 1u;
+              const int kk = bit & (KP - 1);
+              const int jj = kk == 0 ? j[0] : kk == 1 ? j[1] : kk == 2 ? j[2] : j[3];
+              const unsigned slot = (qtail + __popc(ball & lanemask_lt())) & (QCAP - 1);
+              sQ[slot] = make_int2(jj, cb + (bit >> 2));
+            }
+            qtail += __popc(ball);
+            if (qtail - qhead >= 32u) {
+              __syncwarp();
+              const int2 e = sQ[(qhead + lane) & (QCAP - 1)];
+              __syncwarp();
+              qhead += 32u;
+              process_entry(e);
+            }
+          }
+        }
+      };
+
+      if (PRUNE == 0) {
+        for (int t = 0; t < p.n_tiles; ++t) {
+          const int base = t * (NT * KP) + tid;
+          int j[KP];
+#pragma unroll
+          for (int k = 0; k < KP; ++k) j[k] = base + k * NT;
+          run_tile(j);
+        }
+      } else {
+        // rows of the visited box, batched ROWCAP at a time
+        const int cx0 = s_rng[0], cx1 = s_rng[1], cy0 = s_rng[2], cy1 = s_rng[3], cz0 = s_rng[4];
+        const int ny = cy1 - cy0 + 1;
+        for (int rb = 0; rb < nrows; rb += ROWCAP) {
+          const int nb = min(ROWCAP, nrows - rb);
+          int len = 0, start = 0;
+          if (tid < nb) {
+            const int row = rb + tid;
+            const int cz = cz0 + row / ny, cy = cy0 + row % ny;
+            const int base = (cz * p.dimy + cy) * p.dimx;
+            start = p.cell_start[base + cx0];
+            len = p.cell_start[base + cx1 + 1] - start;
+          }
+          // block exclusive scan of len over NT threads
+          int v = len;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int n = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += n;
+          }
+          __shared__ int s_wsum[NWARP];
+          if (lane == 31) s_wsum[warp] = v;
+          __syncthreads();
+          if (warp == 0) {
+            int ws = lane < NWARP ? s_wsum[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < NWARP; o <<= 1) {
+              const int n = __shfl_up_sync(0xffffffffu, ws, o);
+              if (lane >= o) ws += n;
+            }
+            if (lane < NWARP) s_wsum[lane] = ws;
+            if (lane == NWARP - 1) s_total = ws;
+          }
+          __syncthreads();
+          const int excl = v - len + (warp > 0 ? s_wsum[warp - 1] : 0);
+          if (tid < nb) {
+            sRowS[tid] = start;
+            sRowO[tid] = excl;
+          }
+          if (tid == 0) sRowO[nb] = s_total;
+          __syncthreads();
+          const int T = s_total;
+          if (tid == 0) {
+            int live = 0;
+            for (int g = 0; g < G; ++g) live += sM[g] >= 0;
+            visited += (unsigned long long)T * live;
+          }
+          for (int f0 = 0; f0 < T; f0 += NT * KP) {
+            int j[KP];
+#pragma unroll
+            for (int k = 0; k < KP; ++k) {
+              const int f = f0 + tid + k * NT;
+              if (f < T) {
+                int lo = 0, hi = nb - 1;   // largest r with sRowO[r] <= f
+                while (lo < hi) {
+                  const int mid = (lo + hi + 1) >> 1;
+                  if (sRowO[mid] <= f) lo = mid; else hi = mid - 1;
+                }
+                j[k] = sRowS[lo] + (f - sRowO[lo]);
+              } else {
+                j[k] = p.N;  // sentinel
+              }
+            }
+            run_tile(j);
+          }
+          __syncthreads();
+        }
+      }
+      // drain this warp's queue
+      while (qtail != qhead) {
+        const unsigned cnt = min(32u, qtail - qhead);
+        int2 e = make_int2(0, 0);
+        __syncwarp();
+        if ((unsigned)lane < cnt) e = sQ[(qhead + lane) & (QCAP - 1)];
+        __syncwarp();
+        qhead += cnt;
+        if ((unsigned)lane < cnt) process_entry(e);
+      }
+      __syncthreads();
+      // ---- a12: write the images back in the caller's order
+      for (int i = tid; i < G * WW; i += NT) {
+        const int slot = i / WW;
+        const int e = i - slot * WW;
+        int mm = sM[slot];
+        if (mm == -1) continue;
+        float val = 0.0f;
+        if (mm < -1) {
+          mm = -(mm + 2);
+        } else if (MODE == 0) {
+          const uint32_t cnt = sImg[i];
+          if (cnt >= (1u << 24)) atomicOr(&p.err_flags[1], 1);
+          val = (float)cnt;
+        } else {
+          const uint32_t h = (sHi[slot * hiWords + (e >> 1)] >> ((e & 1) * 16)) & 0xffffu;
+          const double fx = (double)h * 4294967296.0 + (double)sImg[i];
+          val = (float)(fx * (1.0 / 8388608.0));
+        }
+        __stcs(&p.out[(long long)mm * WW + e], val);
+      }
+      __syncthreads();
+    }
+    units_done += u1 - u0;
+  }
+
+  // ---- a13: instrumentation
+  const unsigned long long t1 = gtimer();
+  atomicAdd(&s_ctr[0], (unsigned long long)ct.cand);
+  atomicAdd(&s_ctr[1], (unsigned long long)ct.acc);
+  atomicAdd(&s_ctr[2], (unsigned long long)ct.f64);
+  atomicAdd(&s_ctr[3], (unsigned long long)ct.exact);
+  if (tid == 0) atomicAdd(&s_ctr[4], visited);
+  __syncthreads();
+  if (tid == 0) {
+    atomicAdd(&p.stats[ST_CAND], s_ctr[0]);
+    atomicAdd(&p.stats[ST_ACC], s_ctr[1]);
+    atomicAdd(&p.stats[ST_F64], s_ctr[2]);
+    atomicAdd(&p.stats[ST_EXACT], s_ctr[3]);
+    atomicAdd(&p.stats[ST_VISITED], s_ctr[4]);
+    p.cta_t0[blockIdx.x] = t0;
+    p.cta_t1[blockIdx.x] = t1;
+    p.cta_units[blockIdx.x] = units_done;
+  }
+}
+
+// ------------------------------------------------------------------ dispatch
+template <int MODE, int PRUNE>
+static const void* kernel_ptr(int G) {
+  switch (G) {
+    case 8: return (const void*)spin_persistent<MODE, PRUNE, 8>;
+    case 16: return (const void*)spin_persistent<MODE, PRUNE, 16>;
+    default: return (const void*)spin_persistent<MODE, PRUNE, 32>;
+  }
+}
+static const void* kernel_for(int mode, int prune, int G) {
+  if (mode == 0) return prune == 0 ? kernel_ptr<0, 0>(G) : kernel_ptr<0, 1>(G);
+  return prune == 0 ? kernel_ptr<1, 0>(G) : kernel_ptr<1, 1>(G);
+}
+
+LaunchCfg choose_launch(int W, int mode, int prune) {
+  // images live in shared memory: NEAREST 4 B/bin, BILINEAR 6 B/bin; keep the image
+  // block <= 96 KB so that two CTAs fit on an SM (227 KB), else allow one CTA.
+  const size_t per_img = (size_t)W * W * (mode == 0 ? 4 : 6);
+  int G = 32;
+  while (G > 8 && per_img * G > 96 * 1024) G >>= 1;
+  LaunchCfg lc;
+  lc.G = G;
+  lc.threads = NT;
+  lc.smem = make_layout(G, W, mode, prune).total;
+  return lc;
+}
+
+int occupancy_blocks(const LaunchCfg& lc, int W, int mode, int prune) {
+  const void* f = kernel_for(mode, prune, lc.G);
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.smem);
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, lc.threads, lc.smem) != cudaSuccess)
+    return 0;
+  (void)W;
+  return nb;
+}
+
+cudaError_t launch_spin(const LaunchCfg& lc, int mode, int prune, int grid, const KParams& p,
+                        cudaStream_t s) {
+  const void* f = kernel_for(mode, prune, lc.G);
+  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.smem);
+  if (e != cudaSuccess) return e;
+  void* args[] = {(void*)&p};
+  return cudaLaunchKernel(f, dim3(grid), dim3(lc.threads), args, lc.smem, s);
+}
+
+// ------------------------------------------------------------------ a1: relayout + validation
+__device__ __forceinline__ int float_flip(float f) {
+  int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+
+__global__ void k_relayout(const float* __restrict__ pts, const float* __restrict__ nrm, int64_t N,
+                           int64_t Npad, float4* __restrict__ pos, float4* __restrict__ nrm4,
+                           int32_t* bad, int* absmax_bits, int* aabb_bits) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= Npad) return;
+  if (j >= N) {
+    pos[j] = make_float4(0.f, 0.f, 0.f, INFINITY);   // sentinel: |x|^2 = +inf never passes
+    nrm4[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  const float x = pts[3 * j], y = pts[3 * j + 1], z = pts[3 * j + 2];
+  const float a = nrm[3 * j], b = nrm[3 * j + 1], c = nrm[3 * j + 2];
+  const double n2 = (double)a * a + (double)b * b + (double)c * c;
+  const bool ok = isfinite(x) && isfinite(y) && isfinite(z) && isfinite(a) && isfinite(b) &&
+                  isfinite(c) && n2 >= 0.999 * 0.999 && n2 <= 1.001 * 1.001;
+  if (!ok) atomicMin(bad, (int32_t)min(j, (int64_t)0x7fffffff));
+  const double xx = (double)x * x + (double)y * y + (double)z * z;
+  pos[j] = make_float4(x, y, z, __double2float_rn(xx));
+  nrm4[j] = make_float4(a, b, c, 0.f);
+  const float r = __double2float_ru(sqrt(xx));
+  atomicMax(absmax_bits, __float_as_int(ok ? r : 0.f));
+  if (ok) {
+    atomicMin(&aabb_bits[0], float_flip(x));
+    atomicMin(&aabb_bits[1], float_flip(y));
+    atomicMin(&aabb_bits[2], float_flip(z));
+    atomicMax(&aabb_bits[3], float_flip(x));
+    atomicMax(&aabb_bits[4], float_flip(y));
+    atomicMax(&aabb_bits[5], float_flip(z));
+  }
+}
+
+cudaError_t launch_relayout(const float* pts, const float* nrm, int64_t N, int64_t Npad,
+                            float4* pos, float4* nrm4, int32_t* bad, float* absmax, float* aabb,
+                            cudaStream_t s) {
+  const int tb = 256;
+  const int64_t nb = (Npad + tb - 1) / tb;
+  k_relayout<<<(unsigned)nb, tb, 0, s>>>(pts, nrm, N, Npad, pos, nrm4, bad, (int*)absmax,
+                                         (int*)aabb);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ exclusive scan (3 phases)
+constexpr int SCAN_TB = 1024, SCAN_IPT = 4, SCAN_TILE = SCAN_TB * SCAN_IPT;
+
+__device__ int block_excl_scan(int v, int* s_w, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += n;
+  }
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += n;
+    }
+    s_w[lane] = w;
+  }
+  __syncthreads();
+  total = s_w[(blockDim.x >> 5) - 1];
+  const int r = x - v + (warp > 0 ? s_w[warp - 1] : 0);
+  __syncthreads();
+  return r;
+}
+
+__global__ void k_scan_tiles(const int32_t* in, int32_t* out, int64_t n, int32_t* tile_sums) {
+  __shared__ int s_w[32];
+  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_IPT;
+  int v[SCAN_IPT], sum = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_IPT; ++i) {
+    v[i] = (base + i < n) ? in[base + i] : 0;
+    sum += v[i];
+  }
+  int total;
+  int run = block_excl_scan(sum, s_w, total);
+#pragma unroll
+  for (int i = 0; i < SCAN_IPT; ++i) {
+    if (base + i < n) out[base + i] = run;
+    run += v[i];
+  }
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+__global__ void k_scan_sums(int32_t* sums, int nt, int32_t* out_total) {
+  __shared__ int s_w[32];
+  int carry = 0;
+  for (int b0 = 0; b0 < nt; b0 += SCAN_TB) {
+    const int i = b0 + threadIdx.x;
+    const int v = i < nt ? sums[i] : 0;
+    int total;
+    const int r = block_excl_scan(v, s_w, total);
+    if (i < nt) sums[i] = r + carry;
+    carry += total;
+  }
+  if (threadIdx.x == 0) *out_total = carry;
+}
+__global__ void k_scan_add(int32_t* out, int64_t n, const int32_t* sums) {
+  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  const int add = sums[blockIdx.x];
+  for (int i = threadIdx.x; i < SCAN_TILE; i += blockDim.x)
+    if (base + i < n) out[base + i] += add;
+}
+
+size_t scan_tmp_elems(int64_t n) { return (size_t)((n + SCAN_TILE - 1) / SCAN_TILE) + 1; }
+
+// out[0..n] = exclusive scan of in[0..n), out[n] = total
+cudaError_t launch_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, int32_t* tmp,
+                                  cudaStream_t s) {
+  const int nt = (int)((n + SCAN_TILE - 1) / SCAN_TILE);
+  if (nt == 0) return cudaMemsetAsync(out, 0, sizeof(int32_t), s);
+  k_scan_tiles<<<nt, SCAN_TB, 0, s>>>(in, out, n, tmp);
+  k_scan_sums<<<1, SCAN_TB, 0, s>>>(tmp, nt, out + n);
+  k_scan_add<<<nt, SCAN_TB, 0, s>>>(out, n, tmp);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a4: CELLS grid build
+__global__ void k_cell_keys(const float4* __restrict__ pos, int32_t N, float ox, float oy, float oz,
+                            float inv_h, int dx, int dy, int dz, int32_t* keys, int32_t* counts) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const float4 a = pos[j];
+  const int cx = cell_coord(a.x, ox, inv_h, dx);
+  const int cy = cell_coord(a.y, oy, inv_h, dy);
+  const int cz = cell_coord(a.z, oz, inv_h, dz);
+  const int key = (cz * dy + cy) * dx + cx;
+  keys[j] = key;
+  atomicAdd(&counts[key], 1);
+}
+__global__ void k_cell_scatter(const float4* __restrict__ pos, const float4* __restrict__ nrm,
+                               int32_t N, int32_t Npad, const int32_t* keys,
+                               const int32_t* cell_start, int32_t* cursor, float4* spos,
+                               float4* snrm) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= Npad) return;
+  if (j >= N) {
+    spos[j] = make_float4(0.f, 0.f, 0.f, INFINITY);
+    snrm[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  const int key = keys[j];
+  const int dst = cell_start[key] + atomicAdd(&cursor[key], 1);
+  spos[dst] = pos[j];
+  snrm[dst] = nrm[j];
+}
+
+cudaError_t launch_cell_build(const float4* pos, const float4* nrm, int32_t N, int32_t Npad,
+                              float ox, float oy, float oz, float inv_h, int dx, int dy, int dz,
+                              int32_t* keys, int32_t* counts, int32_t* cell_start, int32_t* cursor,
+                              int32_t* scan_tmp, float4* spos, float4* snrm, cudaStream_t s) {
+  const int64_t ncells = (int64_t)dx * dy * dz;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(counts, 0, ncells * sizeof(int32_t), s)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(cursor, 0, ncells * sizeof(int32_t), s)) != cudaSuccess) return e;
+  const int tb = 256;
+  k_cell_keys<<<(N + tb - 1) / tb, tb, 0, s>>>(pos, N, ox, oy, oz, inv_h, dx, dy, dz, keys, counts);
+  if ((e = launch_exclusive_scan(counts, cell_start, ncells, scan_tmp, s)) != cudaSuccess) return e;
+  k_cell_scatter<<<(Npad + tb - 1) / tb, tb, 0, s>>>(pos, nrm, N, Npad, keys, cell_start, cursor,
+                                                     spos, snrm);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a5: centre ordering
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 10 bits -> every third bit
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000ffu;
+  v = (v | (v << 8)) & 0x0300f00fu;
+  v = (v | (v << 4)) & 0x030c30c3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+__global__ void k_centre_keys(const int32_t* centre_idx, int64_t M, const float4* cpos, int32_t N,
+                              float ox, float oy, float oz, float inv_h, int dx, int dy, int dz,
+                              int shift, int32_t* keys, int32_t* counts) {
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  const int c = centre_idx[m];
+  int key = 0;
+  if (c >= 0 && c < N) {
+    const float4 a = cpos[c];
+    const uint32_t cx = (uint32_t)cell_coord(a.x, ox, inv_h, dx) >> shift;
+    const uint32_t cy = (uint32_t)cell_coord(a.y, oy, inv_h, dy) >> shift;
+    const uint32_t cz = (uint32_t)cell_coord(a.z, oz, inv_h, dz) >> shift;
+    key = (int)(spread3(cx) | (spread3(cy) << 1) | (spread3(cz) << 2));
+  }
+  keys[m] = key;
+  atomicAdd(&counts[key], 1);
+}
+__global__ void k_centre_scatter(int64_t M, const int32_t* keys, const int32_t* starts,
+                                 int32_t* cursor, int32_t* order) {
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  const int key = keys[m];
+  order[starts[key] + atomicAdd(&cursor[key], 1)] = (int32_t)m;
+}
+
+cudaError_t launch_centre_order(const int32_t* centre_idx, int64_t M, const float4* cpos, int32_t N,
+                                float ox, float oy, float oz, float inv_h, int dx, int dy, int dz,
+                                int shift, int bits, int32_t* keys, int32_t* counts,
+                                int32_t* starts, int32_t* cursor, int32_t* scan_tmp,
+                                int32_t* order, cudaStream_t s) {
+  const int64_t nb = (int64_t)1 << (3 * bits);
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(counts, 0, nb * sizeof(int32_t), s)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(cursor, 0, nb * sizeof(int32_t), s)) != cudaSuccess) return e;
+  const int tb = 256;
+  const unsigned g = (unsigned)((M + tb - 1) / tb);
+  k_centre_keys<<<g, tb, 0, s>>>(centre_idx, M, cpos, N, ox, oy, oz, inv_h, dx, dy, dz, shift,
+                                 keys, counts);
+  if ((e = launch_exclusive_scan(counts, starts, nb, scan_tmp, s)) != cudaSuccess) return e;
+  k_centre_scatter<<<g, tb, 0, s>>>(M, keys, starts, cursor, order);
+  return cudaGetLastError();
+}
+
+}  // namespace spin

@@ -1,0 +1,233 @@
+"""Thin ctypes binding of libspin (include/spin.h) — argument marshalling only.
+
+Every step of the spin-image path runs inside libspin's sm_100a kernels; this module
+converts tensors / arrays to pointers and statuses to exceptions.  There is no CPU
+fallback: if libspin.so is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libspin.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libspin.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'`")
+_lib = C.CDLL(LIB_PATH)
+
+STATIC, SS, GSS, FAC = 0, 1, 2, 3
+NEAREST, BILINEAR = 0, 1
+BRUTE, CELLS = 0, 1
+F_LITERAL_HALF_WIDTH, F_FLOOR_BINS, F_NO_SORT, F_NO_FAST_CERT = 0x1, 0x2, 0x4, 0x8
+SCHEDULES = {"STATIC": STATIC, "SS": SS, "GSS": GSS, "FAC": FAC}
+MODES = {"nearest": NEAREST, "bilinear": BILINEAR}
+PRUNES = {"brute": BRUTE, "cells": CELLS}
+STATUS = {0: "SPIN_OK", 1: "SPIN_E_INVAL", 2: "SPIN_E_RANGE", 3: "SPIN_E_INPUT",
+          4: "SPIN_E_NOMEM", 5: "SPIN_E_CUDA", 6: "SPIN_E_OVERFLOW"}
+
+
+class ChunkParams(C.Structure):
+    _fields_ = [("P", C.c_int32), ("unit", C.c_int32), ("gss_min_chunk", C.c_int32),
+                ("fac_divisor", C.c_int32), ("flags", C.c_uint32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("elapsed_ms", C.c_double), ("grid_build_ms", C.c_double),
+                ("pairs_visited", C.c_int64), ("pairs_candidate", C.c_int64),
+                ("pairs_accepted", C.c_int64), ("fp64_fallbacks", C.c_int64),
+                ("exact_fallbacks", C.c_int64), ("P", C.c_int32), ("G", C.c_int32),
+                ("n_units", C.c_int32), ("n_chunks", C.c_int32),
+                ("h_cta_start_ns", C.POINTER(C.c_uint64)), ("h_cta_end_ns", C.POINTER(C.c_uint64)),
+                ("h_cta_units", C.POINTER(C.c_int32)), ("cta_capacity", C.c_int32)]
+
+
+_vp = C.c_void_p
+_lib.spin_create.argtypes = [_vp, _vp, C.c_int64, _vp, C.POINTER(_vp)]
+_lib.spin_load_cloud.argtypes = [_vp, _vp, _vp, C.c_int64, _vp]
+_lib.spin_generate.argtypes = [_vp, _vp, C.c_int64, C.c_int32, C.c_double, C.c_double, C.c_int,
+                               C.POINTER(ChunkParams), C.c_int, C.c_int, _vp, C.POINTER(Stats), _vp]
+_lib.spin_generate_host.argtypes = _lib.spin_generate.argtypes
+_lib.spin_chunk_sequence.argtypes = [C.c_int, C.c_int64, C.c_int32, C.POINTER(ChunkParams),
+                                     C.POINTER(C.c_int64), C.c_int64, C.POINTER(C.c_int64)]
+_lib.spin_region_radius.argtypes = [C.c_int32, C.c_double, C.c_int, C.c_uint32]
+_lib.spin_region_radius.restype = C.c_double
+_lib.spin_cos_from_degrees.argtypes = [C.c_double]
+_lib.spin_cos_from_degrees.restype = C.c_double
+_lib.spin_default_P.argtypes = [C.c_int32, C.c_int, C.c_int]
+_lib.spin_default_P.restype = C.c_int32
+_lib.spin_destroy.argtypes = [_vp]
+_lib.spin_last_error.restype = C.c_char_p
+_lib.spin_abi_version.restype = C.c_int32
+for _f in ("spin_create", "spin_load_cloud", "spin_generate", "spin_generate_host", "spin_chunk_sequence"):
+    getattr(_lib, _f).restype = C.c_int
+
+EXPORTS = ["spin_create", "spin_load_cloud", "spin_generate", "spin_generate_host",
+           "spin_chunk_sequence", "spin_region_radius", "spin_cos_from_degrees", "spin_default_P",
+           "spin_destroy", "spin_last_error", "spin_abi_version"]
+
+
+class SpinError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _check(st: int):
+    if st != 0:
+        raise SpinError(st, (_lib.spin_last_error() or b"").decode())
+
+
+def _enum(v, table):
+    return table[v] if isinstance(v, str) else int(v)
+
+
+def _ptr(t):
+    """Device or host pointer of a torch tensor or numpy array (must be contiguous)."""
+    if isinstance(t, np.ndarray):
+        assert t.flags["C_CONTIGUOUS"]
+        return t.ctypes.data
+    assert t.is_contiguous()
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_stream().cuda_stream
+        return None
+    return getattr(stream, "cuda_stream", stream)
+
+
+def abi_version() -> int:
+    return _lib.spin_abi_version()
+
+
+def cos_from_degrees(deg: float) -> float:
+    return _lib.spin_cos_from_degrees(float(deg))
+
+
+def region_radius(W: int, b: float, mode="nearest", flags: int = 0) -> float:
+    return _lib.spin_region_radius(int(W), float(b), _enum(mode, MODES), int(flags))
+
+
+def default_P(W: int, mode="nearest", prune="brute") -> int:
+    return _lib.spin_default_P(int(W), _enum(mode, MODES), _enum(prune, PRUNES))
+
+
+def chunk_sequence(schedule, n_units: int, P: int, gss_min_chunk: int = 0, fac_divisor: int = 0):
+    """Chunk boundaries [0, b1, ..., n_units] of a schedule (host-only; spin_chunk_sequence)."""
+    cp = ChunkParams(0, 0, gss_min_chunk, fac_divisor, 0)
+    n = C.c_int64(0)
+    st = _lib.spin_chunk_sequence(_enum(schedule, SCHEDULES), n_units, P, C.byref(cp), None, 0, C.byref(n))
+    if st not in (0, 2):
+        _check(st)
+    buf = (C.c_int64 * (n.value + 1))()
+    _check(_lib.spin_chunk_sequence(_enum(schedule, SCHEDULES), n_units, P, C.byref(cp), buf,
+                                    n.value + 1, C.byref(n)))
+    return list(buf)
+
+
+def _stats_dict(s: Stats, t0=None, t1=None, un=None):
+    d = {f: getattr(s, f) for f, _ in Stats._fields_ if not f.startswith("h_cta") and f != "cta_capacity"}
+    if t0 is not None:
+        d["cta_start_ns"] = np.asarray(t0)
+        d["cta_end_ns"] = np.asarray(t1)
+        d["cta_units"] = np.asarray(un)
+    return d
+
+
+class SpinEngine:
+    """A libspin handle: the oriented point cloud resident in HBM (spin_create)."""
+
+    def __init__(self, points, normals, stream=None):
+        n = int(points.shape[0])
+        assert tuple(points.shape) == (n, 3) and tuple(normals.shape) == (n, 3)
+        h = _vp()
+        _check(_lib.spin_create(_ptr(points), _ptr(normals), n, _stream(stream), C.byref(h)))
+        self._h = h
+        self.N = n
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.spin_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load_cloud(self, points, normals, stream=None):
+        n = int(points.shape[0])
+        _check(_lib.spin_load_cloud(self._h, _ptr(points), _ptr(normals), n, _stream(stream)))
+        self.N = n
+
+    @staticmethod
+    def _params(P, unit, gss_min_chunk, fac_divisor, flags):
+        return ChunkParams(int(P), int(unit), int(gss_min_chunk), int(fac_divisor), int(flags))
+
+    def generate(self, centre_idx, W, b, cos_As, schedule="STATIC", mode="nearest", prune="brute",
+                 P=0, unit=0, gss_min_chunk=0, fac_divisor=0, flags=0, out=None, stats=False,
+                 cta_capacity=0, stream=None):
+        """Images for device int32 centre_idx [M] into a device fp32 [M, W, W] tensor."""
+        import torch
+        M = int(centre_idx.shape[0])
+        assert centre_idx.dtype == torch.int32 and centre_idx.is_cuda
+        if out is None:
+            out = torch.empty((M, W, W), dtype=torch.float32, device=centre_idx.device)
+        cp = self._params(P, unit, gss_min_chunk, fac_divisor, flags)
+        st = Stats()
+        t0 = t1 = un = None
+        if stats and cta_capacity:
+            t0 = (C.c_uint64 * cta_capacity)()
+            t1 = (C.c_uint64 * cta_capacity)()
+            un = (C.c_int32 * cta_capacity)()
+            st.h_cta_start_ns = C.cast(t0, C.POINTER(C.c_uint64))
+            st.h_cta_end_ns = C.cast(t1, C.POINTER(C.c_uint64))
+            st.h_cta_units = C.cast(un, C.POINTER(C.c_int32))
+            st.cta_capacity = cta_capacity
+        _check(_lib.spin_generate(self._h, _ptr(centre_idx) if M else None, M, int(W), float(b),
+                                  float(cos_As), _enum(schedule, SCHEDULES), C.byref(cp),
+                                  _enum(mode, MODES), _enum(prune, PRUNES),
+                                  _ptr(out) if M else None, C.byref(st) if stats else None,
+                                  _stream(stream)))
+        if stats:
+            return out, _stats_dict(st, t0, t1, un)
+        return out
+
+    def generate_host(self, centre_idx: np.ndarray, W, b, cos_As, schedule="STATIC",
+                      mode="nearest", prune="brute", P=0, unit=0, gss_min_chunk=0,
+                      fac_divisor=0, flags=0, out: np.ndarray | None = None, stats=False,
+                      stream=None):
+        """spin_generate_host: host int32 centres in, host fp32 [M, W, W] images out."""
+        centre_idx = np.ascontiguousarray(centre_idx, dtype=np.int32)
+        M = int(centre_idx.shape[0])
+        if out is None:
+            out = np.empty((M, W, W), np.float32)
+        cp = self._params(P, unit, gss_min_chunk, fac_divisor, flags)
+        st = Stats()
+        _check(_lib.spin_generate_host(self._h, _ptr(centre_idx) if M else None, M, int(W),
+                                       float(b), float(cos_As), _enum(schedule, SCHEDULES),
+                                       C.byref(cp), _enum(mode, MODES), _enum(prune, PRUNES),
+                                       _ptr(out) if M else None, C.byref(st) if stats else None,
+                                       _stream(stream)))
+        if stats:
+            return out, _stats_dict(st)
+        return out
+
+
+def generate(points, normals, centre_idx, W, b, cos_As, **kw):
+    """One-shot convenience: create a handle, generate, destroy."""
+    eng = SpinEngine(points, normals)
+    try:
+        return eng.generate(centre_idx, W, b, cos_As, **kw)
+    finally:
+        eng.close()
+
+
+NO_SUPPORT = -math.inf

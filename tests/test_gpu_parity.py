@@ -1,0 +1,369 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element.
+
+NEAREST must be bit-exact; BILINEAR within the north-star tolerance (per-image rel
+L1 <= 1e-5, per-bin <= 1e-4 x contributing points).  Inputs are the seeded
+generators of synth/clouds.py; expected values come only from oracle/.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import spin_oracle as O
+from synth import clouds
+from parity_util import assert_bilinear_close, assert_nearest_exact
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    if not t.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return t
+
+
+@pytest.fixture(scope="module")
+def spin(torch):
+    from paper_1811_00901_b200 import spin as s
+    return s
+
+
+def _dev(torch, a, dtype=None):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda")
+
+
+def run_gpu(spin, torch, pts, Nn, cen, W, b, c, mode, prune="brute", stats=False, **kw):
+    eng = spin.SpinEngine(_dev(torch, pts), _dev(torch, Nn))
+    try:
+        r = eng.generate(_dev(torch, np.asarray(cen, np.int32)), W, b, c, mode=mode, prune=prune,
+                         stats=stats, **kw)
+        torch.cuda.synchronize()
+        if stats:
+            return r[0].cpu().numpy(), r[1]
+        return r.cpu().numpy()
+    finally:
+        eng.close()
+
+
+def oracle(P, Nn, cen, W, b, c, mode, flags=0, cells=False):
+    st = {}
+    f = O.generate_cells if cells else O.generate
+    img = f(P, Nn, cen, W, b, c, O.NEAREST if mode == "nearest" else O.BILINEAR, flags, stats=st)
+    return img, st
+
+
+def check(gpu, ora, st, mode, what):
+    if mode == "nearest":
+        assert_nearest_exact(gpu, ora, what)
+    else:
+        assert_bilinear_close(gpu, ora, np.stack(st["contributors"]), what)
+
+
+# ------------------------------------------------------------------ hand-worked goldens
+
+def _gold(name):
+    g = json.load(open(os.path.join(GOLD, name)))
+    return g, np.asarray(g["points"], np.float32), np.asarray(g["normals"], np.float32)
+
+
+def test_x1_goldens(spin, torch):
+    g, P, Nn = _gold("x1.json")
+    for mode in ("nearest", "bilinear"):
+        for flags in (0, spin.F_NO_FAST_CERT):
+            img = run_gpu(spin, torch, P, Nn, [0], g["W"], g["b"], -math.inf, mode, flags=flags)[0]
+            np.testing.assert_array_equal(img, np.asarray(g[mode], np.float32), err_msg=f"{mode} {flags}")
+
+
+def test_x2_x3_x4_goldens(spin, torch):
+    g, P, Nn = _gold("x2.json")
+    img = run_gpu(spin, torch, P, Nn, [0], g["W"], g["b"], -math.inf, "nearest")[0]
+    np.testing.assert_array_equal(img, g["nearest_scaled"])
+    img = run_gpu(spin, torch, P, Nn, [0], g["W"], g["b"], -math.inf, "nearest",
+                  flags=spin.F_LITERAL_HALF_WIDTH)[0]
+    np.testing.assert_array_equal(img, g["nearest_literal"])
+    g, P, Nn = _gold("x3.json")
+    img = run_gpu(spin, torch, P, Nn, [0], g["W"], g["b"], -math.inf, "nearest")[0]
+    np.testing.assert_array_equal(img, g["nearest"])
+    g, P, Nn = _gold("x4.json")
+    img = run_gpu(spin, torch, P, Nn, [0], g["W"], g["b"], 0.0, "nearest")[0]
+    np.testing.assert_array_equal(img, g["cos_zero"])
+    img = run_gpu(spin, torch, P, Nn, [0], g["W"], g["b"], math.cos(math.pi / 2), "nearest")[0]
+    np.testing.assert_array_equal(img, g["cos_fl_half_pi"])
+
+
+# ------------------------------------------------------------------ seeded clouds
+
+@pytest.mark.parametrize("mode", ["nearest", "bilinear"])
+def test_config1_full(spin, torch, mode):
+    """Config 1 in full (N = M = 2000, W=8, b=0.05, 60 deg), STATIC, brute force."""
+    cfg = clouds.CONFIGS[1]
+    P, Nn = clouds.make_cloud(1)
+    cen = clouds.make_centres(1, cfg["N"])
+    gpu = run_gpu(spin, torch, P, Nn, cen, cfg["W"], cfg["b"], cfg["cos_As"], mode)
+    ora, st = oracle(P, Nn, cen, cfg["W"], cfg["b"], cfg["cos_As"], mode)
+    check(gpu, ora, st, mode, f"C1 {mode}")
+
+
+@pytest.mark.parametrize("mode", ["nearest", "bilinear"])
+@pytest.mark.parametrize("N,M", [(5000, 300), (1, 1), (1023, 37), (1025, 70)])
+def test_bumpy_ragged(spin, torch, mode, N, M):
+    """Several 1024-point tiles plus a ragged tail; partial groups; W=16, b=0.02, 60 deg."""
+    P, Nn = clouds.bumpy_sphere(N, 2)
+    cen = np.arange(M, dtype=np.int32) % N
+    gpu = run_gpu(spin, torch, P, Nn, cen, 16, 0.02 if N > 100 else 0.5, 0.5, mode)
+    ora, st = oracle(P, Nn, cen, 16, 0.02 if N > 100 else 0.5, 0.5, mode)
+    check(gpu, ora, st, mode, f"bumpy N={N} M={M} {mode}")
+
+
+@pytest.mark.parametrize("W", [1, 2, 5, 24, 32, 64])
+def test_widths(spin, torch, W):
+    """W = 1 .. 64 (G = 32/16/8 kernel variants), odd W (real W/2, #3)."""
+    P, Nn = clouds.bumpy_sphere(3000, 7)
+    cen = np.arange(0, 3000, 41, dtype=np.int32)
+    b = 0.4 / W
+    for mode in ("nearest", "bilinear"):
+        if mode == "bilinear" and W < 2:
+            continue
+        gpu = run_gpu(spin, torch, P, Nn, cen, W, b, 0.0, mode)
+        ora, st = oracle(P, Nn, cen, W, b, 0.0, mode)
+        check(gpu, ora, st, mode, f"W={W} {mode}")
+
+
+@pytest.mark.parametrize("flags", [1, 2, 8])   # LITERAL, FLOOR, NO_FAST_CERT
+def test_flags(spin, torch, flags):
+    P, Nn = clouds.bumpy_sphere(4000, 9)
+    cen = np.arange(0, 4000, 29, dtype=np.int32)
+    W, b = (4, 0.5) if flags == 1 else (16, 0.02)
+    for mode in ("nearest", "bilinear"):
+        if flags == 2 and mode == "bilinear":
+            continue
+        gpu = run_gpu(spin, torch, P, Nn, cen, W, b, 0.5, mode, flags=flags)
+        ora, st = oracle(P, Nn, cen, W, b, 0.5, mode, flags & 3)
+        check(gpu, ora, st, mode, f"flags={flags} {mode}")
+
+
+def _dyadic_ties(n, seed):
+    rng = np.random.default_rng(seed)
+    P = (np.round(rng.uniform(-1, 1, (n, 3)) * 8) / 8).astype(np.float32)
+    g = rng.normal(size=(n, 3))
+    Nn = (g / np.linalg.norm(g, axis=1, keepdims=True)).astype(np.float32)
+    Nn[::3] = [0, 0, 1]
+    Nn[1::3] = [1, 0, 0]
+    return P, Nn
+
+
+@pytest.mark.parametrize("flags", [0, 1, 2])
+def test_exact_ties_dyadic(spin, torch, flags):
+    """Many pairs sit EXACTLY on bin edges: exercises the fp64 and exact stages."""
+    P, Nn = _dyadic_ties(400, 3)
+    cen = np.arange(400, dtype=np.int32)
+    W, b = 6, (1.0 if flags == 1 else 0.25)
+    for c in (-math.inf, 0.0):
+        for mode in ("nearest", "bilinear"):
+            if flags == 2 and mode == "bilinear":
+                continue
+            gpu, st_g = run_gpu(spin, torch, P, Nn, cen, W, b, c, mode, flags=flags, stats=True)
+            ora, st = oracle(P, Nn, cen, W, b, c, mode, flags)
+            check(gpu, ora, st, mode, f"ties flags={flags} c={c} {mode}")
+            assert st_g["fp64_fallbacks"] > 0 and st_g["exact_fallbacks"] > 0
+
+
+def test_near_threshold_ulps(spin, torch):
+    """Points 1 fp32 ulp either side of every row / column edge."""
+    W, b = 16, 0.02
+    xs = [[0, 0, 0]]
+    for k in range(0, W + 2):
+        edge = np.float32((W / 2 - k) * b)
+        for z in (np.nextafter(edge, np.float32(-1)), edge, np.nextafter(edge, np.float32(1))):
+            xs.append([0.05, 0, z])
+        r = np.float32(k * b)
+        for xr in (np.nextafter(r, np.float32(0)), r, np.nextafter(r, np.float32(1))):
+            xs.append([xr, 0, 0.01])
+            xs.append([xr * np.float32(0.6), xr * np.float32(0.8), 0.01])
+    X = np.asarray(xs, np.float32)
+    Nn = np.tile(np.array([0, 0, 1], np.float32), (len(X), 1))
+    for mode in ("nearest", "bilinear"):
+        gpu = run_gpu(spin, torch, X, Nn, [0], W, b, -math.inf, mode)
+        ora, st = oracle(X, Nn, [0], W, b, -math.inf, mode)
+        check(gpu, ora, st, mode, f"ulps {mode}")
+
+
+# ------------------------------------------------------------------ schedules
+
+def test_schedule_invariance(spin, torch):
+    """S:169 keystone: STATIC/SS/GSS/FAC x P x unit give bit-identical images."""
+    P, Nn = clouds.bumpy_sphere(6000, 4)
+    cen = np.arange(0, 6000, 3, dtype=np.int32)
+    for mode in ("nearest", "bilinear"):
+        ref = run_gpu(spin, torch, P, Nn, cen, 16, 0.02, 0.5, mode)
+        for sched in ("STATIC", "SS", "GSS", "FAC"):
+            for Pn in (1, 7, 148, 0):
+                for unit in (0, 1, 5):
+                    got = run_gpu(spin, torch, P, Nn, cen, 16, 0.02, 0.5, mode, schedule=sched,
+                                  P=Pn, unit=unit)
+                    np.testing.assert_array_equal(got, ref, err_msg=f"{mode} {sched} P={Pn} u={unit}")
+        ora, st = oracle(P, Nn, cen[:200], 16, 0.02, 0.5, mode)
+        check(ref[:200], ora, st, mode, f"sched ref {mode}")
+
+
+def test_dealer_stats_and_cta_times(spin, torch):
+    P, Nn = clouds.bumpy_sphere(8000, 5)
+    cen = np.arange(8000, dtype=np.int32)
+    for sched in ("STATIC", "SS", "GSS", "FAC"):
+        _, st = run_gpu(spin, torch, P, Nn, cen, 16, 0.02, 0.5, "nearest", stats=True,
+                        schedule=sched, P=64, cta_capacity=64)
+        assert st["P"] == 64 and st["pairs_visited"] == 8000 * 8000
+        assert int(st["cta_units"].sum()) == st["n_units"] == -(-8000 // st["G"])
+        assert np.all(st["cta_end_ns"] >= st["cta_start_ns"])
+        exp = len(spin.chunk_sequence(sched, st["n_units"], 64)) - 1
+        assert st["n_chunks"] == exp
+
+
+# ------------------------------------------------------------------ cell list
+
+@pytest.mark.parametrize("mode", ["nearest", "bilinear"])
+def test_cells_vs_oracle_and_brute(spin, torch, mode):
+    P, Nn = clouds.clustered(30000, 3)
+    cen = clouds.sample_centres(30000, 600, 13)
+    W, b, c = 16, 0.01, 0.5
+    cells, st_c = run_gpu(spin, torch, P, Nn, cen, W, b, c, mode, prune="cells", stats=True)
+    brute = run_gpu(spin, torch, P, Nn, cen, W, b, c, mode, prune="brute")
+    np.testing.assert_array_equal(cells, brute)
+    ora, st = oracle(P, Nn, cen[:150], W, b, c, mode, cells=True)
+    check(cells[:150], ora, st, mode, f"cells {mode}")
+    assert st_c["pairs_visited"] < 600 * 30000
+    # unsorted control and every schedule give the same images
+    for sched in ("SS", "GSS", "FAC"):
+        got = run_gpu(spin, torch, P, Nn, cen, W, b, c, mode, prune="cells", schedule=sched)
+        np.testing.assert_array_equal(got, cells)
+    got = run_gpu(spin, torch, P, Nn, cen, W, b, c, mode, prune="cells", flags=spin.F_NO_SORT)
+    np.testing.assert_array_equal(got, cells)
+
+
+def test_cells_floor_and_literal(spin, torch):
+    P, Nn = clouds.clustered(20000, 8)
+    cen = clouds.sample_centres(20000, 300, 14)
+    for flags, W, b in ((2, 8, 0.01), (1, 4, 0.3)):
+        cells = run_gpu(spin, torch, P, Nn, cen, W, b, 0.5, "nearest", prune="cells", flags=flags)
+        brute = run_gpu(spin, torch, P, Nn, cen, W, b, 0.5, "nearest", flags=flags)
+        np.testing.assert_array_equal(cells, brute)
+        ora, _ = oracle(P, Nn, cen[:60], W, b, 0.5, "nearest", flags)
+        assert_nearest_exact(cells[:60], ora, f"cells flags={flags}")
+
+
+# ------------------------------------------------------------------ edge cases and errors
+
+def test_edge_cases(spin, torch):
+    P, Nn = clouds.bumpy_sphere(2000, 6)
+    eng = spin.SpinEngine(_dev(torch, P), _dev(torch, Nn))
+    try:
+        empty = torch.zeros(0, dtype=torch.int32, device="cuda")
+        out = eng.generate(empty, 8, 0.05, 0.5)
+        assert out.shape == (0, 8, 8)
+        # duplicated centres give identical images
+        cen = _dev(torch, np.array([5, 5, 17, 5], np.int32))
+        out = eng.generate(cen, 8, 0.05, 0.5).cpu().numpy()
+        np.testing.assert_array_equal(out[0], out[1])
+        np.testing.assert_array_equal(out[0], out[3])
+        # support disabled (S = 2 pi) and S = 0 (only parallel normals)
+        for c in (-math.inf, 1.0):
+            g = eng.generate(_dev(torch, np.arange(0, 2000, 97, dtype=np.int32)), 8, 0.05, c).cpu().numpy()
+            o, _ = oracle(P, Nn, np.arange(0, 2000, 97), 8, 0.05, c, "nearest")
+            assert_nearest_exact(g, o, f"c={c}")
+        # out-of-range centre: zero image, SPIN_E_RANGE
+        bad = _dev(torch, np.array([3, 2000, -1, 4], np.int32))
+        out = torch.full((4, 8, 8), 7.0, device="cuda")
+        with pytest.raises(spin.SpinError) as ei:
+            eng.generate(bad, 8, 0.05, 0.5, out=out, stats=True)
+        assert ei.value.status == 2
+        o = out.cpu().numpy()
+        assert np.all(o[1] == 0) and np.all(o[2] == 0) and o[0].sum() > 0
+        # the next call is clean
+        eng.generate(_dev(torch, np.array([1], np.int32)), 8, 0.05, 0.5, stats=True)
+        # invalid arguments
+        ok = _dev(torch, np.array([1], np.int32))
+        for kw in (dict(W=0), dict(W=65), dict(b=0.0), dict(b=float("nan")), dict(cos_As=1.5),
+                   dict(W=1, mode="bilinear")):
+            args = dict(W=8, b=0.05, cos_As=0.5, mode="nearest")
+            args.update(kw)
+            with pytest.raises(spin.SpinError) as ei:
+                eng.generate(ok, args["W"], args["b"], args["cos_As"], mode=args["mode"])
+            assert ei.value.status == 1
+    finally:
+        eng.close()
+
+
+def test_invalid_cloud(spin, torch):
+    P, Nn = clouds.bumpy_sphere(100, 6)
+    Nn2 = Nn.copy()
+    Nn2[42] *= 1.01
+    with pytest.raises(spin.SpinError) as ei:
+        spin.SpinEngine(_dev(torch, P), _dev(torch, Nn2))
+    assert ei.value.status == 3 and "42" in str(ei.value)
+    P2 = P.copy()
+    P2[7, 1] = np.inf
+    with pytest.raises(spin.SpinError) as ei:
+        spin.SpinEngine(_dev(torch, P2), _dev(torch, Nn))
+    assert ei.value.status == 3 and "7" in str(ei.value)
+
+
+def test_host_path_and_reload(spin, torch):
+    """spin_generate_host (host buffers) equals the device path; spin_load_cloud swaps clouds."""
+    P, Nn = clouds.bumpy_sphere(3000, 10)
+    cen = np.arange(0, 3000, 7, dtype=np.int32)
+    eng = spin.SpinEngine(P, Nn)      # host arrays: spin_create copies with cudaMemcpyDefault
+    try:
+        h = eng.generate_host(cen, 16, 0.02, 0.5, mode="bilinear")
+        d = eng.generate(_dev(torch, cen), 16, 0.02, 0.5, mode="bilinear").cpu().numpy()
+        np.testing.assert_array_equal(h, d)
+        P2, N2 = clouds.bumpy_sphere(5000, 11)
+        eng.load_cloud(P2, N2)
+        h2 = eng.generate_host(cen, 16, 0.02, 0.5)
+        o, _ = oracle(P2, N2, cen, 16, 0.02, 0.5, "nearest")
+        assert_nearest_exact(h2, o, "reloaded cloud")
+        h3 = eng.generate_host(cen, 16, 0.02, 0.5, prune="cells")
+        np.testing.assert_array_equal(h3, h2)
+    finally:
+        eng.close()
+
+
+# ------------------------------------------------------------------ full-size configs, sampled
+
+def _full(spin, torch, cfg_id, mode, prune, n_check, W=None, sched="STATIC"):
+    cfg = clouds.CONFIGS[cfg_id]
+    P, Nn = clouds.make_cloud(cfg_id)
+    cen = clouds.make_centres(cfg_id, cfg["N"])
+    W = W or cfg["W"]
+    gpu, st = run_gpu(spin, torch, P, Nn, cen, W, cfg["b"], cfg["cos_As"], mode, prune=prune,
+                      stats=True, schedule=sched)
+    pick = clouds.subsample(len(cen), n_check, 200 + cfg_id)
+    ora, so = oracle(P, Nn, cen[pick], W, cfg["b"], cfg["cos_As"], mode, cells=(prune == "cells"))
+    check(gpu[pick], ora, so, mode, f"C{cfg_id} {mode} {prune} W={W}")
+    if mode == "nearest":
+        assert gpu.sum(dtype=np.float64) == st["pairs_accepted"]
+    return gpu, st
+
+
+@pytest.mark.parametrize("mode", ["nearest", "bilinear"])
+def test_config2_full_sampled(spin, torch, mode):
+    _full(spin, torch, 2, mode, "brute", 40, sched="GSS")
+
+
+def test_config3_full_sampled(spin, torch):
+    for mode in ("bilinear", "nearest"):
+        _full(spin, torch, 3, mode, "cells", 30, sched="FAC")
+
+
+def test_config4_full_sampled(spin, torch):
+    _full(spin, torch, 4, "bilinear", "brute", 12, sched="SS")
+
+
+@pytest.mark.parametrize("W", [8, 24])
+def test_config5_full_sampled(spin, torch, W):
+    _full(spin, torch, 5, "nearest", "cells", 20, W=W, sched="GSS")
