@@ -57,6 +57,20 @@ __device__ __forceinline__ int cell_coord(float x, float o, float inv_h, int dim
   return (int)floorf(t);
 }
 
+// The conservative pair test as ONE predicate chain plus one predicated OR:
+// pass = (s >= c) && (|beta''| <= h) && (q'' <= Qt)  (NaN compares false).
+__device__ __forceinline__ unsigned pair_bit(unsigned mask, float s, float c, float abe, float h,
+                                             float q, float qt, unsigned bit) {
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.ge.f32 p, %1, %2;\n\t"
+      "setp.le.and.f32 p, %3, %4, p;\n\t"
+      "setp.le.and.f32 p, %5, %6, p;\n\t"
+      "@p or.b32 %0, %0, %7;\n\t}"
+      : "+r"(mask)
+      : "f"(s), "f"(c), "f"(abe), "f"(h), "f"(q), "f"(qt), "r"(bit));
+  return mask;
+}
+
 // ------------------------------------------------------------------ smem layout
 struct Layout {
   size_t oA, oB, oP, oN, oM, oImg, oHi, oQ, oRowS, oRowO, total;
@@ -358,8 +372,7 @@ __global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__
               const float be = fmaf(A4.x, x[k], fmaf(A4.y, y[k], fmaf(A4.z, z[k], A4.w)));
               const float t = fmaf(B4.x, x[k], fmaf(B4.y, y[k], fmaf(B4.z, z[k], xx[k])));
               const float q = fmaf(-be, be, t);
-              const bool pass = (s >= c_test) & (fabsf(be) <= h_test) & (q <= B4.w);
-              if (pass) mask |= 1u << (c * KP + k);
+              mask = pair_bit(mask, s, c_test, fabsf(be), h_test, q, B4.w, 1u << (c * KP + k));
             }
           }
           // compaction: each round every lane with bits left enqueues its lowest one
