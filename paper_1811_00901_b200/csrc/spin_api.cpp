@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -511,6 +512,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   p.literal = (flags & SPIN_F_LITERAL_HALF_WIDTH) ? 1 : 0;
   p.floor_bins = (flags & SPIN_F_FLOOR_BINS) ? 1 : 0;
   p.no_fast_cert = (flags & SPIN_F_NO_FAST_CERT) ? 1 : 0;
+  if (const char* dbg = std::getenv("SPIN_DEBUG_SKIP")) p.debug_skip = std::atoi(dbg);
   // self pair (d = 0): beta = q = 0 exactly, u = W/2 (scaled reading only)
   p.self_fast = p.literal ? 0 : 1;
   if (mode == SPIN_NEAREST) {

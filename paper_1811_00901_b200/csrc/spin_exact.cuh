@@ -123,16 +123,18 @@ __device__ __noinline__ int exact_sign_q_minus(const PairD& P, double b, double 
 
 // Result of the slow decision for one pair.
 struct SlowOut {
-  int accept;  // 0 / 1
-  int k, l;    // NEAREST bins (valid when accept)
+  int accept;   // 0 / 1
+  int k, l;     // NEAREST bins (valid when accept)
+  int n_exact;  // decisions taken by the exact stage
 };
 
 // fp64 stage with per-pair certified bounds, escalating each uncertain decision to
 // the exact stage.  `mode` 0 NEAREST / 1 BILINEAR (BILINEAR returns region only).
 __device__ __noinline__ SlowOut slow_decide(const PairD& P, int W, double A, double b,
                                             double cos_As, int has_support, int literal,
-                                            int floor_bins, int mode, unsigned& n_exact) {
-  SlowOut r{0, 0, 0};
+                                            int floor_bins, int mode) {
+  SlowOut r{0, 0, 0, 0};
+  int& n_exact = r.n_exact;
   const double u = U64;
   // --- support
   if (has_support) {

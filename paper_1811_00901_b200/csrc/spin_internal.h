@@ -44,6 +44,7 @@ struct KParams {
   float inv_b, inv_b2, Af;
   float Es_a, Eu_a, Ew_a, D2g;
   int32_t literal, floor_bins, no_fast_cert;
+  int32_t debug_skip;        // measurement only (env SPIN_DEBUG_SKIP): 1 skip accept, 2 skip compaction too
   int32_t self_fast;         // d == 0 pairs can be decided exactly without arithmetic
   int32_t self_k, self_l;    // their (k, l) (NEAREST) or (i0, -) ; self_k = -1: no contribution
   float self_a;              // BILINEAR: a for the self pair

@@ -31,11 +31,12 @@ namespace spin {
 constexpr int NT = 256;           // threads per CTA
 constexpr int NWARP = NT / 32;
 constexpr int KP = 4;             // points per thread (register blocking)
-constexpr int CB = 8;             // centres per mask batch: CB * KP = 32 bits
-constexpr int QCAP = 64;          // per-warp candidate ring (power of two, >= 2*32)
+constexpr int CB_MAX = 8;         // centres per mask batch: CB * KP <= 32 bits
+__host__ __device__ constexpr int cb_of(int G) { return G < CB_MAX ? G : CB_MAX; }
+constexpr int QCAP = 512;         // per-warp candidate ring of u16 entries (power of two)
 constexpr int ROWCAP = NT;        // CELLS: grid rows staged per batch
 
-static_assert(CB * KP == 32, "mask is one u32");
+static_assert(CB_MAX * KP == 32, "mask is one u32");
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -73,7 +74,7 @@ __device__ __forceinline__ unsigned pair_bit(unsigned mask, float s, float c, fl
 
 // ------------------------------------------------------------------ smem layout
 struct Layout {
-  size_t oA, oB, oP, oN, oM, oImg, oHi, oQ, oRowS, oRowO, total;
+  size_t oA, oB, oP, oN, oM, oImg, oHi, oQ, oTP, oTN, oMask, oRowS, oRowO, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ inline Layout make_layout(int G, int W, int mode, int prune) {
@@ -88,7 +89,11 @@ __host__ __device__ inline Layout make_layout(int G, int W, int mode, int prune)
   L.oImg = o; o = align16(o + 4 * WW * G);
   L.oHi = o;
   if (mode == 1) o = align16(o + 4 * ((WW + 1) / 2) * G);
-  L.oQ = o; o += 8 * (size_t)QCAP * NWARP;
+  L.oQ = o; o += 2 * (size_t)QCAP * NWARP;
+  o = align16(o);
+  L.oTP = o; o += 16 * (size_t)32 * KP * NWARP;    // per-warp staged tile: positions
+  L.oTN = o; o += 16 * (size_t)32 * KP * NWARP;    //                      normals
+  L.oMask = o; o += 4 * (size_t)32 * (G / cb_of(G)) * NWARP;   // per-warp pass masks of the tile
   L.oRowS = o;
   L.oRowO = o;
   if (prune == 1) {
@@ -121,6 +126,23 @@ __device__ __forceinline__ void add_fixed(uint32_t* lo, uint32_t* hi, int bin, f
 }
 
 // ------------------------------------------------------------------ accept path
+// round-to-nearest-even for |x| < 2^22 on the FMA pipe (no F2I/FRND on the XU pipe)
+__device__ __forceinline__ float rint_magic(float x) {
+  return __fsub_rn(__fadd_rn(x, 12582912.0f), 12582912.0f);
+}
+
+// The slow stages, out of line; operands by value so the fast path keeps no stack.
+__device__ __noinline__ SlowOut slow_pair(float4 P4, float4 N4, float4 X4, float4 NX4, int W,
+                                          double A, double b, double cos_As, int has_support,
+                                          int literal, int floor_bins, int mode) {
+  PairD D;
+  D.p[0] = P4.x; D.p[1] = P4.y; D.p[2] = P4.z;
+  D.n[0] = N4.x; D.n[1] = N4.y; D.n[2] = N4.z;
+  D.x[0] = X4.x; D.x[1] = X4.y; D.x[2] = X4.z;
+  D.nx[0] = NX4.x; D.nx[1] = NX4.y; D.nx[2] = NX4.z;
+  return slow_decide(D, W, A, b, cos_As, has_support, literal, floor_bins, mode);
+}
+
 // One candidate (centre slot g, point X): certified fp32 decision, fallbacks, splat.
 template <int MODE>
 __device__ __forceinline__ void accept_pair(const KParams& p, const float4 P4, const float4 N4,
@@ -128,7 +150,7 @@ __device__ __forceinline__ void accept_pair(const KParams& p, const float4 P4, c
                                             uint32_t* hi, Ctr& ct) {
   const int W = p.W;
   ++ct.cand;
-  const float d0 = X4.x - P4.x, d1 = X4.y - P4.y, d2 = X4.z - P4.z;
+  const float d0 = __fsub_rn(X4.x, P4.x), d1 = __fsub_rn(X4.y, P4.y), d2 = __fsub_rn(X4.z, P4.z);
   bool unc = p.no_fast_cert != 0;
   // support test, inclusive, cosine form (#5)
   if (p.has_support) {
@@ -137,45 +159,47 @@ __device__ __forceinline__ void accept_pair(const KParams& p, const float4 P4, c
     if (ds < -p.Es_a) return;            // certainly rejected
     if (!(ds > p.Es_a)) unc = true;
   }
-  int k = 0, l = 0;
-  float uval = 0.f, wval = 0.f;
   if (p.self_fast && d0 == 0.f && d1 == 0.f && d2 == 0.f && !unc) {
     // the self pair (and exact duplicates): beta = 0 and q = 0 exactly (#8)
     if (p.self_k < 0) return;
+    ++ct.acc;
     if (MODE == 0) {
       atomicAdd(&img[p.self_k * W], 1u);
     } else {
       add_fixed(img, hi, p.self_k * W, 1.0f - p.self_a, p.err_flags);
       if (p.self_a > 0.f) add_fixed(img, hi, (p.self_k + 1) * W, p.self_a, p.err_flags);
     }
-    ++ct.acc;
     return;
   }
   const float be = fmaf(N4.x, d0, fmaf(N4.y, d1, N4.z * d2));       // np_i.(X-P)
   const float dd = fmaf(d0, d0, fmaf(d1, d1, d2 * d2));              // ||X-P||^2
   const float q = fmaf(-be, be, dd);                                 // alpha^2
-  uval = p.literal ? (p.Af - be) * p.inv_b : fmaf(-be, p.inv_b, p.Af);
-  wval = q * p.inv_b2;                                               // (alpha/b)^2
+  const float uval = p.literal ? (p.Af - be) * p.inv_b : fmaf(-be, p.inv_b, p.Af);
+  const float wval = q * p.inv_b2;                                   // (alpha/b)^2
   const float Wm1 = (float)(W - 1);
+  int k = 0, l = 0;
   if (!(dd <= p.D2g)) {
     unc = true;                     // outside the domain of the fp32 bounds: no fp32 verdicts
   } else if (MODE == 0) {
     // row k = ceil(u) (or floor): certified when u is farther than Eu from an integer
     const float uc = fminf(fmaxf(uval, -4.0f), (float)W + 4.0f);
-    const float rr = rintf(uc);
-    const bool ku = !(fabsf(uc - rr) > p.Eu_a);
+    const float rr = rint_magic(uc);
+    const float du = uc - rr;                                        // exact
+    const bool ku = !(fabsf(du) > p.Eu_a);
     if (!ku) {
-      k = p.floor_bins ? (int)floorf(uc) : (int)ceilf(uc);
-      if (k < 0 || k >= W) return;
+      const float kf = p.floor_bins ? (du < 0.f ? rr - 1.0f : rr) : (du > 0.f ? rr + 1.0f : rr);
+      if (kf < 0.f || kf >= (float)W) return;
+      k = (int)kf;
     }
     // column l = ceil(sqrt(w)) (or floor): certified when w is farther than Ew from
-    // every perfect square (squares are exact in fp32 here)
-    const float v = sqrtf(fmaxf(wval, 0.0f));
-    const float fl = floorf(v);
-    const float dlo = wval - fl * fl, dhi = (fl + 1.0f) * (fl + 1.0f) - wval;
+    // every perfect square (fl^2 is exact); sqrt only proposes fl, the squares decide
+    const float wc = fmaxf(wval, 0.0f);
+    const float v = wc * rsqrtf(fmaxf(wc, 1e-30f));
+    const float fl = rint_magic(v - 0.5f);
+    const float dlo = fmaf(-fl, fl, wval), dhi = fmaf(fl + 1.0f, fl + 1.0f, -wval);
     bool lu = false;
     if (wval < -p.Ew_a) l = 0;
-    else if (dlo > p.Ew_a && dhi > p.Ew_a) l = p.floor_bins ? (int)fl : (int)fl + 1;
+    else if (dlo > p.Ew_a && dhi > p.Ew_a) l = (int)fl + (p.floor_bins ? 0 : 1);
     else lu = true;
     if (!lu && l >= W) return;
     unc = unc || ku || lu;
@@ -190,13 +214,9 @@ __device__ __forceinline__ void accept_pair(const KParams& p, const float4 P4, c
   }
   if (unc) {
     ++ct.f64;
-    PairD D;
-    D.p[0] = P4.x; D.p[1] = P4.y; D.p[2] = P4.z;
-    D.n[0] = N4.x; D.n[1] = N4.y; D.n[2] = N4.z;
-    D.x[0] = X4.x; D.x[1] = X4.y; D.x[2] = X4.z;
-    D.nx[0] = NX4.x; D.nx[1] = NX4.y; D.nx[2] = NX4.z;
-    SlowOut r = slow_decide(D, W, p.A, p.b, p.cos_As, p.has_support, p.literal, p.floor_bins,
-                            MODE, ct.exact);
+    const SlowOut r = slow_pair(P4, N4, X4, NX4, W, p.A, p.b, p.cos_As, p.has_support, p.literal,
+                                p.floor_bins, MODE);
+    ct.exact += r.n_exact;
     if (!r.accept) return;
     k = r.k;
     l = r.l;
@@ -206,8 +226,8 @@ __device__ __forceinline__ void accept_pair(const KParams& p, const float4 P4, c
     atomicAdd(&img[k * W + l], 1u);                                  // tempSpinImage[k,l]++
   } else {
     const float v = sqrtf(fmaxf(wval, 0.0f));
-    const float fi = fminf(fmaxf(floorf(uval), 0.0f), Wm1 - 1.0f);
-    const float fj = fminf(fmaxf(floorf(v), 0.0f), Wm1 - 1.0f);
+    const float fi = fminf(fmaxf(rint_magic(uval - 0.5f), 0.0f), Wm1 - 1.0f);
+    const float fj = fminf(fmaxf(rint_magic(v - 0.5f), 0.0f), Wm1 - 1.0f);
     const float a = fminf(fmaxf(uval - fi, 0.0f), 1.0f);
     const float c = fminf(fmaxf(v - fj, 0.0f), 1.0f);
     const int bin = (int)fi * W + (int)fj;
@@ -223,7 +243,7 @@ template <int MODE, int PRUNE, int G>
 __global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__ KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_chunk;
-  __shared__ int s_nrows, s_total, s_live;
+  __shared__ int s_total, s_live;
   __shared__ int s_rng[6];
   __shared__ unsigned long long s_ctr[5];
 
@@ -241,7 +261,11 @@ __global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__
   int* sRowO = reinterpret_cast<int*>(smem + L.oRowO);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int2* sQ = reinterpret_cast<int2*>(smem + L.oQ) + warp * QCAP;
+  uint16_t* sQ = reinterpret_cast<uint16_t*>(smem + L.oQ) + warp * QCAP;
+  float4* sTP = reinterpret_cast<float4*>(smem + L.oTP) + warp * 32 * KP;
+  float4* sTN = reinterpret_cast<float4*>(smem + L.oTN) + warp * 32 * KP;
+  constexpr int CB = cb_of(G);
+  unsigned* sMask = reinterpret_cast<unsigned*>(smem + L.oMask) + warp * 32 * (G / CB);
   const int hiWords = (WW + 1) / 2;
 
   if (tid < 5) s_ctr[tid] = 0ull;
@@ -339,13 +363,95 @@ __global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__
       __syncthreads();
 
       // ---- a8-a10: stream points, pair test, compact, accept
+      // Each thread holds KP points in registers for all G centres.  Per batch of CB
+      // centres the pass bits go to one u32 mask (bit = c*KP + k) stored in smem; once
+      // per tile the warp compacts all its bits into a ring of 16-bit entries
+      // (centre slot << 7 | lane << 2 | k) and processes them 32 at a time, reading the
+      // point from the warp's staged copy of the tile (no global re-load).
       unsigned qhead = 0, qtail = 0;
-      uint32_t* img_base = sImg;
-      auto process_entry = [&](int2 e) {
-        const int gs = e.y;
+      constexpr int NWD = G / CB;                      // mask words per lane per tile
+      auto process_entry = [&](unsigned e) {
+        if (p.debug_skip) return;
+        const int gs = (int)(e >> 7);
+        const int src = (int)(e & 127u);
         const float4 P4 = sP[gs], N4 = sN[gs];
-        const float4 X4 = __ldg(&p.pos[e.x]), NX4 = __ldg(&p.nrm[e.x]);
-        accept_pair<MODE>(p, P4, N4, X4, NX4, img_base + gs * WW, sHi + gs * hiWords, ct);
+        const float4 X4 = sTP[src], NX4 = sTN[src];
+        accept_pair<MODE>(p, P4, N4, X4, NX4, sImg + gs * WW, sHi + gs * hiWords, ct);
+      };
+      auto compact_and_accept = [&]() {
+        unsigned mw[NWD];
+        int cnt = 0;
+#pragma unroll
+        for (int w = 0; w < NWD; ++w) {
+          mw[w] = sMask[w * 32 + lane];
+          cnt += __popc(mw[w]);
+        }
+        int x = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, x, 31);
+        if (total == 0) return;
+        bool more = false;
+        if (total <= QCAP) {
+          // common case: one scan gives every lane its slot range
+          unsigned pos = qtail + (unsigned)(x - cnt);
+#pragma unroll
+          for (int w = 0; w < NWD; ++w) {
+            unsigned m = mw[w];
+            while (m) {
+              const int bit = __ffs(m) - 1;
+              m &= m - 1u;
+              sQ[pos & (QCAP - 1)] =
+                  (uint16_t)(((w * CB + (bit >> 2)) << 7) | (lane << 2) | (bit & 3));
+              ++pos;
+            }
+            mw[w] = 0u;
+          }
+          qtail += (unsigned)total;
+        } else {
+          more = true;   // dense tile (CELLS clusters): fill the ring round by round
+        }
+        for (;;) {
+          if (more) {
+            while (qtail - qhead <= (unsigned)(QCAP - 32)) {
+              unsigned m = 0u;
+              int wsel = 0;
+#pragma unroll
+              for (int w = NWD - 1; w >= 0; --w)
+                if (mw[w]) { m = mw[w]; wsel = w; }
+              const unsigned ball = __ballot_sync(0xffffffffu, m != 0u);
+              if (!ball) break;
+              if (m) {
+                const int bit = __ffs(m) - 1;
+#pragma unroll
+                for (int w = 0; w < NWD; ++w)
+                  if (w == wsel) mw[w] &= mw[w] - 1u;
+                const unsigned slot = (qtail + __popc(ball & lanemask_lt())) & (QCAP - 1);
+                sQ[slot] = (uint16_t)(((wsel * CB + (bit >> 2)) << 7) | (lane << 2) | (bit & 3));
+              }
+              qtail += __popc(ball);
+            }
+            unsigned any = 0u;
+#pragma unroll
+            for (int w = 0; w < NWD; ++w) any |= mw[w];
+            more = __any_sync(0xffffffffu, any != 0u);
+          }
+          __syncwarp();
+          for (;;) {
+            const unsigned avail = qtail - qhead;
+            if (avail == 0u || (avail < 32u && more)) break;
+            const unsigned n = min(32u, avail);
+            unsigned e = 0;
+            if ((unsigned)lane < n) e = sQ[(qhead + lane) & (QCAP - 1)];
+            __syncwarp();
+            qhead += n;
+            if ((unsigned)lane < n) process_entry(e);
+          }
+          if (!more) break;
+        }
       };
       auto run_tile = [&](const int (&j)[KP]) {
         float x[KP], y[KP], z[KP], xx[KP], nx[KP], ny[KP], nz[KP];
@@ -355,11 +461,17 @@ __global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__
           const float4 b = __ldg(&p.nrm[j[k]]);
           x[k] = a.x; y[k] = a.y; z[k] = a.z; xx[k] = a.w;
           nx[k] = b.x; ny[k] = b.y; nz[k] = b.z;
+          sTP[lane * KP + k] = a;   // the previous tile's entries were all processed
+          sTN[lane * KP + k] = b;
         }
         const float c_test = p.c_test, h_test = p.h_test;
 #pragma unroll 1
         for (int cb = 0; cb < G; cb += CB) {
           unsigned mask = 0u;
+          if (cb >= gcount) {            // a partial group skips its empty slots
+            sMask[(cb / CB) * 32 + lane] = 0u;
+            continue;
+          }
 #pragma unroll
           for (int c = 0; c < CB; ++c) {
             const float4 A4 = sA[cb + c];
@@ -375,28 +487,11 @@ __global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__
               mask = pair_bit(mask, s, c_test, fabsf(be), h_test, q, B4.w, 1u << (c * KP + k));
             }
           }
-          // compaction: each round every lane with bits left enqueues its lowest one
-          unsigned m = mask;
-          while (__any_sync(0xffffffffu, m != 0u)) {
-            const unsigned ball = __ballot_sync(0xffffffffu, m != 0u);
-            if (m) {
-              const int bit = __ffs(m) - 1;
-              m &= m - 1u;
-              const int kk = bit & (KP - 1);
-              const int jj = kk == 0 ? j[0] : kk == 1 ? j[1] : kk == 2 ? j[2] : j[3];
-              const unsigned slot = (qtail + __popc(ball & lanemask_lt())) & (QCAP - 1);
-              sQ[slot] = make_int2(jj, cb + (bit >> 2));
-            }
-            qtail += __popc(ball);
-            if (qtail - qhead >= 32u) {
-              __syncwarp();
-              const int2 e = sQ[(qhead + lane) & (QCAP - 1)];
-              __syncwarp();
-              qhead += 32u;
-              process_entry(e);
-            }
-          }
+          sMask[(cb / CB) * 32 + lane] = mask;
         }
+        __syncwarp();
+        if (p.debug_skip < 2) compact_and_accept();
+        __syncwarp();
       };
 
       if (PRUNE == 0) {
@@ -476,16 +571,6 @@ __global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__
           __syncthreads();
         }
       }
-      // drain this warp's queue
-      while (qtail != qhead) {
-        const unsigned cnt = min(32u, qtail - qhead);
-        int2 e = make_int2(0, 0);
-        __syncwarp();
-        if ((unsigned)lane < cnt) e = sQ[(qhead + lane) & (QCAP - 1)];
-        __syncwarp();
-        qhead += cnt;
-        if ((unsigned)lane < cnt) process_entry(e);
-      }
       __syncthreads();
       // ---- a12: write the images back in the caller's order
       for (int i = tid; i < G * WW; i += NT) {
@@ -536,6 +621,7 @@ __global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__
 template <int MODE, int PRUNE>
 static const void* kernel_ptr(int G) {
   switch (G) {
+    case 4: return (const void*)spin_persistent<MODE, PRUNE, 4>;
     case 8: return (const void*)spin_persistent<MODE, PRUNE, 8>;
     case 16: return (const void*)spin_persistent<MODE, PRUNE, 16>;
     default: return (const void*)spin_persistent<MODE, PRUNE, 32>;
@@ -547,11 +633,12 @@ static const void* kernel_for(int mode, int prune, int G) {
 }
 
 LaunchCfg choose_launch(int W, int mode, int prune) {
-  // images live in shared memory: NEAREST 4 B/bin, BILINEAR 6 B/bin; keep the image
-  // block <= 96 KB so that two CTAs fit on an SM (227 KB), else allow one CTA.
-  const size_t per_img = (size_t)W * W * (mode == 0 ? 4 : 6);
+  // Images live in shared memory (NEAREST 4 B/bin, BILINEAR 6 B/bin).  Take the
+  // largest G in {32, 16, 8} whose whole layout lets two CTAs share an SM
+  // (2 x (smem + 1 KB reserved) <= 228 KB); W = 64 falls back to one CTA per SM.
   int G = 32;
-  while (G > 8 && per_img * G > 96 * 1024) G >>= 1;
+  while (G > 8 && make_layout(G, W, mode, prune).total > 112 * 1024) G >>= 1;
+  if (make_layout(G, W, mode, prune).total > 220 * 1024) G = 4;   // W = 64 BILINEAR
   LaunchCfg lc;
   lc.G = G;
   lc.threads = NT;

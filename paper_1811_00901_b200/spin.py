@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspin.so")
+LIB_PATH = os.environ.get("SPIN_LIB_PATH") or os.path.join(_HERE, "libspin.so")  # override: A/B builds
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libspin.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'`")
 _lib = C.CDLL(LIB_PATH)
