@@ -43,7 +43,7 @@ def parse(argv=None):
     ap.add_argument("--impl", default="spin", choices=["spin", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--mode", default=None, choices=[None, "nearest", "bilinear"])
-    ap.add_argument("--schedule", default="GSS", choices=["STATIC", "SS", "GSS", "FAC"])
+    ap.add_argument("--schedule", default="SS", choices=["STATIC", "SS", "GSS", "FAC"])
     ap.add_argument("--W", type=int, default=None)
     ap.add_argument("--P", type=int, default=0)
     ap.add_argument("--unit", type=int, default=0)

@@ -33,7 +33,7 @@ constexpr int NWARP = NT / 32;
 constexpr int KP = 4;             // points per thread (register blocking)
 constexpr int CB_MAX = 8;         // centres per mask batch: CB * KP <= 32 bits
 __host__ __device__ constexpr int cb_of(int G) { return G < CB_MAX ? G : CB_MAX; }
-constexpr int QCAP = 512;         // per-warp candidate ring of u16 entries (power of two)
+constexpr int QCAP = 1024;        // per-warp candidate ring of u16 entries (power of two)
 constexpr int ROWCAP = NT;        // CELLS: grid rows staged per batch
 
 static_assert(CB_MAX * KP == 32, "mask is one u32");
@@ -144,73 +144,57 @@ __device__ __noinline__ SlowOut slow_pair(float4 P4, float4 N4, float4 X4, float
 }
 
 // One candidate (centre slot g, point X): certified fp32 decision, fallbacks, splat.
+// Branch-light: one early exit for certain rejections, one branch to the slow stages.
 template <int MODE>
 __device__ __forceinline__ void accept_pair(const KParams& p, const float4 P4, const float4 N4,
                                             const float4 X4, const float4 NX4, uint32_t* img,
                                             uint32_t* hi, Ctr& ct) {
   const int W = p.W;
+  const float Wf = (float)W, Wm1 = Wf - 1.0f;
   ++ct.cand;
   const float d0 = __fsub_rn(X4.x, P4.x), d1 = __fsub_rn(X4.y, P4.y), d2 = __fsub_rn(X4.z, P4.z);
-  bool unc = p.no_fast_cert != 0;
-  // support test, inclusive, cosine form (#5)
-  if (p.has_support) {
-    const float s = fmaf(N4.x, NX4.x, fmaf(N4.y, NX4.y, N4.z * NX4.z));
-    const float ds = s - p.c_f;
-    if (ds < -p.Es_a) return;            // certainly rejected
-    if (!(ds > p.Es_a)) unc = true;
-  }
-  if (p.self_fast && d0 == 0.f && d1 == 0.f && d2 == 0.f && !unc) {
-    // the self pair (and exact duplicates): beta = 0 and q = 0 exactly (#8)
-    if (p.self_k < 0) return;
-    ++ct.acc;
-    if (MODE == 0) {
-      atomicAdd(&img[p.self_k * W], 1u);
-    } else {
-      add_fixed(img, hi, p.self_k * W, 1.0f - p.self_a, p.err_flags);
-      if (p.self_a > 0.f) add_fixed(img, hi, (p.self_k + 1) * W, p.self_a, p.err_flags);
-    }
-    return;
-  }
+  // support test, inclusive, cosine form (#5); c_f = -inf disables it (ds = +inf)
+  const float s = fmaf(N4.x, NX4.x, fmaf(N4.y, NX4.y, N4.z * NX4.z));
+  const float ds = s - p.c_f;
+  if (ds < -p.Es_a) return;                                          // certainly rejected
   const float be = fmaf(N4.x, d0, fmaf(N4.y, d1, N4.z * d2));       // np_i.(X-P)
   const float dd = fmaf(d0, d0, fmaf(d1, d1, d2 * d2));              // ||X-P||^2
   const float q = fmaf(-be, be, dd);                                 // alpha^2
   const float uval = p.literal ? (p.Af - be) * p.inv_b : fmaf(-be, p.inv_b, p.Af);
   const float wval = q * p.inv_b2;                                   // (alpha/b)^2
-  const float Wm1 = (float)(W - 1);
+  bool unc = (p.no_fast_cert != 0) | !(ds > p.Es_a) | !(dd <= p.D2g);
   int k = 0, l = 0;
-  if (!(dd <= p.D2g)) {
-    unc = true;                     // outside the domain of the fp32 bounds: no fp32 verdicts
-  } else if (MODE == 0) {
+  if (MODE == 0) {
+    // the self pair (d == 0): beta = q = 0 exactly, k = ceil(W/2) (or floor), l = 0 (#8)
+    const bool self = (d0 == 0.f) & (d1 == 0.f) & (d2 == 0.f) & (p.self_fast != 0);
     // row k = ceil(u) (or floor): certified when u is farther than Eu from an integer
-    const float uc = fminf(fmaxf(uval, -4.0f), (float)W + 4.0f);
+    const float uc = fminf(fmaxf(uval, -4.0f), Wf + 4.0f);
     const float rr = rint_magic(uc);
     const float du = uc - rr;                                        // exact
-    const bool ku = !(fabsf(du) > p.Eu_a);
-    if (!ku) {
-      const float kf = p.floor_bins ? (du < 0.f ? rr - 1.0f : rr) : (du > 0.f ? rr + 1.0f : rr);
-      if (kf < 0.f || kf >= (float)W) return;
-      k = (int)kf;
-    }
+    const bool ku = !(fabsf(du) > p.Eu_a) & !self;
+    float kf = p.floor_bins ? (du < 0.f ? rr - 1.0f : rr) : (du > 0.f ? rr + 1.0f : rr);
     // column l = ceil(sqrt(w)) (or floor): certified when w is farther than Ew from
     // every perfect square (fl^2 is exact); sqrt only proposes fl, the squares decide
     const float wc = fmaxf(wval, 0.0f);
     const float v = wc * rsqrtf(fmaxf(wc, 1e-30f));
     const float fl = rint_magic(v - 0.5f);
     const float dlo = fmaf(-fl, fl, wval), dhi = fmaf(fl + 1.0f, fl + 1.0f, -wval);
-    bool lu = false;
-    if (wval < -p.Ew_a) l = 0;
-    else if (dlo > p.Ew_a && dhi > p.Ew_a) l = (int)fl + (p.floor_bins ? 0 : 1);
-    else lu = true;
-    if (!lu && l >= W) return;
-    unc = unc || ku || lu;
+    float lf = (wval < -p.Ew_a) ? 0.0f : fl + (p.floor_bins ? 0.0f : 1.0f);
+    const bool lu = !((wval < -p.Ew_a) | ((dlo > p.Ew_a) & (dhi > p.Ew_a))) & !self;
+    if (self) { kf = (float)p.self_k; lf = 0.0f; }
+    const bool kout = (kf < 0.0f) | (kf >= Wf);
+    if (!unc && ((!ku && kout) || (!lu && lf >= Wf))) return;       // certainly outside
+    unc = unc | ku | lu;
+    k = (int)kf;
+    l = (int)lf;
   } else {
-    // BILINEAR region 0 <= u < W-1, w < (W-1)^2  (#12)
-    const bool uu = !(fabsf(uval) > p.Eu_a && fabsf(uval - Wm1) > p.Eu_a);
-    if (!uu && !(uval > 0.f && uval < Wm1)) return;
+    // BILINEAR region 0 <= u < W-1, w < (W-1)^2  (#12); the self pair (u = W/2, w = 0)
+    // is interior for W >= 3 and needs no special case
+    const bool uu = !((fabsf(uval) > p.Eu_a) & (fabsf(uval - Wm1) > p.Eu_a));
     const float lim = Wm1 * Wm1;
     const bool wu = !(fabsf(wval - lim) > p.Ew_a);
-    if (!wu && !(wval < lim)) return;
-    unc = unc || uu || wu;
+    if (!unc && ((!uu && !((uval > 0.f) & (uval < Wm1))) || (!wu && !(wval < lim)))) return;
+    unc = unc | uu | wu;
   }
   if (unc) {
     ++ct.f64;
