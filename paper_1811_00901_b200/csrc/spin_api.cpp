@@ -44,7 +44,6 @@ spin_status cuda_fail(cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail(e_, what);   \
   } while (0)
 
-constexpr int TILE_POINTS = 256 * 4;  // NT * KP of the kernel
 constexpr double U32 = 5.9604644775390625e-08;  // 2^-24
 
 template <typename T>
@@ -194,6 +193,7 @@ namespace {
 spin_status load_cloud(spin_ctx* h, const float* points, const float* normals, int64_t N,
                        cudaStream_t s) {
   if (!points || !normals) return fail(SPIN_E_INVAL, "points/normals must be non-null");
+  const int64_t TILE_POINTS = tile_points();
   if (N < 1 || N >= ((int64_t)1 << 31) - 2 * TILE_POINTS)
     return fail(SPIN_E_INVAL, "N=%lld outside [1, 2^31)", (long long)N);
   const int64_t Npad = ((N + 1 + TILE_POINTS - 1) / TILE_POINTS) * TILE_POINTS;  // >= 1 sentinel
@@ -553,7 +553,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   if (prune == SPIN_BRUTE) {
     p.pos = h->pos;
     p.nrm = h->nrm;
-    p.n_tiles = (int32_t)(((h->N + TILE_POINTS - 1) / TILE_POINTS));
+    p.n_tiles = (int32_t)(((h->N + tile_points() - 1) / tile_points()));
   } else {
     const float R = f32_up(rg.R * (1.0 + 1e-6) + 1e-30);
     spin_status st = ensure_grid(h, R, s, &grid_ms);

@@ -70,13 +70,14 @@ enum StatSlot {
 
 // Launch configuration chosen by the planner.
 struct LaunchCfg {
-  int G;           // images per group (8, 16, 32)
+  int G;           // images per group (4 .. 64)
   int threads;     // NT
   size_t smem;     // dynamic shared memory bytes
 };
 
 // ---- launchers implemented in spin_kernels.cu
 LaunchCfg choose_launch(int W, int mode, int prune);
+int tile_points();   // points per CTA tile (NT x KP)
 int occupancy_blocks(const LaunchCfg& lc, int W, int mode, int prune);
 cudaError_t launch_spin(const LaunchCfg& lc, int mode, int prune, int grid, const KParams& p,
                         cudaStream_t s);

@@ -22,13 +22,14 @@
 #include <cstdint>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 #include "spin_internal.h"
 #include "spin_exact.cuh"
 
 namespace spin {
 
-constexpr int NT = 256;           // threads per CTA
+constexpr int NT = 512;           // threads per CTA (one CTA per SM, 16 warps)
 constexpr int NWARP = NT / 32;
 constexpr int KP = 4;             // points per thread (register blocking)
 constexpr int CB_MAX = 8;         // centres per mask batch: CB * KP <= 32 bits
@@ -72,6 +73,41 @@ __device__ __forceinline__ unsigned pair_bit(unsigned mask, float s, float c, fl
   return mask;
 }
 
+// Packed fp32 (sm_100a FFMA2 / FMUL2): two points per instruction, a scalar centre
+// constant broadcast to both halves.  Halves one FP32 issue slot per pair.
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk2(float a, float b) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ f2 bc2(float a) { return pk2(a, a); }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ void up2(f2 v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+// pass = (s >= c) && (|beta''| <= h) && (-q'' >= -Qt): one predicate chain + one OR
+__device__ __forceinline__ unsigned pair_bit_n(unsigned mask, float s, float c, float abe, float h,
+                                               float qn, float nqt, unsigned bit) {
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.ge.f32 p, %1, %2;\n\t"
+      "setp.le.and.f32 p, %3, %4, p;\n\t"
+      "setp.ge.and.f32 p, %5, %6, p;\n\t"
+      "@p or.b32 %0, %0, %7;\n\t}"
+      : "+r"(mask)
+      : "f"(s), "f"(c), "f"(abe), "f"(h), "f"(qn), "f"(nqt), "r"(bit));
+  return mask;
+}
+
 // ------------------------------------------------------------------ smem layout
 struct Layout {
   size_t oA, oB, oP, oN, oM, oImg, oHi, oQ, oTP, oTN, oMask, oRowS, oRowO, total;
@@ -91,8 +127,8 @@ __host__ __device__ inline Layout make_layout(int G, int W, int mode, int prune)
   if (mode == 1) o = align16(o + 4 * ((WW + 1) / 2) * G);
   L.oQ = o; o += 2 * (size_t)QCAP * NWARP;
   o = align16(o);
-  L.oTP = o; o += 16 * (size_t)32 * KP * NWARP;    // per-warp staged tile: positions
-  L.oTN = o; o += 16 * (size_t)32 * KP * NWARP;    //                      normals
+  L.oTP = o; o += 32 * (size_t)32 * KP * NWARP;    // per-warp staged tile, pair layout (32 B/point)
+  L.oTN = o;
   L.oMask = o; o += 4 * (size_t)32 * (G / cb_of(G)) * NWARP;   // per-warp pass masks of the tile
   L.oRowS = o;
   L.oRowO = o;
@@ -224,7 +260,7 @@ __device__ __forceinline__ void accept_pair(const KParams& p, const float4 P4, c
 
 // ------------------------------------------------------------------ the kernel
 template <int MODE, int PRUNE, int G>
-__global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__ KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_chunk;
   __shared__ int s_total, s_live;
@@ -246,8 +282,10 @@ __global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint16_t* sQ = reinterpret_cast<uint16_t*>(smem + L.oQ) + warp * QCAP;
-  float4* sTP = reinterpret_cast<float4*>(smem + L.oTP) + warp * 32 * KP;
-  float4* sTN = reinterpret_cast<float4*>(smem + L.oTN) + warp * 32 * KP;
+  // staged tile of this warp in pair layout: record r (0..3) of point pair pr (0..KP/2-1)
+  // of lane l at sT[(r * (KP/2) + pr) * 32 + l]; r0 {x,x',y,y'}, r1 {z,z',-|x|^2,-|x'|^2},
+  // r2 {nx,nx',ny,ny'}, r3 {nz,nz',0,0}
+  float4* sT = reinterpret_cast<float4*>(smem + L.oTP) + warp * 32 * KP * 2;
   constexpr int CB = cb_of(G);
   unsigned* sMask = reinterpret_cast<unsigned*>(smem + L.oMask) + warp * 32 * (G / CB);
   const int hiWords = (WW + 1) / 2;
@@ -276,7 +314,7 @@ __global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__
       // ---- a7: group setup (tempSpinImage, init, P = OP[i])
       if (tid < G) {
         const int slot = tid;
-        float4 A4 = make_float4(0.f, 0.f, 0.f, 0.f), B4 = make_float4(0.f, 0.f, 0.f, -INFINITY);
+        float4 A4 = make_float4(0.f, 0.f, 0.f, 0.f), B4 = make_float4(0.f, 0.f, 0.f, INFINITY);
         float4 P4 = make_float4(0.f, 0.f, 0.f, 0.f), N4 = make_float4(0.f, 0.f, 0.f, 0.f);
         int mm = -1;
         if (slot < gcount) {
@@ -292,9 +330,10 @@ __global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__
             const double C = (px * px + py * py + pz * pz) + 2.0 * mid * np + mid * mid;
             const double Qt = p.Qmax - C + p.Eq_hot + 1e-12 * (fabs(C) + p.Qmax);
             A4 = make_float4(N4.x, N4.y, N4.z, __double2float_rn(-np - mid));
-            B4 = make_float4(__double2float_rn(-2.0 * (px + mid * nx)),
-                             __double2float_rn(-2.0 * (py + mid * ny)),
-                             __double2float_rn(-2.0 * (pz + mid * nz)), __double2float_ru(Qt));
+            // negated t-chain: -t = 2(p + mid n).x - |x|^2, tested as -q'' >= -Qt
+            B4 = make_float4(__double2float_rn(2.0 * (px + mid * nx)),
+                             __double2float_rn(2.0 * (py + mid * ny)),
+                             __double2float_rn(2.0 * (pz + mid * nz)), __double2float_rd(-Qt));
             mm = m;
           } else {
             atomicOr(&p.err_flags[0], 1);
@@ -315,11 +354,16 @@ __global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__
         __syncthreads();
         // bounding box of the live centres, grown by R (rounded outward)
         if (warp == 0) {
-          float lo[3], hi3[3];
-          const bool live = lane < G && sM[lane] >= 0;
-          const float4 P4 = live ? sP[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-          lo[0] = live ? P4.x : INFINITY; lo[1] = live ? P4.y : INFINITY; lo[2] = live ? P4.z : INFINITY;
-          hi3[0] = live ? P4.x : -INFINITY; hi3[1] = live ? P4.y : -INFINITY; hi3[2] = live ? P4.z : -INFINITY;
+          float lo[3] = {INFINITY, INFINITY, INFINITY}, hi3[3] = {-INFINITY, -INFINITY, -INFINITY};
+          bool live = false;
+          for (int sl = lane; sl < G; sl += 32) {
+            if (sM[sl] >= 0) {
+              const float4 P4 = sP[sl];
+              live = true;
+              lo[0] = fminf(lo[0], P4.x); lo[1] = fminf(lo[1], P4.y); lo[2] = fminf(lo[2], P4.z);
+              hi3[0] = fmaxf(hi3[0], P4.x); hi3[1] = fmaxf(hi3[1], P4.y); hi3[2] = fmaxf(hi3[2], P4.z);
+            }
+          }
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
@@ -359,7 +403,11 @@ __global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__
         const int gs = (int)(e >> 7);
         const int src = (int)(e & 127u);
         const float4 P4 = sP[gs], N4 = sN[gs];
-        const float4 X4 = sTP[src], NX4 = sTN[src];
+        const int sl = src >> 2, kk = src & 3;                      // source lane, point k
+        const float* rec = reinterpret_cast<const float*>(sT + (kk >> 1) * 32 + sl) + (kk & 1);
+        constexpr int RS = (KP / 2) * 32 * 4;                       // floats between records
+        const float4 X4 = make_float4(rec[0], rec[2], rec[RS], 0.f);
+        const float4 NX4 = make_float4(rec[2 * RS], rec[2 * RS + 2], rec[3 * RS], 0.f);
         accept_pair<MODE>(p, P4, N4, X4, NX4, sImg + gs * WW, sHi + gs * hiWords, ct);
       };
       auto compact_and_accept = [&]() {
@@ -438,15 +486,30 @@ __global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__
         }
       };
       auto run_tile = [&](const int (&j)[KP]) {
-        float x[KP], y[KP], z[KP], xx[KP], nx[KP], ny[KP], nz[KP];
+        // stage the tile in pair layout (also the accept path's copy), then read the
+        // records back so each f32x2 operand arrives as an aligned register pair
+        f2 X2[KP / 2], Y2[KP / 2], Z2[KP / 2], NXX2[KP / 2], NX2[KP / 2], NY2[KP / 2], NZ2[KP / 2];
 #pragma unroll
-        for (int k = 0; k < KP; ++k) {
-          const float4 a = __ldg(&p.pos[j[k]]);
-          const float4 b = __ldg(&p.nrm[j[k]]);
-          x[k] = a.x; y[k] = a.y; z[k] = a.z; xx[k] = a.w;
-          nx[k] = b.x; ny[k] = b.y; nz[k] = b.z;
-          sTP[lane * KP + k] = a;   // the previous tile's entries were all processed
-          sTN[lane * KP + k] = b;
+        for (int k = 0; k < KP; k += 2) {
+          const float4 a0 = __ldg(&p.pos[j[k]]), a1 = __ldg(&p.pos[j[k + 1]]);
+          const float4 b0 = __ldg(&p.nrm[j[k]]), b1 = __ldg(&p.nrm[j[k + 1]]);
+          const int pr = k / 2;
+          sT[(0 * (KP / 2) + pr) * 32 + lane] = make_float4(a0.x, a1.x, a0.y, a1.y);
+          sT[(1 * (KP / 2) + pr) * 32 + lane] = make_float4(a0.z, a1.z, -a0.w, -a1.w);
+          sT[(2 * (KP / 2) + pr) * 32 + lane] = make_float4(b0.x, b1.x, b0.y, b1.y);
+          sT[(3 * (KP / 2) + pr) * 32 + lane] = make_float4(b0.z, b1.z, 0.f, 0.f);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int pr = 0; pr < KP / 2; ++pr) {
+          f2 r[8];
+          const float4* base = sT + pr * 32 + lane;
+          asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r[0]), "=l"(r[1]) : "r"((unsigned)__cvta_generic_to_shared(base)));
+          asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r[2]), "=l"(r[3]) : "r"((unsigned)__cvta_generic_to_shared(base + (KP / 2) * 32)));
+          asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r[4]), "=l"(r[5]) : "r"((unsigned)__cvta_generic_to_shared(base + 2 * (KP / 2) * 32)));
+          asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r[6]), "=l"(r[7]) : "r"((unsigned)__cvta_generic_to_shared(base + 3 * (KP / 2) * 32)));
+          X2[pr] = r[0]; Y2[pr] = r[1]; Z2[pr] = r[2]; NXX2[pr] = r[3];
+          NX2[pr] = r[4]; NY2[pr] = r[5]; NZ2[pr] = r[6];
         }
         const float c_test = p.c_test, h_test = p.h_test;
 #pragma unroll 1
@@ -461,14 +524,20 @@ __global__ void __launch_bounds__(NT, 2) spin_persistent(const __grid_constant__
             const float4 A4 = sA[cb + c];
             const float4 B4 = sB[cb + c];
 #pragma unroll
-            for (int k = 0; k < KP; ++k) {
+            for (int k2 = 0; k2 < KP / 2; ++k2) {
               // support n.nx; beta'' = n.x - n.p - mid;
-              // q'' = |x|^2 - 2(p + mid n).x - beta''^2 = q - C
-              const float s = fmaf(A4.x, nx[k], fmaf(A4.y, ny[k], A4.z * nz[k]));
-              const float be = fmaf(A4.x, x[k], fmaf(A4.y, y[k], fmaf(A4.z, z[k], A4.w)));
-              const float t = fmaf(B4.x, x[k], fmaf(B4.y, y[k], fmaf(B4.z, z[k], xx[k])));
-              const float q = fmaf(-be, be, t);
-              mask = pair_bit(mask, s, c_test, fabsf(be), h_test, q, B4.w, 1u << (c * KP + k));
+              // -q'' = beta''^2 + 2(p + mid n).x - |x|^2 = C - q
+              const f2 s2 = fma2(bc2(A4.x), NX2[k2], fma2(bc2(A4.y), NY2[k2], mul2(bc2(A4.z), NZ2[k2])));
+              const f2 be2 = fma2(bc2(A4.x), X2[k2], fma2(bc2(A4.y), Y2[k2], fma2(bc2(A4.z), Z2[k2], bc2(A4.w))));
+              const f2 tn2 = fma2(bc2(B4.x), X2[k2], fma2(bc2(B4.y), Y2[k2], fma2(bc2(B4.z), Z2[k2], NXX2[k2])));
+              const f2 qn2 = fma2(be2, be2, tn2);
+              float s0, s1, b0, b1, q0, q1;
+              up2(s2, s0, s1);
+              up2(be2, b0, b1);
+              up2(qn2, q0, q1);
+              const int bit = c * KP + 2 * k2;
+              mask = pair_bit_n(mask, s0, c_test, fabsf(b0), h_test, q0, B4.w, 1u << bit);
+              mask = pair_bit_n(mask, s1, c_test, fabsf(b1), h_test, q1, B4.w, 1u << (bit + 1));
             }
           }
           sMask[(cb / CB) * 32 + lane] = mask;
@@ -608,7 +677,8 @@ static const void* kernel_ptr(int G) {
     case 4: return (const void*)spin_persistent<MODE, PRUNE, 4>;
     case 8: return (const void*)spin_persistent<MODE, PRUNE, 8>;
     case 16: return (const void*)spin_persistent<MODE, PRUNE, 16>;
-    default: return (const void*)spin_persistent<MODE, PRUNE, 32>;
+    case 32: return (const void*)spin_persistent<MODE, PRUNE, 32>;
+    default: return (const void*)spin_persistent<MODE, PRUNE, 64>;
   }
 }
 static const void* kernel_for(int mode, int prune, int G) {
@@ -617,18 +687,20 @@ static const void* kernel_for(int mode, int prune, int G) {
 }
 
 LaunchCfg choose_launch(int W, int mode, int prune) {
-  // Images live in shared memory (NEAREST 4 B/bin, BILINEAR 6 B/bin).  Take the
-  // largest G in {32, 16, 8} whose whole layout lets two CTAs share an SM
-  // (2 x (smem + 1 KB reserved) <= 228 KB); W = 64 falls back to one CTA per SM.
-  int G = 32;
-  while (G > 8 && make_layout(G, W, mode, prune).total > 112 * 1024) G >>= 1;
-  if (make_layout(G, W, mode, prune).total > 220 * 1024) G = 4;   // W = 64 BILINEAR
+  // One 512-thread CTA per SM.  Images live in shared memory (NEAREST 4 B/bin,
+  // BILINEAR 6 B/bin); take the largest G in {64, 32, 16, 8, 4} whose layout fits.
+  int G = 64;
+  if (prune == 1) G = 32;   // CELLS: larger groups grow the visited box (measured: 32 best)
+  if (const char* g = std::getenv("SPIN_DEBUG_G")) G = std::atoi(g);   // measurement knob
+  while (G > 4 && make_layout(G, W, mode, prune).total > 220 * 1024) G >>= 1;
   LaunchCfg lc;
   lc.G = G;
   lc.threads = NT;
   lc.smem = make_layout(G, W, mode, prune).total;
   return lc;
 }
+
+int tile_points() { return NT * KP; }
 
 int occupancy_blocks(const LaunchCfg& lc, int W, int mode, int prune) {
   const void* f = kernel_for(mode, prune, lc.G);
