@@ -202,7 +202,7 @@ __device__ __forceinline__ void accept_pair(const KParams& p, const float4 P4, c
   int k = 0, l = 0;
   if (MODE == 0) {
     // the self pair (d == 0): beta = q = 0 exactly, k = ceil(W/2) (or floor), l = 0 (#8)
-    const bool self = (d0 == 0.f) & (d1 == 0.f) & (d2 == 0.f) & (p.self_fast != 0);
+    const bool self = (fabsf(d0) + fabsf(d1) + fabsf(d2) == 0.f) & (p.self_fast != 0);
     // row k = ceil(u) (or floor): certified when u is farther than Eu from an integer
     const float uc = fminf(fmaxf(uval, -4.0f), Wf + 4.0f);
     const float rr = rint_magic(uc);
@@ -212,7 +212,9 @@ __device__ __forceinline__ void accept_pair(const KParams& p, const float4 P4, c
     // column l = ceil(sqrt(w)) (or floor): certified when w is farther than Ew from
     // every perfect square (fl^2 is exact); sqrt only proposes fl, the squares decide
     const float wc = fmaxf(wval, 0.0f);
-    const float v = wc * rsqrtf(fmaxf(wc, 1e-30f));
+    float rs;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(fmaxf(wc, 1e-30f)));   // proposes fl only
+    const float v = wc * rs;
     const float fl = rint_magic(v - 0.5f);
     const float dlo = fmaf(-fl, fl, wval), dhi = fmaf(fl + 1.0f, fl + 1.0f, -wval);
     float lf = (wval < -p.Ew_a) ? 0.0f : fl + (p.floor_bins ? 0.0f : 1.0f);
