@@ -178,6 +178,7 @@ struct spin_ctx {
   bool err_pending = false;
   unsigned long long* cta_t0 = nullptr; unsigned long long* cta_t1 = nullptr;
   int32_t* cta_units = nullptr; int64_t cta_cap = 0;
+  uint32_t* hi_scratch = nullptr; int64_t hi_cap = 0;   // kept zero between launches
   // cloud staging (AoS input) and reductions
   float* stage_p = nullptr; int64_t stage_p_cap = 0;
   float* stage_n = nullptr; int64_t stage_n_cap = 0;
@@ -378,7 +379,7 @@ void spin_destroy(spin_handle h) {
   void* ptrs[] = {h->pos, h->nrm, h->cell_start, h->spos, h->snrm, h->keys, h->counts,
                   h->cursor, h->scan_tmp, h->ckeys, h->cstarts, h->order, h->bounds,
                   h->counter, h->stats, h->err, h->cta_t0, h->cta_t1, h->cta_units, h->cidx,
-                  h->outbuf, h->stage_p, h->stage_n, h->red};
+                  h->outbuf, h->stage_p, h->stage_n, h->red, h->hi_scratch};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->h_err) cudaFreeHost(h->h_err);
@@ -548,6 +549,15 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   p.cta_t1 = h->cta_t1;
   p.cta_units = h->cta_units;
   p.err_flags = h->err;
+  if (mode == SPIN_BILINEAR) {
+    const int64_t need = (int64_t)P * lc.G * ((W * W + 1) / 2);
+    if (need > h->hi_cap) {
+      spin_status st = ensure(h->hi_scratch, h->hi_cap, need, "carry scratch");
+      if (st != SPIN_OK) return st;
+      CK(cudaMemsetAsync(h->hi_scratch, 0, need * sizeof(uint32_t), s), "memset");
+    }
+    p.hi_scratch = h->hi_scratch;
+  }
   p.row_cap = 256;
   double grid_ms = 0.0;
   if (prune == SPIN_BRUTE) {

@@ -62,6 +62,7 @@ struct KParams {
   unsigned long long* cta_t1;              // [P]
   int32_t* cta_units;                      // [P]
   int32_t* err_flags;                      // [0]: bad centre index seen; [1]: overflow
+  uint32_t* hi_scratch;                    // BILINEAR carry words, [P][G][(W*W+1)/2], zero
 };
 
 enum StatSlot {

@@ -29,12 +29,14 @@
 
 namespace spin {
 
-constexpr int NT = 512;           // threads per CTA (one CTA per SM, 16 warps)
+constexpr int NT = 768;           // threads per CTA (one CTA per SM, 24 warps)
 constexpr int NWARP = NT / 32;
 constexpr int KP = 4;             // points per thread (register blocking)
 constexpr int CB_MAX = 8;         // centres per mask batch: CB * KP <= 32 bits
 __host__ __device__ constexpr int cb_of(int G) { return G < CB_MAX ? G : CB_MAX; }
-constexpr int QCAP = 1024;        // per-warp candidate ring of u16 entries (power of two)
+// per-warp candidate ring of u16 entries (power of two): BRUTE tiles hold few candidates
+// (~2% of pairs), CELLS tiles in dense clusters many
+__host__ __device__ constexpr int qcap_of(int prune) { return prune ? 1024 : 512; }
 constexpr int ROWCAP = NT;        // CELLS: grid rows staged per batch
 
 static_assert(CB_MAX * KP == 32, "mask is one u32");
@@ -124,8 +126,7 @@ __host__ __device__ inline Layout make_layout(int G, int W, int mode, int prune)
   const size_t WW = (size_t)W * W;
   L.oImg = o; o = align16(o + 4 * WW * G);
   L.oHi = o;
-  if (mode == 1) o = align16(o + 4 * ((WW + 1) / 2) * G);
-  L.oQ = o; o += 2 * (size_t)QCAP * NWARP;
+  L.oQ = o; o += 2 * (size_t)qcap_of(prune) * NWARP;
   o = align16(o);
   L.oTP = o; o += 32 * (size_t)32 * KP * NWARP;    // per-warp staged tile, pair layout (32 B/point)
   L.oTN = o;
@@ -147,17 +148,20 @@ struct Ctr {
   unsigned cand, acc, f64, exact;
 };
 
-// BILINEAR accumulator: 2^-23 fixed point, 32-bit low word + 16-bit carry word
-// packed two bins per u32.  round(w * 2^23) for w in [0,1] is the mantissa of 1 + w.
+// BILINEAR accumulator: 2^-23 fixed point.  The 32-bit low words live in shared
+// memory; the rare carries (one per 512 units of weight in a bin) go to 16-bit carry
+// words (two bins per u32) in a per-CTA global scratch that is zero between groups,
+// and raise a shared flag so that only groups with carries read or clear it.
+// round(w * 2^23) for w in [0,1] is the mantissa of 1 + w.
 __device__ __forceinline__ void add_fixed(uint32_t* lo, uint32_t* hi, int bin, float w,
-                                          int32_t* err) {
-  uint32_t v = __float_as_uint(w + 1.0f) - 0x3f800000u;
-  if (v == 0u) return;
-  uint32_t old = atomicAdd(&lo[bin], v);
+                                          int32_t* err, int* carry_flag) {
+  const uint32_t v = __float_as_uint(w + 1.0f) - 0x3f800000u;
+  const uint32_t old = atomicAdd(&lo[bin], v);
   if (old + v < old) {
-    uint32_t sh = (uint32_t)(bin & 1) * 16u;
-    uint32_t prev = atomicAdd(&hi[bin >> 1], 1u << sh);
+    const uint32_t sh = (uint32_t)(bin & 1) * 16u;
+    const uint32_t prev = atomicAdd(&hi[bin >> 1], 1u << sh);
     if (((prev >> sh) & 0xffffu) == 0xffffu) atomicOr(&err[1], 1);
+    *carry_flag = 1;
   }
 }
 
@@ -184,7 +188,7 @@ __device__ __noinline__ SlowOut slow_pair(float4 P4, float4 N4, float4 X4, float
 template <int MODE>
 __device__ __forceinline__ void accept_pair(const KParams& p, const float4 P4, const float4 N4,
                                             const float4 X4, const float4 NX4, uint32_t* img,
-                                            uint32_t* hi, Ctr& ct) {
+                                            uint32_t* hi, int* carry_flag, Ctr& ct) {
   const int W = p.W;
   const float Wf = (float)W, Wm1 = Wf - 1.0f;
   ++ct.cand;
@@ -253,10 +257,10 @@ __device__ __forceinline__ void accept_pair(const KParams& p, const float4 P4, c
     const float a = fminf(fmaxf(uval - fi, 0.0f), 1.0f);
     const float c = fminf(fmaxf(v - fj, 0.0f), 1.0f);
     const int bin = (int)fi * W + (int)fj;
-    add_fixed(img, hi, bin, (1.0f - a) * (1.0f - c), p.err_flags);
-    add_fixed(img, hi, bin + W, a * (1.0f - c), p.err_flags);
-    add_fixed(img, hi, bin + 1, (1.0f - a) * c, p.err_flags);
-    add_fixed(img, hi, bin + W + 1, a * c, p.err_flags);
+    add_fixed(img, hi, bin, (1.0f - a) * (1.0f - c), p.err_flags, carry_flag);
+    add_fixed(img, hi, bin + W, a * (1.0f - c), p.err_flags, carry_flag);
+    add_fixed(img, hi, bin + 1, (1.0f - a) * c, p.err_flags, carry_flag);
+    add_fixed(img, hi, bin + W + 1, a * c, p.err_flags, carry_flag);
   }
 }
 
@@ -278,11 +282,12 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   float4* sN = reinterpret_cast<float4*>(smem + L.oN);
   int* sM = reinterpret_cast<int*>(smem + L.oM);
   uint32_t* sImg = reinterpret_cast<uint32_t*>(smem + L.oImg);
-  uint32_t* sHi = reinterpret_cast<uint32_t*>(smem + L.oHi);
+  __shared__ int s_carry;
   int* sRowS = reinterpret_cast<int*>(smem + L.oRowS);
   int* sRowO = reinterpret_cast<int*>(smem + L.oRowO);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int QCAP = qcap_of(PRUNE);
   uint16_t* sQ = reinterpret_cast<uint16_t*>(smem + L.oQ) + warp * QCAP;
   // staged tile of this warp in pair layout: record r (0..3) of point pair pr (0..KP/2-1)
   // of lane l at sT[(r * (KP/2) + pr) * 32 + l]; r0 {x,x',y,y'}, r1 {z,z',-|x|^2,-|x'|^2},
@@ -291,6 +296,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   constexpr int CB = cb_of(G);
   unsigned* sMask = reinterpret_cast<unsigned*>(smem + L.oMask) + warp * 32 * (G / CB);
   const int hiWords = (WW + 1) / 2;
+  uint32_t* gHi = p.hi_scratch + (size_t)blockIdx.x * G * hiWords;   // zero outside groups
+  if (tid == 0) s_carry = 0;
 
   if (tid < 5) s_ctr[tid] = 0ull;
   const unsigned long long t0 = gtimer();
@@ -349,8 +356,6 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         sM[slot] = mm;
       }
       for (int i = tid; i < G * WW; i += NT) sImg[i] = 0u;
-      if (MODE == 1)
-        for (int i = tid; i < G * hiWords; i += NT) sHi[i] = 0u;
       int nrows = 0;
       if (PRUNE == 1) {
         __syncthreads();
@@ -410,7 +415,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         constexpr int RS = (KP / 2) * 32 * 4;                       // floats between records
         const float4 X4 = make_float4(rec[0], rec[2], rec[RS], 0.f);
         const float4 NX4 = make_float4(rec[2 * RS], rec[2 * RS + 2], rec[3 * RS], 0.f);
-        accept_pair<MODE>(p, P4, N4, X4, NX4, sImg + gs * WW, sHi + gs * hiWords, ct);
+        accept_pair<MODE>(p, P4, N4, X4, NX4, sImg + gs * WW, gHi + gs * hiWords, &s_carry, ct);
       };
       auto compact_and_accept = [&]() {
         unsigned mw[NWD];
@@ -641,11 +646,20 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           if (cnt >= (1u << 24)) atomicOr(&p.err_flags[1], 1);
           val = (float)cnt;
         } else {
-          const uint32_t h = (sHi[slot * hiWords + (e >> 1)] >> ((e & 1) * 16)) & 0xffffu;
+          const uint32_t h =
+              s_carry ? (gHi[slot * hiWords + (e >> 1)] >> ((e & 1) * 16)) & 0xffffu : 0u;
           const double fx = (double)h * 4294967296.0 + (double)sImg[i];
           val = (float)(fx * (1.0 / 8388608.0));
         }
         __stcs(&p.out[(long long)mm * WW + e], val);
+      }
+      if (MODE == 1) {
+        __syncthreads();
+        if (s_carry) {                       // leave the carry scratch zero for the next group
+          for (int i = tid; i < G * hiWords; i += NT) gHi[i] = 0u;
+          __syncthreads();
+          if (tid == 0) s_carry = 0;
+        }
       }
       __syncthreads();
     }

@@ -367,3 +367,19 @@ def test_config4_full_sampled(spin, torch):
 @pytest.mark.parametrize("W", [8, 24])
 def test_config5_full_sampled(spin, torch, W):
     _full(spin, torch, 5, "nearest", "cells", 20, W=W, sched="GSS")
+
+
+def test_bilinear_fixed_point_carries(spin, torch):
+    """> 512 units of weight in one bin exercise the 2^-23 fixed-point carry words."""
+    rng = np.random.default_rng(21)
+    n = 4000
+    P = (rng.normal(size=(n, 3)) * 1e-3).astype(np.float32)
+    Nn = np.tile(np.array([0, 0, 1], np.float32), (n, 1))
+    cen = np.arange(0, n, 400, dtype=np.int32)
+    for W, b in ((4, 1.0), (6, 0.0013)):
+        gpu = run_gpu(spin, torch, P, Nn, cen, W, b, 0.5, "bilinear")
+        ora, st = oracle(P, Nn, cen, W, b, 0.5, "bilinear")
+        assert ora.max() > 600
+        check(gpu, ora, st, "bilinear", f"carries W={W}")
+        again = run_gpu(spin, torch, P, Nn, cen, W, b, 0.5, "bilinear", schedule="SS", unit=1)
+        np.testing.assert_array_equal(again, gpu)    # deterministic (integer accumulation)
