@@ -183,27 +183,34 @@ __device__ __noinline__ SlowOut slow_pair(float4 P4, float4 N4, float4 X4, float
   return slow_decide(D, W, A, b, cos_As, has_support, literal, floor_bins, mode);
 }
 
-// One candidate (centre slot g, point X): certified fp32 decision, fallbacks, splat.
-// Branch-light: one early exit for certain rejections, one branch to the slow stages.
+// One candidate (centre slot g, point X): the certified fp32 decision, branch-free.
+//   status 0: certainly no contribution; 1: contributes (bin / weights below);
+//   2: some decision is not certified in fp32 -> slow_pair (fp64, then exact).
+struct Dec {
+  int status;
+  int bin;      // NEAREST: k*W + l; BILINEAR: i0*W + j0
+  float a, c;   // BILINEAR fractional offsets along k and l
+};
+
 template <int MODE>
-__device__ __forceinline__ void accept_pair(const KParams& p, const float4 P4, const float4 N4,
-                                            const float4 X4, const float4 NX4, uint32_t* img,
-                                            uint32_t* hi, int* carry_flag, Ctr& ct) {
+__device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const float4 N4,
+                                      const float4 X4, const float4 NX4) {
   const int W = p.W;
   const float Wf = (float)W, Wm1 = Wf - 1.0f;
-  ++ct.cand;
   const float d0 = __fsub_rn(X4.x, P4.x), d1 = __fsub_rn(X4.y, P4.y), d2 = __fsub_rn(X4.z, P4.z);
   // support test, inclusive, cosine form (#5); c_f = -inf disables it (ds = +inf)
   const float s = fmaf(N4.x, NX4.x, fmaf(N4.y, NX4.y, N4.z * NX4.z));
   const float ds = s - p.c_f;
-  if (ds < -p.Es_a) return;                                          // certainly rejected
+  const bool sup_out = ds < -p.Es_a;                                 // certainly rejected
   const float be = fmaf(N4.x, d0, fmaf(N4.y, d1, N4.z * d2));       // np_i.(X-P)
   const float dd = fmaf(d0, d0, fmaf(d1, d1, d2 * d2));              // ||X-P||^2
   const float q = fmaf(-be, be, dd);                                 // alpha^2
   const float uval = p.literal ? (p.Af - be) * p.inv_b : fmaf(-be, p.inv_b, p.Af);
   const float wval = q * p.inv_b2;                                   // (alpha/b)^2
-  bool unc = (p.no_fast_cert != 0) | !(ds > p.Es_a) | !(dd <= p.D2g);
-  int k = 0, l = 0;
+  const bool unc0 = (p.no_fast_cert != 0) | !(ds > p.Es_a) | !(dd <= p.D2g);
+  Dec r;
+  r.a = 0.f;
+  r.c = 0.f;
   if (MODE == 0) {
     // the self pair (d == 0): beta = q = 0 exactly, k = ceil(W/2) (or floor), l = 0 (#8)
     const bool self = (fabsf(d0) + fabsf(d1) + fabsf(d2) == 0.f) & (p.self_fast != 0);
@@ -217,50 +224,60 @@ __device__ __forceinline__ void accept_pair(const KParams& p, const float4 P4, c
     // every perfect square (fl^2 is exact); sqrt only proposes fl, the squares decide
     const float wc = fmaxf(wval, 0.0f);
     float rs;
-    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(fmaxf(wc, 1e-30f)));   // proposes fl only
-    const float v = wc * rs;
-    const float fl = rint_magic(v - 0.5f);
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(fmaxf(wc, 1e-30f)));
+    const float fl = rint_magic(wc * rs - 0.5f);
     const float dlo = fmaf(-fl, fl, wval), dhi = fmaf(fl + 1.0f, fl + 1.0f, -wval);
-    float lf = (wval < -p.Ew_a) ? 0.0f : fl + (p.floor_bins ? 0.0f : 1.0f);
-    const bool lu = !((wval < -p.Ew_a) | ((dlo > p.Ew_a) & (dhi > p.Ew_a))) & !self;
+    const bool wneg = wval < -p.Ew_a;
+    float lf = wneg ? 0.0f : fl + (p.floor_bins ? 0.0f : 1.0f);
+    const bool lu = !(wneg | ((dlo > p.Ew_a) & (dhi > p.Ew_a))) & !self;
     if (self) { kf = (float)p.self_k; lf = 0.0f; }
-    const bool kout = (kf < 0.0f) | (kf >= Wf);
-    if (!unc && ((!ku && kout) || (!lu && lf >= Wf))) return;       // certainly outside
-    unc = unc | ku | lu;
-    k = (int)kf;
-    l = (int)lf;
+    const bool out = (!ku & ((kf < 0.0f) | (kf >= Wf))) | (!lu & (lf >= Wf));
+    const bool unc = unc0 | ku | lu;
+    r.status = (sup_out | (!unc0 & out)) ? 0 : (unc ? 2 : 1);
+    r.bin = (int)kf * W + (int)lf;
   } else {
     // BILINEAR region 0 <= u < W-1, w < (W-1)^2  (#12); the self pair (u = W/2, w = 0)
     // is interior for W >= 3 and needs no special case
     const bool uu = !((fabsf(uval) > p.Eu_a) & (fabsf(uval - Wm1) > p.Eu_a));
     const float lim = Wm1 * Wm1;
     const bool wu = !(fabsf(wval - lim) > p.Ew_a);
-    if (!unc && ((!uu && !((uval > 0.f) & (uval < Wm1))) || (!wu && !(wval < lim)))) return;
-    unc = unc | uu | wu;
-  }
-  if (unc) {
-    ++ct.f64;
-    const SlowOut r = slow_pair(P4, N4, X4, NX4, W, p.A, p.b, p.cos_As, p.has_support, p.literal,
-                                p.floor_bins, MODE);
-    ct.exact += r.n_exact;
-    if (!r.accept) return;
-    k = r.k;
-    l = r.l;
-  }
-  ++ct.acc;
-  if (MODE == 0) {
-    atomicAdd(&img[k * W + l], 1u);                                  // tempSpinImage[k,l]++
-  } else {
+    const bool out = (!uu & !((uval > 0.f) & (uval < Wm1))) | (!wu & !(wval < lim));
+    const bool unc = unc0 | uu | wu;
+    r.status = (sup_out | (!unc0 & out)) ? 0 : (unc ? 2 : 1);
     const float v = sqrtf(fmaxf(wval, 0.0f));
     const float fi = fminf(fmaxf(rint_magic(uval - 0.5f), 0.0f), Wm1 - 1.0f);
     const float fj = fminf(fmaxf(rint_magic(v - 0.5f), 0.0f), Wm1 - 1.0f);
-    const float a = fminf(fmaxf(uval - fi, 0.0f), 1.0f);
-    const float c = fminf(fmaxf(v - fj, 0.0f), 1.0f);
-    const int bin = (int)fi * W + (int)fj;
-    add_fixed(img, hi, bin, (1.0f - a) * (1.0f - c), p.err_flags, carry_flag);
-    add_fixed(img, hi, bin + W, a * (1.0f - c), p.err_flags, carry_flag);
-    add_fixed(img, hi, bin + 1, (1.0f - a) * c, p.err_flags, carry_flag);
-    add_fixed(img, hi, bin + W + 1, a * c, p.err_flags, carry_flag);
+    r.a = fminf(fmaxf(uval - fi, 0.0f), 1.0f);
+    r.c = fminf(fmaxf(v - fj, 0.0f), 1.0f);
+    r.bin = (int)fi * W + (int)fj;
+  }
+  return r;
+}
+
+// Resolve an uncertain decision in fp64 / exactly (out of line, rare).
+template <int MODE>
+__device__ __forceinline__ void resolve(const KParams& p, Dec& d, const float4 P4, const float4 N4,
+                                        const float4 X4, const float4 NX4, Ctr& ct) {
+  ++ct.f64;
+  const SlowOut r = slow_pair(P4, N4, X4, NX4, p.W, p.A, p.b, p.cos_As, p.has_support, p.literal,
+                              p.floor_bins, MODE);
+  ct.exact += r.n_exact;
+  d.status = r.accept;
+  if (MODE == 0) d.bin = r.k * p.W + r.l;
+}
+
+// Splat an accepted pair into its image (tempSpinImage[k,l]++).
+template <int MODE>
+__device__ __forceinline__ void apply(const KParams& p, const Dec& d, uint32_t* img, uint32_t* hi,
+                                      int* carry_flag) {
+  if (MODE == 0) {
+    atomicAdd(&img[d.bin], 1u);
+  } else {
+    const int W = p.W;
+    add_fixed(img, hi, d.bin, (1.0f - d.a) * (1.0f - d.c), p.err_flags, carry_flag);
+    add_fixed(img, hi, d.bin + W, d.a * (1.0f - d.c), p.err_flags, carry_flag);
+    add_fixed(img, hi, d.bin + 1, (1.0f - d.a) * d.c, p.err_flags, carry_flag);
+    add_fixed(img, hi, d.bin + W + 1, d.a * d.c, p.err_flags, carry_flag);
   }
 }
 
@@ -405,26 +422,48 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       // point from the warp's staged copy of the tile (no global re-load).
       unsigned qhead = 0, qtail = 0;
       constexpr int NWD = G / CB;                      // mask words per lane per tile
-      auto process_entry = [&](unsigned e) {
-        if (p.debug_skip) return;
+      // candidate operands: centre slot gs, point (source lane, k) from the staged tile
+      auto load_entry = [&](unsigned e, float4& P4, float4& N4, float4& X4, float4& NX4) {
         const int gs = (int)(e >> 7);
         const int src = (int)(e & 127u);
-        const float4 P4 = sP[gs], N4 = sN[gs];
+        P4 = sP[gs];
+        N4 = sN[gs];
         const int sl = src >> 2, kk = src & 3;                      // source lane, point k
         const float* rec = reinterpret_cast<const float*>(sT + (kk >> 1) * 32 + sl) + (kk & 1);
         constexpr int RS = (KP / 2) * 32 * 4;                       // floats between records
-        const float4 X4 = make_float4(rec[0], rec[2], rec[RS], 0.f);
-        const float4 NX4 = make_float4(rec[2 * RS], rec[2 * RS + 2], rec[3 * RS], 0.f);
-        accept_pair<MODE>(p, P4, N4, X4, NX4, sImg + gs * WW, gHi + gs * hiWords, &s_carry, ct);
+        X4 = make_float4(rec[0], rec[2], rec[RS], 0.f);
+        NX4 = make_float4(rec[2 * RS], rec[2 * RS + 2], rec[3 * RS], 0.f);
+      };
+      // CELLS (dense, latency-bound) takes two candidates per lane per pass so that the
+      // two independent decisions interleave; BRUTE keeps one (fewer live registers).
+      constexpr int APL = PRUNE == 1 ? 2 : 1;
+      auto process_pair = [&](unsigned e0, bool v0, unsigned e1, bool v1) {
+        if (p.debug_skip) return;
+        float4 P0, N0, X0, NX0, P1, N1, X1, NX1;
+        load_entry(e0, P0, N0, X0, NX0);
+        Dec d0 = decide<MODE>(p, P0, N0, X0, NX0);
+        Dec d1;
+        d1.status = 0;
+        if (APL == 2) {
+          load_entry(e1, P1, N1, X1, NX1);
+          d1 = decide<MODE>(p, P1, N1, X1, NX1);
+          if (!v1) d1.status = 0;
+        }
+        if (!v0) d0.status = 0;
+        ct.cand += (unsigned)v0 + (APL == 2 ? (unsigned)v1 : 0u);
+        if (d0.status == 2) resolve<MODE>(p, d0, P0, N0, X0, NX0, ct);
+        if (APL == 2 && d1.status == 2) resolve<MODE>(p, d1, P1, N1, X1, NX1, ct);
+        const int g0 = (int)(e0 >> 7), g1 = (int)(e1 >> 7);
+        if (d0.status) { ++ct.acc; apply<MODE>(p, d0, sImg + g0 * WW, gHi + g0 * hiWords, &s_carry); }
+        if (APL == 2 && d1.status) {
+          ++ct.acc;
+          apply<MODE>(p, d1, sImg + g1 * WW, gHi + g1 * hiWords, &s_carry);
+        }
       };
       auto compact_and_accept = [&]() {
-        unsigned mw[NWD];
         int cnt = 0;
 #pragma unroll
-        for (int w = 0; w < NWD; ++w) {
-          mw[w] = sMask[w * 32 + lane];
-          cnt += __popc(mw[w]);
-        }
+        for (int w = 0; w < NWD; ++w) cnt += __popc(sMask[w * 32 + lane]);
         int x = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -433,61 +472,65 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         }
         const int total = __shfl_sync(0xffffffffu, x, 31);
         if (total == 0) return;
-        bool more = false;
-        if (total <= QCAP) {
-          // common case: one scan gives every lane its slot range
-          unsigned pos = qtail + (unsigned)(x - cnt);
+        // common case: the whole tile fits the ring and one scan places every entry;
+        // dense tiles go a quarter mask word (2 centres, <= 256 entries) at a time, each
+        // appended after the ring was drained to < 64 pending entries (QCAP >= 512).
+        static_assert(QCAP >= 64 + 256, "ring too small for the dense path");
+        const bool dense = total > QCAP - 64;
+        const int nchunks = dense ? 4 * NWD : 1;
+        for (int ci = 0;;) {
+          if (ci < nchunks) {
+            if (!dense) {
+              unsigned pos = qtail + (unsigned)(x - cnt);
 #pragma unroll
-          for (int w = 0; w < NWD; ++w) {
-            unsigned m = mw[w];
-            while (m) {
-              const int bit = __ffs(m) - 1;
-              m &= m - 1u;
-              sQ[pos & (QCAP - 1)] =
-                  (uint16_t)(((w * CB + (bit >> 2)) << 7) | (lane << 2) | (bit & 3));
-              ++pos;
-            }
-            mw[w] = 0u;
-          }
-          qtail += (unsigned)total;
-        } else {
-          more = true;   // dense tile (CELLS clusters): fill the ring round by round
-        }
-        for (;;) {
-          if (more) {
-            while (qtail - qhead <= (unsigned)(QCAP - 32)) {
-              unsigned m = 0u;
-              int wsel = 0;
-#pragma unroll
-              for (int w = NWD - 1; w >= 0; --w)
-                if (mw[w]) { m = mw[w]; wsel = w; }
-              const unsigned ball = __ballot_sync(0xffffffffu, m != 0u);
-              if (!ball) break;
-              if (m) {
-                const int bit = __ffs(m) - 1;
-#pragma unroll
-                for (int w = 0; w < NWD; ++w)
-                  if (w == wsel) mw[w] &= mw[w] - 1u;
-                const unsigned slot = (qtail + __popc(ball & lanemask_lt())) & (QCAP - 1);
-                sQ[slot] = (uint16_t)(((wsel * CB + (bit >> 2)) << 7) | (lane << 2) | (bit & 3));
+              for (int w = 0; w < NWD; ++w) {
+                unsigned m = sMask[w * 32 + lane];
+                while (m) {
+                  const int bit = __ffs(m) - 1;
+                  m &= m - 1u;
+                  sQ[pos & (QCAP - 1)] =
+                      (uint16_t)(((w * CB + (bit >> 2)) << 7) | (lane << 2) | (bit & 3));
+                  ++pos;
+                }
               }
-              qtail += __popc(ball);
-            }
-            unsigned any = 0u;
+              qtail += (unsigned)total;
+            } else {
+              const int quarter = ci & 3;
+              unsigned m = (sMask[(ci >> 2) * 32 + lane] >> (8 * quarter)) & 0xffu;
+              const int c2 = __popc(m);
+              int x2 = c2;
 #pragma unroll
-            for (int w = 0; w < NWD; ++w) any |= mw[w];
-            more = __any_sync(0xffffffffu, any != 0u);
+              for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x2, o);
+                if (lane >= o) x2 += y;
+              }
+              const int t2 = __shfl_sync(0xffffffffu, x2, 31);
+              unsigned pos = qtail + (unsigned)(x2 - c2);
+              const int cbase = (ci >> 2) * CB + 2 * quarter;
+              while (m) {
+                const int bit = __ffs(m) - 1;
+                m &= m - 1u;
+                sQ[pos & (QCAP - 1)] =
+                    (uint16_t)(((cbase + (bit >> 2)) << 7) | (lane << 2) | (bit & 3));
+                ++pos;
+              }
+              qtail += (unsigned)t2;
+            }
+            ++ci;
           }
+          const bool more = ci < nchunks;
           __syncwarp();
           for (;;) {
             const unsigned avail = qtail - qhead;
-            if (avail == 0u || (avail < 32u && more)) break;
-            const unsigned n = min(32u, avail);
-            unsigned e = 0;
-            if ((unsigned)lane < n) e = sQ[(qhead + lane) & (QCAP - 1)];
+            constexpr unsigned PASS = 32u * APL;
+            if (avail == 0u || (avail < PASS && more)) break;
+            const unsigned n = min(PASS, avail);
+            const bool v0 = (unsigned)lane < n, v1 = APL == 2 && (unsigned)lane + 32u < n;
+            const unsigned e0 = sQ[(qhead + lane) & (QCAP - 1)];
+            const unsigned e1 = APL == 2 ? sQ[(qhead + 32u + lane) & (QCAP - 1)] : 0u;
             __syncwarp();
             qhead += n;
-            if ((unsigned)lane < n) process_entry(e);
+            if (v0) process_pair(v0 ? e0 : 0u, v0, v1 ? e1 : 0u, v1);
           }
           if (!more) break;
         }
