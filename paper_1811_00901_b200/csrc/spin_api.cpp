@@ -245,6 +245,7 @@ spin_status load_cloud(spin_ctx* h, const float* points, const float* normals, i
 spin_status ensure_grid(spin_ctx* h, float R, cudaStream_t s, double* build_ms) {
   // cell edge R/2; grow it if the grid would exceed 2^24 cells
   double hh = 0.5 * R;
+  if (const char* c = std::getenv("SPIN_DEBUG_CELLS_PER_R")) hh = R / std::atof(c);   // measurement knob
   const double ex = std::max(1e-30, (double)h->aabb[3] - h->aabb[0]);
   const double ey = std::max(1e-30, (double)h->aabb[4] - h->aabb[1]);
   const double ez = std::max(1e-30, (double)h->aabb[5] - h->aabb[2]);
@@ -499,13 +500,15 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   double Eu_a;
   if (!(flags & SPIN_F_LITERAL_HALF_WIDTH))
     Eu_a = ((Eb_a + 1.01 * u * D) / b + u * (p.A + D / b)) * 1.01;
-  else
-    Eu_a = (Eb_a + 3.01 * u * (p.A + D)) / b * 1.01;
+  else  // u = fma(-beta, fl(1/b), fl(W/(2b))): rounding of both constants and the fma
+    Eu_a = (Eb_a + 4.01 * u * (p.A + D)) / b * 1.05;
   const double Ew_a = (Eq_a + 2.01 * u * D2) / (b * b) * 1.01;
   p.c_f = has_support ? (float)cos_As : -INFINITY;
   p.inv_b = (float)(1.0 / b);
   p.inv_b2 = (float)(1.0 / (b * b));
   p.Af = (float)p.A;
+  p.Au = (flags & SPIN_F_LITERAL_HALF_WIDTH) ? (float)(p.A / b) : (float)p.A;
+  p.floor_f = (flags & SPIN_F_FLOOR_BINS) ? 1.0f : 0.0f;
   p.Es_a = f32_up(Es_a);
   p.Eu_a = f32_up(Eu_a);
   p.Ew_a = f32_up(Ew_a);
@@ -519,6 +522,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   if (mode == SPIN_NEAREST) {
     const int k = p.floor_bins ? (int)std::floor(p.A) : (int)std::ceil(p.A);
     p.self_k = (k >= 0 && k < W) ? k : -1;
+    p.self_kf = (float)p.self_k;
     p.self_l = 0;
     p.self_a = 0.f;
   } else {

@@ -42,6 +42,9 @@ struct KParams {
   // accept path, fp32 stage
   float c_f;                 // (float)cos_As, its rounding is inside Es_a
   float inv_b, inv_b2, Af;
+  float Au;                  // u = fma(-beta, inv_b, Au): W/2 (scaled) or fl32(W/(2b)) (literal)
+  float floor_f;             // 1.0 for SPIN_F_FLOOR_BINS, else 0.0
+  float self_kf;             // (float)self_k
   float Es_a, Eu_a, Ew_a, D2g;
   int32_t literal, floor_bins, no_fast_cert;
   int32_t debug_skip;        // measurement only (env SPIN_DEBUG_SKIP): 1 skip accept, 2 skip compaction too

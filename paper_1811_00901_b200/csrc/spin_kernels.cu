@@ -195,8 +195,7 @@ struct Dec {
 template <int MODE>
 __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const float4 N4,
                                       const float4 X4, const float4 NX4) {
-  const int W = p.W;
-  const float Wf = (float)W, Wm1 = Wf - 1.0f;
+  const float Wf = (float)p.W, Wm1 = Wf - 1.0f;
   const float d0 = __fsub_rn(X4.x, P4.x), d1 = __fsub_rn(X4.y, P4.y), d2 = __fsub_rn(X4.z, P4.z);
   // support test, inclusive, cosine form (#5); c_f = -inf disables it (ds = +inf)
   const float s = fmaf(N4.x, NX4.x, fmaf(N4.y, NX4.y, N4.z * NX4.z));
@@ -205,36 +204,38 @@ __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const f
   const float be = fmaf(N4.x, d0, fmaf(N4.y, d1, N4.z * d2));       // np_i.(X-P)
   const float dd = fmaf(d0, d0, fmaf(d1, d1, d2 * d2));              // ||X-P||^2
   const float q = fmaf(-be, be, dd);                                 // alpha^2
-  const float uval = p.literal ? (p.Af - be) * p.inv_b : fmaf(-be, p.inv_b, p.Af);
+  // u = W/2 - beta/b (scaled, #2) or (W/2 - beta)/b (literal: Au = fl(W/(2b)), in Eu)
+  const float uval = fmaf(-be, p.inv_b, p.Au);
   const float wval = q * p.inv_b2;                                   // (alpha/b)^2
-  const bool unc0 = (p.no_fast_cert != 0) | !(ds > p.Es_a) | !(dd <= p.D2g);
+  // fp32 verdicts need the certified domain (|d| <= D) and |u| < 2^21 (magic rounding)
+  const bool unc0 = (p.no_fast_cert != 0) | !(ds > p.Es_a) | !(dd <= p.D2g) |
+                    !(fabsf(uval) < 2097152.0f);
   Dec r;
   r.a = 0.f;
   r.c = 0.f;
   if (MODE == 0) {
     // the self pair (d == 0): beta = q = 0 exactly, k = ceil(W/2) (or floor), l = 0 (#8)
     const bool self = (fabsf(d0) + fabsf(d1) + fabsf(d2) == 0.f) & (p.self_fast != 0);
-    // row k = ceil(u) (or floor): certified when u is farther than Eu from an integer
-    const float uc = fminf(fmaxf(uval, -4.0f), Wf + 4.0f);
-    const float rr = rint_magic(uc);
-    const float du = uc - rr;                                        // exact
-    const bool ku = !(fabsf(du) > p.Eu_a) & !self;
-    float kf = p.floor_bins ? (du < 0.f ? rr - 1.0f : rr) : (du > 0.f ? rr + 1.0f : rr);
+    // row k = ceil(u) (or floor): certified when u is farther than Eu from an integer;
+    // |u| < 2^22 inside the certified domain (dd <= D2g), garbage is ignored outside it
+    const float rr = rint_magic(uval);
+    const float du = uval - rr;                                      // exact
+    bool ku = !(fabsf(du) > p.Eu_a);
+    float kf = rr + (du > 0.f ? 1.0f : 0.0f) - p.floor_f;
     // column l = ceil(sqrt(w)) (or floor): certified when w is farther than Ew from
     // every perfect square (fl^2 is exact); sqrt only proposes fl, the squares decide
     const float wc = fmaxf(wval, 0.0f);
     float rs;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(fmaxf(wc, 1e-30f)));
-    const float fl = rint_magic(wc * rs - 0.5f);
+    const float fl = rint_magic(fmaf(wc, rs, -0.5f));
     const float dlo = fmaf(-fl, fl, wval), dhi = fmaf(fl + 1.0f, fl + 1.0f, -wval);
     const bool wneg = wval < -p.Ew_a;
-    float lf = wneg ? 0.0f : fl + (p.floor_bins ? 0.0f : 1.0f);
-    const bool lu = !(wneg | ((dlo > p.Ew_a) & (dhi > p.Ew_a))) & !self;
-    if (self) { kf = (float)p.self_k; lf = 0.0f; }
+    bool lu = !(wneg | ((dlo > p.Ew_a) & (dhi > p.Ew_a)));
+    float lf = wneg ? 0.0f : fl + 1.0f - p.floor_f;
+    if (self) { kf = p.self_kf; lf = 0.0f; ku = false; lu = false; }
     const bool out = (!ku & ((kf < 0.0f) | (kf >= Wf))) | (!lu & (lf >= Wf));
-    const bool unc = unc0 | ku | lu;
-    r.status = (sup_out | (!unc0 & out)) ? 0 : (unc ? 2 : 1);
-    r.bin = (int)kf * W + (int)lf;
+    r.status = (sup_out | (!unc0 & out)) ? 0 : ((unc0 | ku | lu) ? 2 : 1);
+    r.bin = (int)kf * p.W + (int)lf;
   } else {
     // BILINEAR region 0 <= u < W-1, w < (W-1)^2  (#12); the self pair (u = W/2, w = 0)
     // is interior for W >= 3 and needs no special case
@@ -242,14 +243,13 @@ __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const f
     const float lim = Wm1 * Wm1;
     const bool wu = !(fabsf(wval - lim) > p.Ew_a);
     const bool out = (!uu & !((uval > 0.f) & (uval < Wm1))) | (!wu & !(wval < lim));
-    const bool unc = unc0 | uu | wu;
-    r.status = (sup_out | (!unc0 & out)) ? 0 : (unc ? 2 : 1);
+    r.status = (sup_out | (!unc0 & out)) ? 0 : ((unc0 | uu | wu) ? 2 : 1);
     const float v = sqrtf(fmaxf(wval, 0.0f));
     const float fi = fminf(fmaxf(rint_magic(uval - 0.5f), 0.0f), Wm1 - 1.0f);
     const float fj = fminf(fmaxf(rint_magic(v - 0.5f), 0.0f), Wm1 - 1.0f);
     r.a = fminf(fmaxf(uval - fi, 0.0f), 1.0f);
     r.c = fminf(fmaxf(v - fj, 0.0f), 1.0f);
-    r.bin = (int)fi * W + (int)fj;
+    r.bin = (int)fi * p.W + (int)fj;
   }
   return r;
 }
