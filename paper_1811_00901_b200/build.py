@@ -38,14 +38,20 @@ def _stale(objs):
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
-    objs = [os.path.join(BUILD, s + ".o") for s in SOURCES]
-    if not force and not _stale(objs):
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defs: tuple = ()) -> str:
+    """Build libspin.so (or, for A/B measurements, a variant with -D`defs` at `out`)."""
+    global OUT
+    if out:
+        OUT = os.path.abspath(out)
+    build_dir = BUILD if not defs else BUILD + "_" + "_".join(d.strip("-D").replace("=", "") for d in defs)
+    os.makedirs(build_dir, exist_ok=True)
+    objs = [os.path.join(build_dir, s + ".o") for s in SOURCES]
+    if not force and not defs and not _stale(objs):
         return OUT
     def comp(src, obj):
         extra = ["-Xptxas", "-v"] if (verbose and src.endswith(".cu")) else []
-        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", os.path.join(HERE, "..", "include"),
+        cmd = [NVCC, *ARCH, *FLAGS, *defs, *extra, "-I", os.path.join(HERE, "..", "include"),
                "-c", os.path.join(CSRC, src), "-o", obj]
         return _run(cmd)
     with ThreadPoolExecutor(len(SOURCES)) as ex:
@@ -58,4 +64,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    out = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--out=")), None)
+    defs = tuple(a for a in sys.argv if a.startswith("-D"))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=out, defs=defs))

@@ -25,14 +25,22 @@
 #include <cstdlib>
 
 #include "spin_internal.h"
+
+#ifndef SPIN_NT
+#define SPIN_NT 768
+#endif
+#ifndef SPIN_KP
+#define SPIN_KP 4
+#endif
 #include "spin_exact.cuh"
 
 namespace spin {
 
-constexpr int NT = 768;           // threads per CTA (one CTA per SM, 24 warps)
+constexpr int NT = SPIN_NT;       // threads per CTA (one CTA per SM)
 constexpr int NWARP = NT / 32;
-constexpr int KP = 4;             // points per thread (register blocking)
-constexpr int CB_MAX = 8;         // centres per mask batch: CB * KP <= 32 bits
+constexpr int KP = SPIN_KP;       // points per thread (register blocking), 2 or 4
+constexpr int LOGKP = KP == 4 ? 2 : 1;
+constexpr int CB_MAX = 32 / KP;   // centres per mask batch: CB * KP <= 32 bits
 __host__ __device__ constexpr int cb_of(int G) { return G < CB_MAX ? G : CB_MAX; }
 // per-warp candidate ring of u16 entries (power of two): BRUTE tiles hold few candidates
 // (~2% of pairs), CELLS tiles in dense clusters many
@@ -428,7 +436,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         const int src = (int)(e & 127u);
         P4 = sP[gs];
         N4 = sN[gs];
-        const int sl = src >> 2, kk = src & 3;                      // source lane, point k
+        const int sl = src >> LOGKP, kk = src & (KP - 1);           // source lane, point k
         const float* rec = reinterpret_cast<const float*>(sT + (kk >> 1) * 32 + sl) + (kk & 1);
         constexpr int RS = (KP / 2) * 32 * 4;                       // floats between records
         X4 = make_float4(rec[0], rec[2], rec[RS], 0.f);
@@ -489,7 +497,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
                   const int bit = __ffs(m) - 1;
                   m &= m - 1u;
                   sQ[pos & (QCAP - 1)] =
-                      (uint16_t)(((w * CB + (bit >> 2)) << 7) | (lane << 2) | (bit & 3));
+                      (uint16_t)(((w * CB + (bit >> LOGKP)) << 7) | (lane << LOGKP) | (bit & (KP - 1)));
                   ++pos;
                 }
               }
@@ -506,12 +514,12 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
               }
               const int t2 = __shfl_sync(0xffffffffu, x2, 31);
               unsigned pos = qtail + (unsigned)(x2 - c2);
-              const int cbase = (ci >> 2) * CB + 2 * quarter;
+              const int cbase = (ci >> 2) * CB + (8 / KP) * quarter;
               while (m) {
                 const int bit = __ffs(m) - 1;
                 m &= m - 1u;
                 sQ[pos & (QCAP - 1)] =
-                    (uint16_t)(((cbase + (bit >> 2)) << 7) | (lane << 2) | (bit & 3));
+                    (uint16_t)(((cbase + (bit >> LOGKP)) << 7) | (lane << LOGKP) | (bit & (KP - 1)));
                 ++pos;
               }
               qtail += (unsigned)t2;
