@@ -158,7 +158,11 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
  * spin_generate_host — spin_generate with HOST buffers: copies h_centre_idx [M]
  * to the device, runs, copies the images to h_out [M][W][W] (pinned memory is
  * fastest; pageable works) and synchronises `stream`.  Device scratch for the
- * centres and images is owned by the handle and grown on demand.
+ * centres and images is owned by the handle and grown on demand.  For BRUTE runs
+ * of >= 8 MB of images the D2H copy is pipelined with the kernel: the kernel counts
+ * finished images per output segment (16 segments) and a handle-owned copy stream
+ * waits on each counter (cuStreamWaitValue32, resolved through
+ * cudaGetDriverEntryPoint) before copying that segment.
  */
 spin_status spin_generate_host(spin_handle h, const int32_t* h_centre_idx, int64_t M,
                                int32_t W, double b, double cos_As, spin_schedule sched,

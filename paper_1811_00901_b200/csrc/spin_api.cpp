@@ -6,6 +6,7 @@
 // the centre ordering (a5), then one launch of the persistent kernel (a6-a13).
 #include "../../include/spin.h"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -141,6 +142,8 @@ void build_bounds(spin_schedule sched, int64_t n, int32_t P, int32_t gss_min, in
 
 }  // namespace
 
+typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
 struct spin_ctx {
   int dev = 0, sms = 0;
   int64_t N = 0, Npad = 0, cap = 0;
@@ -179,6 +182,13 @@ struct spin_ctx {
   unsigned long long* cta_t0 = nullptr; unsigned long long* cta_t1 = nullptr;
   int32_t* cta_units = nullptr; int64_t cta_cap = 0;
   uint32_t* hi_scratch = nullptr; int64_t hi_cap = 0;   // kept zero between launches
+  // e2e pipelining of spin_generate_host: per-segment completion counters + copy stream
+  unsigned* seg_done = nullptr; int64_t seg_cap = 0;
+  int32_t pipe_seg_images = 0;                         // armed for the next launch only
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_seg0 = nullptr;
+  int stream_wait_ok = -1;                             // -1 unknown, 0 no, 1 yes
+  WaitValue32Fn wait_value32 = nullptr;
   // cloud staging (AoS input) and reductions
   float* stage_p = nullptr; int64_t stage_p_cap = 0;
   float* stage_n = nullptr; int64_t stage_n_cap = 0;
@@ -380,14 +390,15 @@ void spin_destroy(spin_handle h) {
   void* ptrs[] = {h->pos, h->nrm, h->cell_start, h->spos, h->snrm, h->keys, h->counts,
                   h->cursor, h->scan_tmp, h->ckeys, h->cstarts, h->order, h->bounds,
                   h->counter, h->stats, h->err, h->cta_t0, h->cta_t1, h->cta_units, h->cidx,
-                  h->outbuf, h->stage_p, h->stage_n, h->red, h->hi_scratch};
+                  h->outbuf, h->stage_p, h->stage_n, h->red, h->hi_scratch, h->seg_done};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->h_err) cudaFreeHost(h->h_err);
   if (h->h_red) cudaFreeHost(h->h_red);
-  cudaEvent_t evs[] = {h->ev_err, h->ev0, h->ev1, h->evg0, h->evg1};
+  cudaEvent_t evs[] = {h->ev_err, h->ev0, h->ev1, h->evg0, h->evg1, h->ev_seg0};
   for (cudaEvent_t e : evs)
     if (e) cudaEventDestroy(e);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   delete h;
 }
 
@@ -601,6 +612,19 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
     }
   }
 
+  // ---- e2e pipelining armed by spin_generate_host (BRUTE: images leave in caller order)
+  if (h->pipe_seg_images > 0 && p.order == nullptr) {
+    const int64_t nseg = (M + h->pipe_seg_images - 1) / h->pipe_seg_images;
+    spin_status st = ensure(h->seg_done, h->seg_cap, nseg, "segment counters");
+    if (st != SPIN_OK) return st;
+    CK(cudaMemsetAsync(h->seg_done, 0, nseg * sizeof(unsigned), s), "memset");
+    CK(cudaEventRecord(h->ev_seg0, s), "event");
+    p.seg_done = h->seg_done;
+    p.seg_images = h->pipe_seg_images;
+  } else {
+    h->pipe_seg_images = 0;
+  }
+
   // ---- a6-a13: the persistent launch
   CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned), s), "memset");
   CK(cudaMemsetAsync(h->stats, 0, ST_NSLOTS * sizeof(unsigned long long), s), "memset");
@@ -660,8 +684,53 @@ spin_status spin_generate_host(spin_handle h, const int32_t* h_centre_idx, int64
   if ((st = ensure(h->cidx, h->cidx_cap, M, "centre scratch")) != SPIN_OK) return st;
   if ((st = ensure(h->outbuf, h->outbuf_cap, M * W * W, "image scratch")) != SPIN_OK) return st;
   CK(cudaMemcpyAsync(h->cidx, h_centre_idx, M * sizeof(int32_t), cudaMemcpyHostToDevice, s), "H2D centres");
+  // Pipeline the D2H of the images with the kernel: the kernel counts finished images
+  // per output segment; a copy stream waits on each counter (cuStreamWaitValue32) and
+  // copies that segment while later groups are still being computed.
+  const size_t img_bytes = (size_t)W * W * sizeof(float);
+  const bool pipe = prune == SPIN_BRUTE && (size_t)M * img_bytes >= ((size_t)8 << 20);
+  if (pipe && h->stream_wait_ok != 0) {
+    if (!h->copy_stream) {
+      CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking), "copy stream");
+      CK(cudaEventCreateWithFlags(&h->ev_seg0, cudaEventDisableTiming), "event");
+    }
+    if (h->stream_wait_ok < 0) {
+      // the driver entry point through the runtime (libspin does not link libcuda)
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      h->stream_wait_ok = (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) ==
+                               cudaSuccess && q == cudaDriverEntryPointSuccess && fn)
+                              ? 1 : 0;
+      h->wait_value32 = reinterpret_cast<WaitValue32Fn>(fn);
+    }
+  }
+  const bool piped = pipe && h->stream_wait_ok == 1;
+  const int32_t nseg_target = 16;
+  const int32_t seg_images = (int32_t)std::max<int64_t>(1, (M + nseg_target - 1) / nseg_target);
+  h->pipe_seg_images = piped ? seg_images : 0;
   st = spin_generate(h, h->cidx, M, W, b, cos_As, sched, cp, mode, prune, h->outbuf, stats, stream);
+  const bool armed = h->pipe_seg_images > 0;
+  h->pipe_seg_images = 0;
   if (st != SPIN_OK) return st;
+  if (armed) {
+    CK(cudaStreamWaitEvent(h->copy_stream, h->ev_seg0, 0), "wait");
+    for (int64_t a = 0, sg = 0; a < M; a += seg_images, ++sg) {
+      const int64_t n = std::min<int64_t>(seg_images, M - a);
+      if (h->wait_value32((CUstream)h->copy_stream, (CUdeviceptr)(h->seg_done + sg), (cuuint32_t)n,
+                          CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
+        // could not enqueue the wait: finish the remaining copy after the kernel instead
+        CK(cudaStreamSynchronize(s), "sync");
+        CK(cudaMemcpyAsync(h_out + a * W * W, h->outbuf + a * W * W, (size_t)(M - a) * img_bytes,
+                           cudaMemcpyDeviceToHost, h->copy_stream), "D2H images");
+        break;
+      }
+      CK(cudaMemcpyAsync(h_out + a * W * W, h->outbuf + a * W * W, (size_t)n * img_bytes,
+                         cudaMemcpyDeviceToHost, h->copy_stream), "D2H images");
+    }
+    CK(cudaStreamSynchronize(h->copy_stream), "sync copy");
+    CK(cudaStreamSynchronize(s), "sync");
+    return SPIN_OK;
+  }
   CK(cudaMemcpyAsync(h_out, h->outbuf, (size_t)M * W * W * sizeof(float), cudaMemcpyDeviceToHost, s), "D2H images");
   CK(cudaStreamSynchronize(s), "sync");
   return SPIN_OK;

@@ -66,6 +66,8 @@ struct KParams {
   int32_t* cta_units;                      // [P]
   int32_t* err_flags;                      // [0]: bad centre index seen; [1]: overflow
   uint32_t* hi_scratch;                    // BILINEAR carry words, [P][G][(W*W+1)/2], zero
+  unsigned int* seg_done;                  // e2e pipelining: images finished per output segment
+  int32_t seg_images;                      // images per segment (seg_done != nullptr)
 };
 
 enum StatSlot {

@@ -704,6 +704,22 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         }
         __stcs(&p.out[(long long)mm * WW + e], val);
       }
+      if (p.seg_done != nullptr) {
+        // e2e pipelining (spin_generate_host): publish finished images per output segment
+        // so the copy stream can start their D2H while the kernel still runs
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0) {
+          long long a = g0;
+          const long long bnd = g0 + gcount;
+          while (a < bnd) {
+            const long long sg = a / p.seg_images;
+            const long long e = min(bnd, (sg + 1) * (long long)p.seg_images);
+            atomicAdd(&p.seg_done[sg], (unsigned)(e - a));
+            a = e;
+          }
+        }
+      }
       if (MODE == 1) {
         __syncthreads();
         if (s_carry) {                       // leave the carry scratch zero for the next group

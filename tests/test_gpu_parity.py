@@ -383,3 +383,23 @@ def test_bilinear_fixed_point_carries(spin, torch):
         check(gpu, ora, st, "bilinear", f"carries W={W}")
         again = run_gpu(spin, torch, P, Nn, cen, W, b, 0.5, "bilinear", schedule="SS", unit=1)
         np.testing.assert_array_equal(again, gpu)    # deterministic (integer accumulation)
+
+
+def test_host_path_pipelined_d2h(spin, torch):
+    """spin_generate_host pipelines the image D2H with the kernel (per-segment completion
+    counters + a copy stream); the host images must equal the device path bit for bit."""
+    P, Nn = clouds.bumpy_sphere(20000, 12)
+    cen = np.arange(20000, dtype=np.int32)[::-1].copy()
+    eng = spin.SpinEngine(P, Nn)
+    try:
+        for mode in ("nearest", "bilinear"):
+            for sched, unit in (("SS", 0), ("GSS", 1), ("STATIC", 0)):
+                out = np.full((len(cen), 16, 16), -1.0, np.float32)
+                h = eng.generate_host(cen, 16, 0.02, 0.5, mode=mode, schedule=sched, unit=unit, out=out)
+                d = eng.generate(_dev(torch, cen), 16, 0.02, 0.5, mode=mode).cpu().numpy()
+                np.testing.assert_array_equal(h, d, err_msg=f"{mode} {sched} unit={unit}")
+        pick = np.arange(0, 20000, 997)
+        ora, _ = oracle(P, Nn, cen[pick], 16, 0.02, 0.5, "nearest")
+        assert_nearest_exact(h[pick] if False else eng.generate_host(cen, 16, 0.02, 0.5)[pick], ora, "piped host")
+    finally:
+        eng.close()
