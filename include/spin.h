@@ -68,6 +68,8 @@ typedef enum { SPIN_BRUTE = 0, SPIN_CELLS = 1 } spin_prune;
 #define SPIN_F_FLOOR_BINS         0x2u /* NEAREST: k = floor(u), l = floor(v) (Johnson) instead of ceil */
 #define SPIN_F_NO_SORT            0x4u /* CELLS: keep the caller's centre order (control run)    */
 #define SPIN_F_NO_FAST_CERT       0x8u /* testing: send every candidate through the fp64 / exact decision stages   */
+#define SPIN_F_SUPPORT_LAST       0x10u /* evaluate the support test only for pairs inside the region: same
+                                           images, fewer flops per pair (the region test runs first)            */
 
 /* Scheduling parameters.  All-zero = defaults. */
 typedef struct {

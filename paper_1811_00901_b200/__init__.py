@@ -6,6 +6,6 @@ loads libspin.so and fails loudly if it is missing (no CPU fallback).
 """
 from .spin import (  # noqa: F401
     BILINEAR, BRUTE, CELLS, F_FLOOR_BINS, F_LITERAL_HALF_WIDTH, F_NO_FAST_CERT, F_NO_SORT, FAC,
-    GSS, LIB_PATH, NEAREST, NO_SUPPORT, SS, STATIC, SpinEngine, SpinError, abi_version,
+    GSS, LIB_PATH, NEAREST, F_SUPPORT_LAST, NO_SUPPORT, SS, STATIC, SpinEngine, SpinError, abi_version,
     chunk_sequence, cos_from_degrees, default_P, generate, region_radius,
 )

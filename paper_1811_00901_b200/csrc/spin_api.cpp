@@ -430,7 +430,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   if (cp) cpar = *cp;
   if (cpar.P < 0 || cpar.unit < 0 || cpar.gss_min_chunk < 0 || cpar.fac_divisor < 0)
     return fail(SPIN_E_INVAL, "negative chunk parameter");
-  if (cpar.flags & ~0xfu) return fail(SPIN_E_INVAL, "unknown flag bits 0x%x", cpar.flags);
+  if (cpar.flags & ~0x1fu) return fail(SPIN_E_INVAL, "unknown flag bits 0x%x", cpar.flags);
   if (M > 0 && (!d_centre_idx || !d_out)) return fail(SPIN_E_INVAL, "null d_centre_idx or d_out with M > 0");
   if (stats) {
     stats->elapsed_ms = stats->grid_build_ms = 0.0;
@@ -498,6 +498,9 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   p.c_test = has_support ? f32_down(cos_As - Es_h) : -INFINITY;
   p.h_test = f32_up(rg.h + Eb_h);
   p.has_support = has_support ? 1 : 0;
+  // the hot loop skips the support test when there is none, or when asked to decide it
+  // only for geometric candidates (SPIN_F_SUPPORT_LAST; same result, fewer flops)
+  p.support_in_hot = (has_support && !(cpar.flags & SPIN_F_SUPPORT_LAST)) ? 1 : 0;
   // candidates satisfy |d| <= D: q <= Qmax + 2Eq, |beta| <= |mid| + h_test + Eb
   const double Cmax = (X + amid) * (X + amid) * 1.01;
   const double bmax = amid + (double)p.h_test + Eb_h;

@@ -39,6 +39,7 @@ struct KParams {
   double Eq_hot;             // hot-loop bound on |q''_fp32 - q''| (added to Qmax - C per centre)
   float c_test, h_test;      // hot loop: s >= c_test, |beta''| <= h_test
   int32_t has_support;
+  int32_t support_in_hot;    // 1: hot loop tests the support (default); 0: accept path only
   // accept path, fp32 stage
   float c_f;                 // (float)cos_As, its rounding is inside Es_a
   float inv_b, inv_b2, Af;

@@ -118,6 +118,18 @@ __device__ __forceinline__ unsigned pair_bit_n(unsigned mask, float s, float c, 
   return mask;
 }
 
+// Region-only test (support decided later): (|beta''| <= h) && (-q'' >= -Qt)
+__device__ __forceinline__ unsigned pair_bit_r(unsigned mask, float abe, float h, float qn,
+                                               float nqt, unsigned bit) {
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.le.f32 p, %1, %2;\n\t"
+      "setp.ge.and.f32 p, %3, %4, p;\n\t"
+      "@p or.b32 %0, %0, %5;\n\t}"
+      : "+r"(mask)
+      : "f"(abe), "f"(h), "f"(qn), "f"(nqt), "r"(bit));
+  return mask;
+}
+
 // ------------------------------------------------------------------ smem layout
 struct Layout {
   size_t oA, oB, oP, oN, oM, oImg, oHi, oQ, oTP, oTN, oMask, oRowS, oRowO, total;
@@ -290,7 +302,10 @@ __device__ __forceinline__ void apply(const KParams& p, const Dec& d, uint32_t* 
 }
 
 // ------------------------------------------------------------------ the kernel
-template <int MODE, int PRUNE, int G>
+// SUP = 1: the hot loop evaluates the support test for every pair (the paper's order,
+// P:166 before P:169-171); SUP = 0: the hot loop tests the region only and the support
+// test is decided in the accept path (SPIN_F_SUPPORT_LAST, or no support test at all).
+template <int MODE, int PRUNE, int G, int SUP>
 __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__ KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_chunk;
@@ -585,7 +600,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             for (int k2 = 0; k2 < KP / 2; ++k2) {
               // support n.nx; beta'' = n.x - n.p - mid;
               // -q'' = beta''^2 + 2(p + mid n).x - |x|^2 = C - q
-              const f2 s2 = fma2(bc2(A4.x), NX2[k2], fma2(bc2(A4.y), NY2[k2], mul2(bc2(A4.z), NZ2[k2])));
+              f2 s2 = 0ull;
+              if (SUP) s2 = fma2(bc2(A4.x), NX2[k2], fma2(bc2(A4.y), NY2[k2], mul2(bc2(A4.z), NZ2[k2])));
               const f2 be2 = fma2(bc2(A4.x), X2[k2], fma2(bc2(A4.y), Y2[k2], fma2(bc2(A4.z), Z2[k2], bc2(A4.w))));
               const f2 tn2 = fma2(bc2(B4.x), X2[k2], fma2(bc2(B4.y), Y2[k2], fma2(bc2(B4.z), Z2[k2], NXX2[k2])));
               const f2 qn2 = fma2(be2, be2, tn2);
@@ -594,8 +610,13 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
               up2(be2, b0, b1);
               up2(qn2, q0, q1);
               const int bit = c * KP + 2 * k2;
-              mask = pair_bit_n(mask, s0, c_test, fabsf(b0), h_test, q0, B4.w, 1u << bit);
-              mask = pair_bit_n(mask, s1, c_test, fabsf(b1), h_test, q1, B4.w, 1u << (bit + 1));
+              if (SUP) {
+                mask = pair_bit_n(mask, s0, c_test, fabsf(b0), h_test, q0, B4.w, 1u << bit);
+                mask = pair_bit_n(mask, s1, c_test, fabsf(b1), h_test, q1, B4.w, 1u << (bit + 1));
+              } else {
+                mask = pair_bit_r(mask, fabsf(b0), h_test, q0, B4.w, 1u << bit);
+                mask = pair_bit_r(mask, fabsf(b1), h_test, q1, B4.w, 1u << (bit + 1));
+              }
             }
           }
           sMask[(cb / CB) * 32 + lane] = mask;
@@ -754,19 +775,23 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
 }
 
 // ------------------------------------------------------------------ dispatch
-template <int MODE, int PRUNE>
+template <int MODE, int PRUNE, int SUP>
 static const void* kernel_ptr(int G) {
   switch (G) {
-    case 4: return (const void*)spin_persistent<MODE, PRUNE, 4>;
-    case 8: return (const void*)spin_persistent<MODE, PRUNE, 8>;
-    case 16: return (const void*)spin_persistent<MODE, PRUNE, 16>;
-    case 32: return (const void*)spin_persistent<MODE, PRUNE, 32>;
-    default: return (const void*)spin_persistent<MODE, PRUNE, 64>;
+    case 4: return (const void*)spin_persistent<MODE, PRUNE, 4, SUP>;
+    case 8: return (const void*)spin_persistent<MODE, PRUNE, 8, SUP>;
+    case 16: return (const void*)spin_persistent<MODE, PRUNE, 16, SUP>;
+    case 32: return (const void*)spin_persistent<MODE, PRUNE, 32, SUP>;
+    default: return (const void*)spin_persistent<MODE, PRUNE, 64, SUP>;
   }
 }
-static const void* kernel_for(int mode, int prune, int G) {
-  if (mode == 0) return prune == 0 ? kernel_ptr<0, 0>(G) : kernel_ptr<0, 1>(G);
-  return prune == 0 ? kernel_ptr<1, 0>(G) : kernel_ptr<1, 1>(G);
+static const void* kernel_for(int mode, int prune, int G, int sup) {
+  if (sup) {
+    if (mode == 0) return prune == 0 ? kernel_ptr<0, 0, 1>(G) : kernel_ptr<0, 1, 1>(G);
+    return prune == 0 ? kernel_ptr<1, 0, 1>(G) : kernel_ptr<1, 1, 1>(G);
+  }
+  if (mode == 0) return prune == 0 ? kernel_ptr<0, 0, 0>(G) : kernel_ptr<0, 1, 0>(G);
+  return prune == 0 ? kernel_ptr<1, 0, 0>(G) : kernel_ptr<1, 1, 0>(G);
 }
 
 LaunchCfg choose_launch(int W, int mode, int prune) {
@@ -786,7 +811,7 @@ LaunchCfg choose_launch(int W, int mode, int prune) {
 int tile_points() { return NT * KP; }
 
 int occupancy_blocks(const LaunchCfg& lc, int W, int mode, int prune) {
-  const void* f = kernel_for(mode, prune, lc.G);
+  const void* f = kernel_for(mode, prune, lc.G, 1);
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.smem);
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, lc.threads, lc.smem) != cudaSuccess)
@@ -797,7 +822,7 @@ int occupancy_blocks(const LaunchCfg& lc, int W, int mode, int prune) {
 
 cudaError_t launch_spin(const LaunchCfg& lc, int mode, int prune, int grid, const KParams& p,
                         cudaStream_t s) {
-  const void* f = kernel_for(mode, prune, lc.G);
+  const void* f = kernel_for(mode, prune, lc.G, p.support_in_hot);
   cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.smem);
   if (e != cudaSuccess) return e;
   void* args[] = {(void*)&p};

@@ -21,7 +21,7 @@ _lib = C.CDLL(LIB_PATH)
 STATIC, SS, GSS, FAC = 0, 1, 2, 3
 NEAREST, BILINEAR = 0, 1
 BRUTE, CELLS = 0, 1
-F_LITERAL_HALF_WIDTH, F_FLOOR_BINS, F_NO_SORT, F_NO_FAST_CERT = 0x1, 0x2, 0x4, 0x8
+F_LITERAL_HALF_WIDTH, F_FLOOR_BINS, F_NO_SORT, F_NO_FAST_CERT, F_SUPPORT_LAST = 0x1, 0x2, 0x4, 0x8, 0x10
 SCHEDULES = {"STATIC": STATIC, "SS": SS, "GSS": GSS, "FAC": FAC}
 MODES = {"nearest": NEAREST, "bilinear": BILINEAR}
 PRUNES = {"brute": BRUTE, "cells": CELLS}

@@ -403,3 +403,20 @@ def test_host_path_pipelined_d2h(spin, torch):
         assert_nearest_exact(h[pick] if False else eng.generate_host(cen, 16, 0.02, 0.5)[pick], ora, "piped host")
     finally:
         eng.close()
+
+
+@pytest.mark.parametrize("prune", ["brute", "cells"])
+def test_support_last_same_images(spin, torch, prune):
+    """SPIN_F_SUPPORT_LAST (support test decided after the region test) and the no-support
+    case (cos_As = -inf, hot loop without the support test) leave the images unchanged."""
+    P, Nn = clouds.clustered(20000, 17)
+    cen = clouds.sample_centres(20000, 500, 18)
+    for mode in ("nearest", "bilinear"):
+        for c in (0.5, 0.0, -math.inf):
+            a = run_gpu(spin, torch, P, Nn, cen, 16, 0.01, c, mode, prune=prune)
+            b = run_gpu(spin, torch, P, Nn, cen, 16, 0.01, c, mode, prune=prune,
+                        flags=spin.F_SUPPORT_LAST)
+            np.testing.assert_array_equal(a, b, err_msg=f"{mode} c={c}")
+        ora, st = oracle(P, Nn, cen[:40], 16, 0.01, 0.5, mode, cells=(prune == "cells"))
+        check(b if c == 0.5 else run_gpu(spin, torch, P, Nn, cen[:40], 16, 0.01, 0.5, mode, prune=prune,
+                                         flags=spin.F_SUPPORT_LAST), ora, st, mode, f"support-last {mode}")
