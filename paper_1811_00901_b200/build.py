@@ -18,7 +18,12 @@ BUILD = os.path.join(HERE, "..", "build", "spin")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr"]
-SOURCES = ["spin_kernels.cu", "spin_api.cpp"]
+# (source, extra defines, object name): the persistent kernel's 40 instantiations are
+# split over four translation units (one per (mode, support-in-hot-loop) pair)
+UNITS = [("spin_kernels.cu", (), "spin_kernels"), ("spin_api.cpp", (), "spin_api")] + [
+    ("spin_inst.cu", (f"-DINST_MODE={m}", f"-DINST_SUP={u}"), f"spin_inst_{m}_{u}")
+    for m in (0, 1) for u in (0, 1)]
+SOURCES = [u[0] for u in UNITS]
 
 
 def _run(cmd):
@@ -46,16 +51,17 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
         OUT = os.path.abspath(out)
     build_dir = BUILD if not defs else BUILD + "_" + "_".join(d.strip("-D").replace("=", "") for d in defs)
     os.makedirs(build_dir, exist_ok=True)
-    objs = [os.path.join(build_dir, s + ".o") for s in SOURCES]
+    objs = [os.path.join(build_dir, u[2] + ".o") for u in UNITS]
     if not force and not defs and not _stale(objs):
         return OUT
-    def comp(src, obj):
+    def comp(unit, obj):
+        src, udefs, _ = unit
         extra = ["-Xptxas", "-v"] if (verbose and src.endswith(".cu")) else []
-        cmd = [NVCC, *ARCH, *FLAGS, *defs, *extra, "-I", os.path.join(HERE, "..", "include"),
+        cmd = [NVCC, *ARCH, *FLAGS, *defs, *udefs, *extra, "-I", os.path.join(HERE, "..", "include"),
                "-c", os.path.join(CSRC, src), "-o", obj]
         return _run(cmd)
-    with ThreadPoolExecutor(len(SOURCES)) as ex:
-        logs = list(ex.map(comp, SOURCES, objs))
+    with ThreadPoolExecutor(len(UNITS)) as ex:
+        logs = list(ex.map(comp, UNITS, objs))
     _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", OUT + ".tmp", *objs])
     os.replace(OUT + ".tmp", OUT)
     if verbose:

@@ -58,7 +58,7 @@ struct PairD {
 };
 
 // sign(n . nx - c), exactly (products of two fp32 values are exact in double)
-__device__ __noinline__ int exact_sign_support(const PairD& P, double c) {
+static __device__ __noinline__ int exact_sign_support(const PairD& P, double c) {
   double e[8];
   int m = 0;
   for (int i = 0; i < 3; ++i) m = grow(e, m, P.n[i] * P.nx[i]);
@@ -69,7 +69,7 @@ __device__ __noinline__ int exact_sign_support(const PairD& P, double c) {
 // T(k) = (A - k) b (scaled reading #2) or A - k b (literal, P:169 as printed).
 // Returns sign(beta - T(k)), beta = n.(x - p) = sum n_i x_i - sum n_i p_i.
 // u <= k  <=>  sign >= 0 for both readings.
-__device__ __noinline__ int exact_sign_beta_minus_T(const PairD& P, double A, double b, int k,
+static __device__ __noinline__ int exact_sign_beta_minus_T(const PairD& P, double A, double b, int k,
                                                     int literal) {
   double e[16];
   int m = 0;
@@ -92,7 +92,7 @@ __device__ __noinline__ int exact_sign_beta_minus_T(const PairD& P, double A, do
 }
 
 // sign(q - mm * b^2) with q = |x - p|^2 - beta^2, mm = m^2 a small integer.
-__device__ __noinline__ int exact_sign_q_minus(const PairD& P, double b, double mm) {
+static __device__ __noinline__ int exact_sign_q_minus(const PairD& P, double b, double mm) {
   double e[80];
   int m = 0;
   // |d|^2 with d_i = dh_i + dl_i exactly
@@ -130,7 +130,7 @@ struct SlowOut {
 
 // fp64 stage with per-pair certified bounds, escalating each uncertain decision to
 // the exact stage.  `mode` 0 NEAREST / 1 BILINEAR (BILINEAR returns region only).
-__device__ __noinline__ SlowOut slow_decide(const PairD& P, int W, double A, double b,
+static __device__ __noinline__ SlowOut slow_decide(const PairD& P, int W, double A, double b,
                                             double cos_As, int has_support, int literal,
                                             int floor_bins, int mode) {
   SlowOut r{0, 0, 0, 0};

@@ -1,0 +1,28 @@
+// spin_inst.cu — explicit instantiations of spin_persistent for one (MODE, SUP) pair,
+// selected with -DINST_MODE=0|1 -DINST_SUP=0|1 (built four times by build.py).
+#include "spin_persistent.cuh"
+
+namespace spin {
+
+#define SPIN_CAT2(a, b, c) a##b##_##c
+#define SPIN_CAT(a, b, c) SPIN_CAT2(a, b, c)
+const void* SPIN_CAT(kernel_ptr_, INST_MODE, INST_SUP)(int prune, int G) {
+  if (prune == 0) {
+    switch (G) {
+      case 4: return (const void*)spin_persistent<INST_MODE, 0, 4, INST_SUP>;
+      case 8: return (const void*)spin_persistent<INST_MODE, 0, 8, INST_SUP>;
+      case 16: return (const void*)spin_persistent<INST_MODE, 0, 16, INST_SUP>;
+      case 32: return (const void*)spin_persistent<INST_MODE, 0, 32, INST_SUP>;
+      default: return (const void*)spin_persistent<INST_MODE, 0, 64, INST_SUP>;
+    }
+  }
+  switch (G) {
+    case 4: return (const void*)spin_persistent<INST_MODE, 1, 4, INST_SUP>;
+    case 8: return (const void*)spin_persistent<INST_MODE, 1, 8, INST_SUP>;
+    case 16: return (const void*)spin_persistent<INST_MODE, 1, 16, INST_SUP>;
+    case 32: return (const void*)spin_persistent<INST_MODE, 1, 32, INST_SUP>;
+    default: return (const void*)spin_persistent<INST_MODE, 1, 64, INST_SUP>;
+  }
+}
+
+}  // namespace spin

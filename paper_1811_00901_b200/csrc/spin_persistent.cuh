@@ -1,0 +1,780 @@
+// spin_persistent.cuh — the persistent spin kernel of the hot path (sm_100a).
+// Instantiated in spin_inst_*.cu (one translation unit per (mode, support) pair so the
+// 40 variants compile in parallel); dispatched from spin_kernels.cu.
+//
+// Persistent spin kernel: P resident CTAs; each CTA
+// asks the device "master" (one u32 in global memory) for the next chunk of the
+// schedule (the five-step protocol of PAPER.md:262-267 collapsed to one atomicAdd;
+// STATIC takes chunk blockIdx.x), and for every group of G images in the chunk:
+//   a7  loads the G centres (p, n) and folds them into per-centre fp32 constants,
+//       zeroes G images in shared memory (tempSpinImage + init),
+//   a8  streams the cloud through registers (BRUTE: all N points, Alg. 1's inner
+//       loop P:161; CELLS: the grid rows around the group), each thread holding K
+//       points that are reused against all G centres (n-body blocking),
+//   a9  runs the conservative fp32 pair test — support n.nx >= cos_As,
+//       beta window and alpha^2 bound — packing pass bits into a mask,
+//   a10 compacts candidates into a per-warp shared-memory queue and processes them
+//       32 at a time: exact-certified bin decision, shared-memory u32 atomics
+//       (NEAREST ++) or 2^-23 fixed point (BILINEAR),
+//   a11 re-takes any decision fp32 cannot certify in fp64 and then exactly
+//       (spin_exact.cuh),
+//   a12 writes the G images to out[m] in the caller's order (add(spinImages)),
+//   a13 records %globaltimer start/finish and units per CTA (fig:loadim).
+// No tensor cores: the pair test is not a contraction.
+#pragma once
+#include <cstdint>
+#include <cfloat>
+#include <cmath>
+#include <cstdlib>
+
+#include "spin_internal.h"
+
+#ifndef SPIN_NT
+#define SPIN_NT 768
+#endif
+#ifndef SPIN_KP
+#define SPIN_KP 4
+#endif
+#include "spin_exact.cuh"
+
+namespace spin {
+
+constexpr int NT = SPIN_NT;       // threads per CTA (one CTA per SM)
+constexpr int NWARP = NT / 32;
+constexpr int KP = SPIN_KP;       // points per thread (register blocking), 2 or 4
+constexpr int LOGKP = KP == 4 ? 2 : 1;
+constexpr int CB_MAX = 32 / KP;   // centres per mask batch: CB * KP <= 32 bits
+__host__ __device__ constexpr int cb_of(int G) { return G < CB_MAX ? G : CB_MAX; }
+// per-warp candidate ring of u16 entries (power of two): BRUTE tiles hold few candidates
+// (~2% of pairs), CELLS tiles in dense clusters many
+__host__ __device__ constexpr int qcap_of(int prune) { return prune ? 1024 : 512; }
+constexpr int ROWCAP = NT;        // CELLS: grid rows staged per batch
+
+static_assert(CB_MAX * KP == 32, "mask is one u32");
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// The ONE cell-coordinate function used for binning points and for bounding the
+// visited rows: monotone non-decreasing in x (IEEE sub/mul by a positive constant
+// and floor are monotone), clamped to [0, dim).
+__device__ __forceinline__ int cell_coord(float x, float o, float inv_h, int dim) {
+  float t = __fmul_rn(__fsub_rn(x, o), inv_h);
+  t = fminf(fmaxf(t, 0.0f), (float)(dim - 1));
+  return (int)floorf(t);
+}
+
+// The conservative pair test as ONE predicate chain plus one predicated OR:
+// pass = (s >= c) && (|beta''| <= h) && (q'' <= Qt)  (NaN compares false).
+__device__ __forceinline__ unsigned pair_bit(unsigned mask, float s, float c, float abe, float h,
+                                             float q, float qt, unsigned bit) {
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.ge.f32 p, %1, %2;\n\t"
+      "setp.le.and.f32 p, %3, %4, p;\n\t"
+      "setp.le.and.f32 p, %5, %6, p;\n\t"
+      "@p or.b32 %0, %0, %7;\n\t}"
+      : "+r"(mask)
+      : "f"(s), "f"(c), "f"(abe), "f"(h), "f"(q), "f"(qt), "r"(bit));
+  return mask;
+}
+
+// Packed fp32 (sm_100a FFMA2 / FMUL2): two points per instruction, a scalar centre
+// constant broadcast to both halves.  Halves one FP32 issue slot per pair.
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk2(float a, float b) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ f2 bc2(float a) { return pk2(a, a); }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ void up2(f2 v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+// pass = (s >= c) && (|beta''| <= h) && (-q'' >= -Qt): one predicate chain + one OR
+__device__ __forceinline__ unsigned pair_bit_n(unsigned mask, float s, float c, float abe, float h,
+                                               float qn, float nqt, unsigned bit) {
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.ge.f32 p, %1, %2;\n\t"
+      "setp.le.and.f32 p, %3, %4, p;\n\t"
+      "setp.ge.and.f32 p, %5, %6, p;\n\t"
+      "@p or.b32 %0, %0, %7;\n\t}"
+      : "+r"(mask)
+      : "f"(s), "f"(c), "f"(abe), "f"(h), "f"(qn), "f"(nqt), "r"(bit));
+  return mask;
+}
+
+// Region-only test (support decided later): (|beta''| <= h) && (-q'' >= -Qt)
+__device__ __forceinline__ unsigned pair_bit_r(unsigned mask, float abe, float h, float qn,
+                                               float nqt, unsigned bit) {
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.le.f32 p, %1, %2;\n\t"
+      "setp.ge.and.f32 p, %3, %4, p;\n\t"
+      "@p or.b32 %0, %0, %5;\n\t}"
+      : "+r"(mask)
+      : "f"(abe), "f"(h), "f"(qn), "f"(nqt), "r"(bit));
+  return mask;
+}
+
+// ------------------------------------------------------------------ smem layout
+struct Layout {
+  size_t oA, oB, oP, oN, oM, oImg, oHi, oQ, oTP, oTN, oMask, oRowS, oRowO, total;
+};
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+__host__ __device__ inline Layout make_layout(int G, int W, int mode, int prune) {
+  Layout L;
+  size_t o = 0;
+  L.oA = o; o += 16 * (size_t)G;
+  L.oB = o; o += 16 * (size_t)G;
+  L.oP = o; o += 16 * (size_t)G;
+  L.oN = o; o += 16 * (size_t)G;
+  L.oM = o; o = align16(o + 4 * (size_t)G);
+  const size_t WW = (size_t)W * W;
+  L.oImg = o; o = align16(o + 4 * WW * G);
+  L.oHi = o;
+  L.oQ = o; o += 2 * (size_t)qcap_of(prune) * NWARP;
+  o = align16(o);
+  L.oTP = o; o += 32 * (size_t)32 * KP * NWARP;    // per-warp staged tile, pair layout (32 B/point)
+  L.oTN = o;
+  L.oMask = o; o += 4 * (size_t)32 * (G / cb_of(G)) * NWARP;   // per-warp pass masks of the tile
+  L.oRowS = o;
+  L.oRowO = o;
+  if (prune == 1) {
+    o += 4 * ROWCAP;
+    L.oRowO = o;
+    o += 4 * (ROWCAP + 1);
+    o = align16(o);
+  }
+  L.total = o;
+  return L;
+}
+
+// ------------------------------------------------------------------ counters
+struct Ctr {
+  unsigned cand, acc, f64, exact;
+};
+
+// BILINEAR accumulator: 2^-23 fixed point.  The 32-bit low words live in shared
+// memory; the rare carries (one per 512 units of weight in a bin) go to 16-bit carry
+// words (two bins per u32) in a per-CTA global scratch that is zero between groups,
+// and raise a shared flag so that only groups with carries read or clear it.
+// round(w * 2^23) for w in [0,1] is the mantissa of 1 + w.
+__device__ __forceinline__ void add_fixed(uint32_t* lo, uint32_t* hi, int bin, float w,
+                                          int32_t* err, int* carry_flag) {
+  const uint32_t v = __float_as_uint(w + 1.0f) - 0x3f800000u;
+  const uint32_t old = atomicAdd(&lo[bin], v);
+  if (old + v < old) {
+    const uint32_t sh = (uint32_t)(bin & 1) * 16u;
+    const uint32_t prev = atomicAdd(&hi[bin >> 1], 1u << sh);
+    if (((prev >> sh) & 0xffffu) == 0xffffu) atomicOr(&err[1], 1);
+    *carry_flag = 1;
+  }
+}
+
+// ------------------------------------------------------------------ accept path
+// round-to-nearest-even for |x| < 2^22 on the FMA pipe (no F2I/FRND on the XU pipe)
+__device__ __forceinline__ float rint_magic(float x) {
+  return __fsub_rn(__fadd_rn(x, 12582912.0f), 12582912.0f);
+}
+
+// The slow stages, out of line; operands by value so the fast path keeps no stack.
+static __device__ __noinline__ SlowOut slow_pair(float4 P4, float4 N4, float4 X4, float4 NX4, int W,
+                                          double A, double b, double cos_As, int has_support,
+                                          int literal, int floor_bins, int mode) {
+  PairD D;
+  D.p[0] = P4.x; D.p[1] = P4.y; D.p[2] = P4.z;
+  D.n[0] = N4.x; D.n[1] = N4.y; D.n[2] = N4.z;
+  D.x[0] = X4.x; D.x[1] = X4.y; D.x[2] = X4.z;
+  D.nx[0] = NX4.x; D.nx[1] = NX4.y; D.nx[2] = NX4.z;
+  return slow_decide(D, W, A, b, cos_As, has_support, literal, floor_bins, mode);
+}
+
+// One candidate (centre slot g, point X): the certified fp32 decision, branch-free.
+//   status 0: certainly no contribution; 1: contributes (bin / weights below);
+//   2: some decision is not certified in fp32 -> slow_pair (fp64, then exact).
+struct Dec {
+  int status;
+  int bin;      // NEAREST: k*W + l; BILINEAR: i0*W + j0
+  float a, c;   // BILINEAR fractional offsets along k and l
+};
+
+template <int MODE>
+__device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const float4 N4,
+                                      const float4 X4, const float4 NX4) {
+  const float Wf = (float)p.W, Wm1 = Wf - 1.0f;
+  const float d0 = __fsub_rn(X4.x, P4.x), d1 = __fsub_rn(X4.y, P4.y), d2 = __fsub_rn(X4.z, P4.z);
+  // support test, inclusive, cosine form (#5); c_f = -inf disables it (ds = +inf)
+  const float s = fmaf(N4.x, NX4.x, fmaf(N4.y, NX4.y, N4.z * NX4.z));
+  const float ds = s - p.c_f;
+  const bool sup_out = ds < -p.Es_a;                                 // certainly rejected
+  const float be = fmaf(N4.x, d0, fmaf(N4.y, d1, N4.z * d2));       // np_i.(X-P)
+  const float dd = fmaf(d0, d0, fmaf(d1, d1, d2 * d2));              // ||X-P||^2
+  const float q = fmaf(-be, be, dd);                                 // alpha^2
+  // u = W/2 - beta/b (scaled, #2) or (W/2 - beta)/b (literal: Au = fl(W/(2b)), in Eu)
+  const float uval = fmaf(-be, p.inv_b, p.Au);
+  const float wval = q * p.inv_b2;                                   // (alpha/b)^2
+  // fp32 verdicts need the certified domain (|d| <= D) and |u| < 2^21 (magic rounding)
+  const bool unc0 = (p.no_fast_cert != 0) | !(ds > p.Es_a) | !(dd <= p.D2g) |
+                    !(fabsf(uval) < 2097152.0f);
+  Dec r;
+  r.a = 0.f;
+  r.c = 0.f;
+  if (MODE == 0) {
+    // the self pair (d == 0): beta = q = 0 exactly, k = ceil(W/2) (or floor), l = 0 (#8)
+    const bool self = (fabsf(d0) + fabsf(d1) + fabsf(d2) == 0.f) & (p.self_fast != 0);
+    // row k = ceil(u) (or floor): certified when u is farther than Eu from an integer;
+    // |u| < 2^22 inside the certified domain (dd <= D2g), garbage is ignored outside it
+    const float rr = rint_magic(uval);
+    const float du = uval - rr;                                      // exact
+    bool ku = !(fabsf(du) > p.Eu_a);
+    float kf = rr + (du > 0.f ? 1.0f : 0.0f) - p.floor_f;
+    // column l = ceil(sqrt(w)) (or floor): certified when w is farther than Ew from
+    // every perfect square (fl^2 is exact); sqrt only proposes fl, the squares decide
+    const float wc = fmaxf(wval, 0.0f);
+    float rs;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(fmaxf(wc, 1e-30f)));
+    const float fl = rint_magic(fmaf(wc, rs, -0.5f));
+    const float dlo = fmaf(-fl, fl, wval), dhi = fmaf(fl + 1.0f, fl + 1.0f, -wval);
+    const bool wneg = wval < -p.Ew_a;
+    bool lu = !(wneg | ((dlo > p.Ew_a) & (dhi > p.Ew_a)));
+    float lf = wneg ? 0.0f : fl + 1.0f - p.floor_f;
+    if (self) { kf = p.self_kf; lf = 0.0f; ku = false; lu = false; }
+    const bool out = (!ku & ((kf < 0.0f) | (kf >= Wf))) | (!lu & (lf >= Wf));
+    r.status = (sup_out | (!unc0 & out)) ? 0 : ((unc0 | ku | lu) ? 2 : 1);
+    r.bin = (int)kf * p.W + (int)lf;
+  } else {
+    // BILINEAR region 0 <= u < W-1, w < (W-1)^2  (#12); the self pair (u = W/2, w = 0)
+    // is interior for W >= 3 and needs no special case
+    const bool uu = !((fabsf(uval) > p.Eu_a) & (fabsf(uval - Wm1) > p.Eu_a));
+    const float lim = Wm1 * Wm1;
+    const bool wu = !(fabsf(wval - lim) > p.Ew_a);
+    const bool out = (!uu & !((uval > 0.f) & (uval < Wm1))) | (!wu & !(wval < lim));
+    r.status = (sup_out | (!unc0 & out)) ? 0 : ((unc0 | uu | wu) ? 2 : 1);
+    const float v = sqrtf(fmaxf(wval, 0.0f));
+    const float fi = fminf(fmaxf(rint_magic(uval - 0.5f), 0.0f), Wm1 - 1.0f);
+    const float fj = fminf(fmaxf(rint_magic(v - 0.5f), 0.0f), Wm1 - 1.0f);
+    r.a = fminf(fmaxf(uval - fi, 0.0f), 1.0f);
+    r.c = fminf(fmaxf(v - fj, 0.0f), 1.0f);
+    r.bin = (int)fi * p.W + (int)fj;
+  }
+  return r;
+}
+
+// Resolve an uncertain decision in fp64 / exactly (out of line, rare).
+template <int MODE>
+__device__ __forceinline__ void resolve(const KParams& p, Dec& d, const float4 P4, const float4 N4,
+                                        const float4 X4, const float4 NX4, Ctr& ct) {
+  ++ct.f64;
+  const SlowOut r = slow_pair(P4, N4, X4, NX4, p.W, p.A, p.b, p.cos_As, p.has_support, p.literal,
+                              p.floor_bins, MODE);
+  ct.exact += r.n_exact;
+  d.status = r.accept;
+  if (MODE == 0) d.bin = r.k * p.W + r.l;
+}
+
+// Splat an accepted pair into its image (tempSpinImage[k,l]++).
+template <int MODE>
+__device__ __forceinline__ void apply(const KParams& p, const Dec& d, uint32_t* img, uint32_t* hi,
+                                      int* carry_flag) {
+  if (MODE == 0) {
+    atomicAdd(&img[d.bin], 1u);
+  } else {
+    const int W = p.W;
+    add_fixed(img, hi, d.bin, (1.0f - d.a) * (1.0f - d.c), p.err_flags, carry_flag);
+    add_fixed(img, hi, d.bin + W, d.a * (1.0f - d.c), p.err_flags, carry_flag);
+    add_fixed(img, hi, d.bin + 1, (1.0f - d.a) * d.c, p.err_flags, carry_flag);
+    add_fixed(img, hi, d.bin + W + 1, d.a * d.c, p.err_flags, carry_flag);
+  }
+}
+
+// ------------------------------------------------------------------ the kernel
+// SUP = 1: the hot loop evaluates the support test for every pair (the paper's order,
+// P:166 before P:169-171); SUP = 0: the hot loop tests the region only and the support
+// test is decided in the accept path (SPIN_F_SUPPORT_LAST, or no support test at all).
+template <int MODE, int PRUNE, int G, int SUP>
+__global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__ KParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_chunk;
+  __shared__ int s_total, s_live;
+  __shared__ int s_rng[6];
+  __shared__ unsigned long long s_ctr[5];
+
+  const int W = p.W;
+  const int WW = W * W;
+  const Layout L = make_layout(G, W, MODE, PRUNE);
+  float4* sA = reinterpret_cast<float4*>(smem + L.oA);
+  float4* sB = reinterpret_cast<float4*>(smem + L.oB);
+  float4* sP = reinterpret_cast<float4*>(smem + L.oP);
+  float4* sN = reinterpret_cast<float4*>(smem + L.oN);
+  int* sM = reinterpret_cast<int*>(smem + L.oM);
+  uint32_t* sImg = reinterpret_cast<uint32_t*>(smem + L.oImg);
+  __shared__ int s_carry;
+  int* sRowS = reinterpret_cast<int*>(smem + L.oRowS);
+  int* sRowO = reinterpret_cast<int*>(smem + L.oRowO);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int QCAP = qcap_of(PRUNE);
+  uint16_t* sQ = reinterpret_cast<uint16_t*>(smem + L.oQ) + warp * QCAP;
+  // staged tile of this warp in pair layout: record r (0..3) of point pair pr (0..KP/2-1)
+  // of lane l at sT[(r * (KP/2) + pr) * 32 + l]; r0 {x,x',y,y'}, r1 {z,z',-|x|^2,-|x'|^2},
+  // r2 {nx,nx',ny,ny'}, r3 {nz,nz',0,0}
+  float4* sT = reinterpret_cast<float4*>(smem + L.oTP) + warp * 32 * KP * 2;
+  constexpr int CB = cb_of(G);
+  unsigned* sMask = reinterpret_cast<unsigned*>(smem + L.oMask) + warp * 32 * (G / CB);
+  const int hiWords = (WW + 1) / 2;
+  uint32_t* gHi = p.hi_scratch + (size_t)blockIdx.x * G * hiWords;   // zero outside groups
+  if (tid == 0) s_carry = 0;
+
+  if (tid < 5) s_ctr[tid] = 0ull;
+  const unsigned long long t0 = gtimer();
+  Ctr ct{0, 0, 0, 0};
+  int units_done = 0;
+  unsigned long long visited = 0;
+  bool first = true;
+
+  for (;;) {
+    // ---- a6: request a chunk (PAPER.md:336-342 / 372-377)
+    if (tid == 0) s_chunk = p.is_static ? (first ? (int)blockIdx.x : p.n_chunks)
+                                        : (int)atomicAdd(p.counter, 1u);
+    __syncthreads();
+    const int u = s_chunk;
+    first = false;
+    if (u >= p.n_chunks) break;
+    const int u0 = p.bounds[u], u1 = p.bounds[u + 1];
+    const long long i0 = (long long)u0 * p.unit_images;
+    const long long i1 = min((long long)u1 * p.unit_images, (long long)p.M);
+
+    for (long long g0 = i0; g0 < i1; g0 += G) {
+      const int gcount = (int)min((long long)G, i1 - g0);
+      // ---- a7: group setup (tempSpinImage, init, P = OP[i])
+      if (tid < G) {
+        const int slot = tid;
+        float4 A4 = make_float4(0.f, 0.f, 0.f, 0.f), B4 = make_float4(0.f, 0.f, 0.f, INFINITY);
+        float4 P4 = make_float4(0.f, 0.f, 0.f, 0.f), N4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        int mm = -1;
+        if (slot < gcount) {
+          const long long ip = g0 + slot;
+          const int m = p.order ? p.order[ip] : (int)ip;
+          const int c = p.centre_idx[m];
+          if (c >= 0 && c < p.N) {
+            P4 = __ldg(&p.cpos[c]);
+            N4 = __ldg(&p.cnrm[c]);
+            const double px = P4.x, py = P4.y, pz = P4.z, nx = N4.x, ny = N4.y, nz = N4.z;
+            const double np = nx * px + ny * py + nz * pz;
+            const double mid = p.mid;
+            const double C = (px * px + py * py + pz * pz) + 2.0 * mid * np + mid * mid;
+            const double Qt = p.Qmax - C + p.Eq_hot + 1e-12 * (fabs(C) + p.Qmax);
+            A4 = make_float4(N4.x, N4.y, N4.z, __double2float_rn(-np - mid));
+            // negated t-chain: -t = 2(p + mid n).x - |x|^2, tested as -q'' >= -Qt
+            B4 = make_float4(__double2float_rn(2.0 * (px + mid * nx)),
+                             __double2float_rn(2.0 * (py + mid * ny)),
+                             __double2float_rn(2.0 * (pz + mid * nz)), __double2float_rd(-Qt));
+            mm = m;
+          } else {
+            atomicOr(&p.err_flags[0], 1);
+            mm = -(m + 2);  // image written as zeros
+          }
+        }
+        sA[slot] = A4;
+        sB[slot] = B4;
+        sP[slot] = P4;
+        sN[slot] = N4;
+        sM[slot] = mm;
+      }
+      for (int i = tid; i < G * WW; i += NT) sImg[i] = 0u;
+      int nrows = 0;
+      if (PRUNE == 1) {
+        __syncthreads();
+        // bounding box of the live centres, grown by R (rounded outward)
+        if (warp == 0) {
+          float lo[3] = {INFINITY, INFINITY, INFINITY}, hi3[3] = {-INFINITY, -INFINITY, -INFINITY};
+          bool live = false;
+          for (int sl = lane; sl < G; sl += 32) {
+            if (sM[sl] >= 0) {
+              const float4 P4 = sP[sl];
+              live = true;
+              lo[0] = fminf(lo[0], P4.x); lo[1] = fminf(lo[1], P4.y); lo[2] = fminf(lo[2], P4.z);
+              hi3[0] = fmaxf(hi3[0], P4.x); hi3[1] = fmaxf(hi3[1], P4.y); hi3[2] = fmaxf(hi3[2], P4.z);
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+              hi3[a] = fmaxf(hi3[a], __shfl_xor_sync(0xffffffffu, hi3[a], o));
+            }
+          }
+          const int anyl = __any_sync(0xffffffffu, live);
+          if (lane == 0) {
+            s_live = anyl;
+            if (anyl) {
+              s_rng[0] = cell_coord(__fsub_rd(lo[0], p.R_up), p.ox, p.inv_h, p.dimx);
+              s_rng[1] = cell_coord(__fadd_ru(hi3[0], p.R_up), p.ox, p.inv_h, p.dimx);
+              s_rng[2] = cell_coord(__fsub_rd(lo[1], p.R_up), p.oy, p.inv_h, p.dimy);
+              s_rng[3] = cell_coord(__fadd_ru(hi3[1], p.R_up), p.oy, p.inv_h, p.dimy);
+              s_rng[4] = cell_coord(__fsub_rd(lo[2], p.R_up), p.oz, p.inv_h, p.dimz);
+              s_rng[5] = cell_coord(__fadd_ru(hi3[2], p.R_up), p.oz, p.inv_h, p.dimz);
+            }
+          }
+        }
+        __syncthreads();
+        if (s_live) nrows = (s_rng[3] - s_rng[2] + 1) * (s_rng[5] - s_rng[4] + 1);
+      }
+      __syncthreads();
+
+      // ---- a8-a10: stream points, pair test, compact, accept
+      // Each thread holds KP points in registers for all G centres.  Per batch of CB
+      // centres the pass bits go to one u32 mask (bit = c*KP + k) stored in smem; once
+      // per tile the warp compacts all its bits into a ring of 16-bit entries
+      // (centre slot << 7 | lane << 2 | k) and processes them 32 at a time, reading the
+      // point from the warp's staged copy of the tile (no global re-load).
+      unsigned qhead = 0, qtail = 0;
+      constexpr int NWD = G / CB;                      // mask words per lane per tile
+      // candidate operands: centre slot gs, point (source lane, k) from the staged tile
+      auto load_entry = [&](unsigned e, float4& P4, float4& N4, float4& X4, float4& NX4) {
+        const int gs = (int)(e >> 7);
+        const int src = (int)(e & 127u);
+        P4 = sP[gs];
+        N4 = sN[gs];
+        const int sl = src >> LOGKP, kk = src & (KP - 1);           // source lane, point k
+        const float* rec = reinterpret_cast<const float*>(sT + (kk >> 1) * 32 + sl) + (kk & 1);
+        constexpr int RS = (KP / 2) * 32 * 4;                       // floats between records
+        X4 = make_float4(rec[0], rec[2], rec[RS], 0.f);
+        NX4 = make_float4(rec[2 * RS], rec[2 * RS + 2], rec[3 * RS], 0.f);
+      };
+      // CELLS (dense, latency-bound) takes two candidates per lane per pass so that the
+      // two independent decisions interleave; BRUTE keeps one (fewer live registers).
+      constexpr int APL = PRUNE == 1 ? 2 : 1;
+      auto process_pair = [&](unsigned e0, bool v0, unsigned e1, bool v1) {
+        if (p.debug_skip) return;
+        float4 P0, N0, X0, NX0, P1, N1, X1, NX1;
+        load_entry(e0, P0, N0, X0, NX0);
+        Dec d0 = decide<MODE>(p, P0, N0, X0, NX0);
+        Dec d1;
+        d1.status = 0;
+        if (APL == 2) {
+          load_entry(e1, P1, N1, X1, NX1);
+          d1 = decide<MODE>(p, P1, N1, X1, NX1);
+          if (!v1) d1.status = 0;
+        }
+        if (!v0) d0.status = 0;
+        ct.cand += (unsigned)v0 + (APL == 2 ? (unsigned)v1 : 0u);
+        if (d0.status == 2) resolve<MODE>(p, d0, P0, N0, X0, NX0, ct);
+        if (APL == 2 && d1.status == 2) resolve<MODE>(p, d1, P1, N1, X1, NX1, ct);
+        const int g0 = (int)(e0 >> 7), g1 = (int)(e1 >> 7);
+        if (d0.status) { ++ct.acc; apply<MODE>(p, d0, sImg + g0 * WW, gHi + g0 * hiWords, &s_carry); }
+        if (APL == 2 && d1.status) {
+          ++ct.acc;
+          apply<MODE>(p, d1, sImg + g1 * WW, gHi + g1 * hiWords, &s_carry);
+        }
+      };
+      auto compact_and_accept = [&]() {
+        int cnt = 0;
+#pragma unroll
+        for (int w = 0; w < NWD; ++w) cnt += __popc(sMask[w * 32 + lane]);
+        int x = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, x, 31);
+        if (total == 0) return;
+        // common case: the whole tile fits the ring and one scan places every entry;
+        // dense tiles go a quarter mask word (2 centres, <= 256 entries) at a time, each
+        // appended after the ring was drained to < 64 pending entries (QCAP >= 512).
+        static_assert(QCAP >= 64 + 256, "ring too small for the dense path");
+        const bool dense = total > QCAP - 64;
+        const int nchunks = dense ? 4 * NWD : 1;
+        for (int ci = 0;;) {
+          if (ci < nchunks) {
+            if (!dense) {
+              unsigned pos = qtail + (unsigned)(x - cnt);
+#pragma unroll
+              for (int w = 0; w < NWD; ++w) {
+                unsigned m = sMask[w * 32 + lane];
+                while (m) {
+                  const int bit = __ffs(m) - 1;
+                  m &= m - 1u;
+                  sQ[pos & (QCAP - 1)] =
+                      (uint16_t)(((w * CB + (bit >> LOGKP)) << 7) | (lane << LOGKP) | (bit & (KP - 1)));
+                  ++pos;
+                }
+              }
+              qtail += (unsigned)total;
+            } else {
+              const int quarter = ci & 3;
+              unsigned m = (sMask[(ci >> 2) * 32 + lane] >> (8 * quarter)) & 0xffu;
+              const int c2 = __popc(m);
+              int x2 = c2;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x2, o);
+                if (lane >= o) x2 += y;
+              }
+              const int t2 = __shfl_sync(0xffffffffu, x2, 31);
+              unsigned pos = qtail + (unsigned)(x2 - c2);
+              const int cbase = (ci >> 2) * CB + (8 / KP) * quarter;
+              while (m) {
+                const int bit = __ffs(m) - 1;
+                m &= m - 1u;
+                sQ[pos & (QCAP - 1)] =
+                    (uint16_t)(((cbase + (bit >> LOGKP)) << 7) | (lane << LOGKP) | (bit & (KP - 1)));
+                ++pos;
+              }
+              qtail += (unsigned)t2;
+            }
+            ++ci;
+          }
+          const bool more = ci < nchunks;
+          __syncwarp();
+          for (;;) {
+            const unsigned avail = qtail - qhead;
+            constexpr unsigned PASS = 32u * APL;
+            if (avail == 0u || (avail < PASS && more)) break;
+            const unsigned n = min(PASS, avail);
+            const bool v0 = (unsigned)lane < n, v1 = APL == 2 && (unsigned)lane + 32u < n;
+            const unsigned e0 = sQ[(qhead + lane) & (QCAP - 1)];
+            const unsigned e1 = APL == 2 ? sQ[(qhead + 32u + lane) & (QCAP - 1)] : 0u;
+            __syncwarp();
+            qhead += n;
+            if (v0) process_pair(v0 ? e0 : 0u, v0, v1 ? e1 : 0u, v1);
+          }
+          if (!more) break;
+        }
+      };
+      auto run_tile = [&](const int (&j)[KP]) {
+        // stage the tile in pair layout (also the accept path's copy), then read the
+        // records back so each f32x2 operand arrives as an aligned register pair
+        f2 X2[KP / 2], Y2[KP / 2], Z2[KP / 2], NXX2[KP / 2], NX2[KP / 2], NY2[KP / 2], NZ2[KP / 2];
+#pragma unroll
+        for (int k = 0; k < KP; k += 2) {
+          const float4 a0 = __ldg(&p.pos[j[k]]), a1 = __ldg(&p.pos[j[k + 1]]);
+          const float4 b0 = __ldg(&p.nrm[j[k]]), b1 = __ldg(&p.nrm[j[k + 1]]);
+          const int pr = k / 2;
+          sT[(0 * (KP / 2) + pr) * 32 + lane] = make_float4(a0.x, a1.x, a0.y, a1.y);
+          sT[(1 * (KP / 2) + pr) * 32 + lane] = make_float4(a0.z, a1.z, -a0.w, -a1.w);
+          sT[(2 * (KP / 2) + pr) * 32 + lane] = make_float4(b0.x, b1.x, b0.y, b1.y);
+          sT[(3 * (KP / 2) + pr) * 32 + lane] = make_float4(b0.z, b1.z, 0.f, 0.f);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int pr = 0; pr < KP / 2; ++pr) {
+          f2 r[8];
+          const float4* base = sT + pr * 32 + lane;
+          asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r[0]), "=l"(r[1]) : "r"((unsigned)__cvta_generic_to_shared(base)));
+          asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r[2]), "=l"(r[3]) : "r"((unsigned)__cvta_generic_to_shared(base + (KP / 2) * 32)));
+          asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r[4]), "=l"(r[5]) : "r"((unsigned)__cvta_generic_to_shared(base + 2 * (KP / 2) * 32)));
+          asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r[6]), "=l"(r[7]) : "r"((unsigned)__cvta_generic_to_shared(base + 3 * (KP / 2) * 32)));
+          X2[pr] = r[0]; Y2[pr] = r[1]; Z2[pr] = r[2]; NXX2[pr] = r[3];
+          NX2[pr] = r[4]; NY2[pr] = r[5]; NZ2[pr] = r[6];
+        }
+        const float c_test = p.c_test, h_test = p.h_test;
+#pragma unroll 1
+        for (int cb = 0; cb < G; cb += CB) {
+          unsigned mask = 0u;
+          if (cb >= gcount) {            // a partial group skips its empty slots
+            sMask[(cb / CB) * 32 + lane] = 0u;
+            continue;
+          }
+#pragma unroll
+          for (int c = 0; c < CB; ++c) {
+            const float4 A4 = sA[cb + c];
+            const float4 B4 = sB[cb + c];
+#pragma unroll
+            for (int k2 = 0; k2 < KP / 2; ++k2) {
+              // support n.nx; beta'' = n.x - n.p - mid;
+              // -q'' = beta''^2 + 2(p + mid n).x - |x|^2 = C - q
+              f2 s2 = 0ull;
+              if (SUP) s2 = fma2(bc2(A4.x), NX2[k2], fma2(bc2(A4.y), NY2[k2], mul2(bc2(A4.z), NZ2[k2])));
+              const f2 be2 = fma2(bc2(A4.x), X2[k2], fma2(bc2(A4.y), Y2[k2], fma2(bc2(A4.z), Z2[k2], bc2(A4.w))));
+              const f2 tn2 = fma2(bc2(B4.x), X2[k2], fma2(bc2(B4.y), Y2[k2], fma2(bc2(B4.z), Z2[k2], NXX2[k2])));
+              const f2 qn2 = fma2(be2, be2, tn2);
+              float s0, s1, b0, b1, q0, q1;
+              up2(s2, s0, s1);
+              up2(be2, b0, b1);
+              up2(qn2, q0, q1);
+              const int bit = c * KP + 2 * k2;
+              if (SUP) {
+                mask = pair_bit_n(mask, s0, c_test, fabsf(b0), h_test, q0, B4.w, 1u << bit);
+                mask = pair_bit_n(mask, s1, c_test, fabsf(b1), h_test, q1, B4.w, 1u << (bit + 1));
+              } else {
+                mask = pair_bit_r(mask, fabsf(b0), h_test, q0, B4.w, 1u << bit);
+                mask = pair_bit_r(mask, fabsf(b1), h_test, q1, B4.w, 1u << (bit + 1));
+              }
+            }
+          }
+          sMask[(cb / CB) * 32 + lane] = mask;
+        }
+        __syncwarp();
+        if (p.debug_skip < 2) compact_and_accept();
+        __syncwarp();
+      };
+
+      if (PRUNE == 0) {
+        for (int t = 0; t < p.n_tiles; ++t) {
+          const int base = t * (NT * KP) + tid;
+          int j[KP];
+#pragma unroll
+          for (int k = 0; k < KP; ++k) j[k] = base + k * NT;
+          run_tile(j);
+        }
+      } else {
+        // rows of the visited box, batched ROWCAP at a time
+        const int cx0 = s_rng[0], cx1 = s_rng[1], cy0 = s_rng[2], cy1 = s_rng[3], cz0 = s_rng[4];
+        const int ny = cy1 - cy0 + 1;
+        for (int rb = 0; rb < nrows; rb += ROWCAP) {
+          const int nb = min(ROWCAP, nrows - rb);
+          int len = 0, start = 0;
+          if (tid < nb) {
+            const int row = rb + tid;
+            const int cz = cz0 + row / ny, cy = cy0 + row % ny;
+            const int base = (cz * p.dimy + cy) * p.dimx;
+            start = p.cell_start[base + cx0];
+            len = p.cell_start[base + cx1 + 1] - start;
+          }
+          // block exclusive scan of len over NT threads
+          int v = len;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int n = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += n;
+          }
+          __shared__ int s_wsum[NWARP];
+          if (lane == 31) s_wsum[warp] = v;
+          __syncthreads();
+          if (warp == 0) {
+            int ws = lane < NWARP ? s_wsum[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < NWARP; o <<= 1) {
+              const int n = __shfl_up_sync(0xffffffffu, ws, o);
+              if (lane >= o) ws += n;
+            }
+            if (lane < NWARP) s_wsum[lane] = ws;
+            if (lane == NWARP - 1) s_total = ws;
+          }
+          __syncthreads();
+          const int excl = v - len + (warp > 0 ? s_wsum[warp - 1] : 0);
+          if (tid < nb) {
+            sRowS[tid] = start;
+            sRowO[tid] = excl;
+          }
+          if (tid == 0) sRowO[nb] = s_total;
+          __syncthreads();
+          const int T = s_total;
+          if (tid == 0) {
+            int live = 0;
+            for (int g = 0; g < G; ++g) live += sM[g] >= 0;
+            visited += (unsigned long long)T * live;
+          }
+          for (int f0 = 0; f0 < T; f0 += NT * KP) {
+            int j[KP];
+#pragma unroll
+            for (int k = 0; k < KP; ++k) {
+              const int f = f0 + tid + k * NT;
+              if (f < T) {
+                int lo = 0, hi = nb - 1;   // largest r with sRowO[r] <= f
+                while (lo < hi) {
+                  const int mid = (lo + hi + 1) >> 1;
+                  if (sRowO[mid] <= f) lo = mid; else hi = mid - 1;
+                }
+                j[k] = sRowS[lo] + (f - sRowO[lo]);
+              } else {
+                j[k] = p.N;  // sentinel
+              }
+            }
+            run_tile(j);
+          }
+          __syncthreads();
+        }
+      }
+      __syncthreads();
+      // ---- a12: write the images back in the caller's order
+      for (int i = tid; i < G * WW; i += NT) {
+        const int slot = i / WW;
+        const int e = i - slot * WW;
+        int mm = sM[slot];
+        if (mm == -1) continue;
+        float val = 0.0f;
+        if (mm < -1) {
+          mm = -(mm + 2);
+        } else if (MODE == 0) {
+          const uint32_t cnt = sImg[i];
+          if (cnt >= (1u << 24)) atomicOr(&p.err_flags[1], 1);
+          val = (float)cnt;
+        } else {
+          const uint32_t h =
+              s_carry ? (gHi[slot * hiWords + (e >> 1)] >> ((e & 1) * 16)) & 0xffffu : 0u;
+          const double fx = (double)h * 4294967296.0 + (double)sImg[i];
+          val = (float)(fx * (1.0 / 8388608.0));
+        }
+        __stcs(&p.out[(long long)mm * WW + e], val);
+      }
+      if (p.seg_done != nullptr) {
+        // e2e pipelining (spin_generate_host): publish finished images per output segment
+        // so the copy stream can start their D2H while the kernel still runs
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0) {
+          long long a = g0;
+          const long long bnd = g0 + gcount;
+          while (a < bnd) {
+            const long long sg = a / p.seg_images;
+            const long long e = min(bnd, (sg + 1) * (long long)p.seg_images);
+            atomicAdd(&p.seg_done[sg], (unsigned)(e - a));
+            a = e;
+          }
+        }
+      }
+      if (MODE == 1) {
+        __syncthreads();
+        if (s_carry) {                       // leave the carry scratch zero for the next group
+          for (int i = tid; i < G * hiWords; i += NT) gHi[i] = 0u;
+          __syncthreads();
+          if (tid == 0) s_carry = 0;
+        }
+      }
+      __syncthreads();
+    }
+    units_done += u1 - u0;
+  }
+
+  // ---- a13: instrumentation
+  const unsigned long long t1 = gtimer();
+  atomicAdd(&s_ctr[0], (unsigned long long)ct.cand);
+  atomicAdd(&s_ctr[1], (unsigned long long)ct.acc);
+  atomicAdd(&s_ctr[2], (unsigned long long)ct.f64);
+  atomicAdd(&s_ctr[3], (unsigned long long)ct.exact);
+  if (tid == 0) atomicAdd(&s_ctr[4], visited);
+  __syncthreads();
+  if (tid == 0) {
+    atomicAdd(&p.stats[ST_CAND], s_ctr[0]);
+    atomicAdd(&p.stats[ST_ACC], s_ctr[1]);
+    atomicAdd(&p.stats[ST_F64], s_ctr[2]);
+    atomicAdd(&p.stats[ST_EXACT], s_ctr[3]);
+    atomicAdd(&p.stats[ST_VISITED], s_ctr[4]);
+    p.cta_t0[blockIdx.x] = t0;
+    p.cta_t1[blockIdx.x] = t1;
+    p.cta_units[blockIdx.x] = units_done;
+  }
+}
+
+}  // namespace spin
