@@ -47,8 +47,9 @@ def parse(argv=None):
     ap.add_argument("--W", type=int, default=None)
     ap.add_argument("--P", type=int, default=0)
     ap.add_argument("--unit", type=int, default=0)
-    ap.add_argument("--support-last", action="store_true",
-                    help="SPIN_F_SUPPORT_LAST: decide the support test only for region candidates")
+    ap.add_argument("--support", choices=("auto", "first", "last"), default="auto",
+                    help="support-test placement: library default (BRUTE adaptive per warp), "
+                         "SPIN_F_SUPPORT_FIRST (every pair, P:166 order), SPIN_F_SUPPORT_LAST")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -250,7 +251,7 @@ def run_spin(args):
     d_cen = torch.from_numpy(cen).to(dev)
     out = torch.empty((M, W, W), dtype=torch.float32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # > 126 MB L2
-    flags = spin.F_SUPPORT_LAST if args.support_last else 0
+    flags = {"auto": 0, "first": spin.F_SUPPORT_FIRST, "last": spin.F_SUPPORT_LAST}[args.support]
     kw = dict(schedule=args.schedule, mode=mode, prune=prune, P=args.P, unit=args.unit, out=out,
               flags=flags)
 
@@ -289,12 +290,11 @@ def run_spin(args):
     pairs_step = st0["pairs_visited"]
     achieved_tflops = pairs_step * FLOP_PER_PAIR / (kern * 1e-3) / 1e12
 
-    # secondary (same run): the support test decided only for region candidates
-    # (SPIN_F_SUPPORT_LAST) -- identical images, fewer flops per pair; reported beside
-    # the main line, which keeps the paper's order (support test on every pair)
+    # secondary (same run): the support test on every pair in the hot loop, the paper's
+    # order (P:166 before P:169-171) -- identical images; reported beside the main line
     alt = None
-    if not args.support_last and cfg["cos_As"] > -math.inf:
-        akw = dict(kw, flags=spin.F_SUPPORT_LAST)
+    if args.support == "auto" and cfg["cos_As"] > -math.inf:
+        akw = dict(kw, flags=spin.F_SUPPORT_FIRST)
         for _ in range(2):
             eng.generate(d_cen, W, b, c, **akw)
         torch.cuda.synchronize()
@@ -308,12 +308,12 @@ def run_spin(args):
         torch.cuda.synchronize()
         a_ms = allreduce_max(sum(e0.elapsed_time(e1) for e0, e1 in aev), dev) / args.steps
         _, ast = eng.generate(d_cen, W, b, c, stats=True, **akw)
-        alt = {"flag": "SPIN_F_SUPPORT_LAST", "value": pairs_step * world / (a_ms * 1e-3),
+        alt = {"flag": "SPIN_F_SUPPORT_FIRST", "value": pairs_step * world / (a_ms * 1e-3),
                "unit": UNIT, "ms_per_step": a_ms, "kernel_ms": ast["elapsed_ms"],
                "fp32_frac_algorithmic_20flop": pairs_step * FLOP_PER_PAIR / (ast["elapsed_ms"] * 1e-3)
                                                / (FP32_PEAK_TFLOPS * 1e12),
-               "flop_per_pair_executed": 14, "pairs_candidate": ast["pairs_candidate"],
-               "note": "hot loop skips n.n_x (3 FMA + 1 compare) for non-candidates; images identical"}
+               "pairs_candidate": ast["pairs_candidate"],
+               "note": "support test n.n_x >= cos_As on every pair in the hot loop; images identical"}
 
     pairs_all = pairs_step * world
     value = pairs_all * args.steps / (total_ms * 1e-3)
@@ -354,7 +354,10 @@ def run_spin(args):
         "config": {"workload": cfg["name"], "N": N, "M": M, "W": W, "b": b, "cos_As": c,
                    "mode": mode, "prune": prune, "schedule": args.schedule,
                    "P": st0["P"], "G": st0["G"], "unit": args.unit or st0["G"],
-                   "support_test": "after region test" if args.support_last else "every pair (P:166 order)",
+                   "support_test": {"auto": "adaptive per warp tile (library default)",
+                                    "first": "every pair (P:166 order)",
+                                    "last": "candidates only"}[args.support],
+                   "tiles_support_hot": st0["tiles_support_hot"],
                    "n_chunks": st0["n_chunks"], "l2": "flushed (256 MB write) before every step",
                    "parallelism": f"replicas x{world} (independent images, no collective)"},
         "images_per_s": images_per_s,
@@ -369,7 +372,7 @@ def run_spin(args):
         "pairs": {"visited": st0["pairs_visited"], "candidate": st0["pairs_candidate"],
                   "accepted": st0["pairs_accepted"], "fp64_fallbacks": st0["fp64_fallbacks"],
                   "exact_fallbacks": st0["exact_fallbacks"]},
-        "support_last": alt,
+        "support_first": alt,
         "clocks": clocks,
         "e2e": e2e,
         "gpu_launches": launches * args.steps,

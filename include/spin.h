@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SPIN_ABI_VERSION 1
+#define SPIN_ABI_VERSION 2
 
 typedef struct spin_ctx* spin_handle;
 typedef struct CUstream_st* spin_stream; /* identical to cudaStream_t */
@@ -68,8 +68,11 @@ typedef enum { SPIN_BRUTE = 0, SPIN_CELLS = 1 } spin_prune;
 #define SPIN_F_FLOOR_BINS         0x2u /* NEAREST: k = floor(u), l = floor(v) (Johnson) instead of ceil */
 #define SPIN_F_NO_SORT            0x4u /* CELLS: keep the caller's centre order (control run)    */
 #define SPIN_F_NO_FAST_CERT       0x8u /* testing: send every candidate through the fp64 / exact decision stages   */
-#define SPIN_F_SUPPORT_LAST       0x10u /* evaluate the support test only for pairs inside the region: same
-                                           images, fewer flops per pair (the region test runs first)            */
+#define SPIN_F_SUPPORT_LAST       0x10u /* evaluate the support test only for the pair-test candidates: same
+                                           images, fewer flops per pair (the geometric test runs first)         */
+#define SPIN_F_SUPPORT_FIRST      0x20u /* evaluate the support test for every pair, as P:166 orders it.  With
+                                           neither flag, CELLS does so and BRUTE places it adaptively per warp
+                                           (accept path while it rejects few candidates)         */
 
 /* Scheduling parameters.  All-zero = defaults. */
 typedef struct {
@@ -100,6 +103,8 @@ typedef struct {
   uint64_t* h_cta_end_ns;   /* caller array [P] or NULL: %globaltimer at CTA finish        */
   int32_t* h_cta_units;     /* caller array [P] or NULL: units processed per CTA           */
   int32_t cta_capacity;     /* length of the three arrays above                            */
+  int64_t tiles_support_hot; /* BRUTE: warp tiles (32 x 4 points x G centres) whose hot
+                                 loop ran the support test (adaptive placement)             */
 } spin_stats;
 
 /*

@@ -430,7 +430,9 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   if (cp) cpar = *cp;
   if (cpar.P < 0 || cpar.unit < 0 || cpar.gss_min_chunk < 0 || cpar.fac_divisor < 0)
     return fail(SPIN_E_INVAL, "negative chunk parameter");
-  if (cpar.flags & ~0x1fu) return fail(SPIN_E_INVAL, "unknown flag bits 0x%x", cpar.flags);
+  if (cpar.flags & ~0x3fu) return fail(SPIN_E_INVAL, "unknown flag bits 0x%x", cpar.flags);
+  if ((cpar.flags & SPIN_F_SUPPORT_LAST) && (cpar.flags & SPIN_F_SUPPORT_FIRST))
+    return fail(SPIN_E_INVAL, "SPIN_F_SUPPORT_LAST and SPIN_F_SUPPORT_FIRST are exclusive");
   if (M > 0 && (!d_centre_idx || !d_out)) return fail(SPIN_E_INVAL, "null d_centre_idx or d_out with M > 0");
   if (stats) {
     stats->elapsed_ms = stats->grid_build_ms = 0.0;
@@ -483,28 +485,44 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   const double X = std::max((double)h->absmax, 1e-30) * (1.0 + 1e-6);
   const double u = U32;
   const double amid = std::fabs(rg.mid);
-  // hot loop (fp32, expanded forms; bounds hold for any pair inside the region)
+  // hot loop (fp32): candidates are the pairs inside the sphere about the rounded window
+  // centre c~ = fl(2(p + mid n))/2 that contains the region cylinder (|beta - mid| <= h,
+  // alpha^2 <= Qmax), margin m = B.x - |x|^2 + K with B = 2c~, K = rho^2 - |c~|^2 + 2E
+  // (DESIGN.md 7.1).  |c~ - c'| <= u (X + |mid|) widens the radius.
+  const double rho = std::sqrt(rg.h * rg.h + rg.Qmax) + 1.01 * u * (X + amid);
+  const double Ms = rho * rho + (2.0 * X + amid) * (2.0 * X + amid) * 1.01;
+  const double E_sph = 6.0 * u * Ms * 1.05;
+  const double Es_h = 4.0 * u * 1.01;
+  // CELLS hot loop: the region cylinder in expanded forms (bounds hold inside the region)
   const double Eb_h = 8.0 * u * (X + amid) * 1.01;
   const double Et_h = 16.0 * u * (X + amid) * (X + amid) * 1.01;
   const double Eq_h = Et_h + Eb_h * (2.0 * rg.h + Eb_h) + 2.0 * u * (rg.Qmax + 2.0 * (X + amid) * (X + amid));
-  const double Es_h = 4.0 * u * 1.01;
   KParams p{};
   p.b = b;
   p.cos_As = has_support ? cos_As : -INFINITY;
   p.A = 0.5 * W;
   p.mid = rg.mid;
   p.Qmax = rg.Qmax;
+  p.rho2 = rho * rho;
+  p.E_sph = E_sph;
   p.Eq_hot = Eq_h;
-  p.c_test = has_support ? f32_down(cos_As - Es_h) : -INFINITY;
   p.h_test = f32_up(rg.h + Eb_h);
+  p.c_test = has_support ? f32_down(cos_As - Es_h) : -INFINITY;
   p.has_support = has_support ? 1 : 0;
-  // the hot loop skips the support test when there is none, or when asked to decide it
-  // only for geometric candidates (SPIN_F_SUPPORT_LAST; same result, fewer flops)
-  p.support_in_hot = (has_support && !(cpar.flags & SPIN_F_SUPPORT_LAST)) ? 1 : 0;
-  // candidates satisfy |d| <= D: q <= Qmax + 2Eq, |beta| <= |mid| + h_test + Eb
+  // where the support test runs (same images either way): not at all without one; in the
+  // accept path only (SPIN_F_SUPPORT_LAST); on every pair (SPIN_F_SUPPORT_FIRST, and CELLS
+  // by default); BRUTE by default adaptively per warp (2)
+  p.support_in_hot = !has_support ? 0
+                     : (cpar.flags & SPIN_F_SUPPORT_LAST) ? 0
+                     : (cpar.flags & SPIN_F_SUPPORT_FIRST) ? 1
+                     : (prune == SPIN_BRUTE ? 2 : 1);
+  // candidates satisfy |d| <= D.  BRUTE: |x - c~|^2 <= rho^2 + 4E, so
+  // |d| <= |c~ - p| + sqrt(rho^2 + 4E).  CELLS: q <= Qmax + 2Eq, |beta| <= |mid| + h_test + Eb.
+  const double Dh = (amid + 1.01 * u * (X + amid) + std::sqrt(rho * rho + 4.0 * E_sph)) * 1.001;
   const double Cmax = (X + amid) * (X + amid) * 1.01;
   const double bmax = amid + (double)p.h_test + Eb_h;
-  const double D2 = (rg.Qmax + 2.0 * Eq_h + 4.0 * u * (rg.Qmax + Cmax) + bmax * bmax) * 1.001 + 1e-30;
+  const double D2c = (rg.Qmax + 2.0 * Eq_h + 4.0 * u * (rg.Qmax + Cmax) + bmax * bmax) * 1.001;
+  const double D2 = (prune == SPIN_BRUTE ? Dh * Dh : D2c) + 1e-30;
   const double D = std::sqrt(D2);
   // accept path, fp32 direct forms, valid while |d| <= D
   const double Es_a = 5.5 * u * 1.01;
@@ -656,6 +674,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
     stats->pairs_accepted = (int64_t)sv[ST_ACC];
     stats->fp64_fallbacks = (int64_t)sv[ST_F64];
     stats->exact_fallbacks = (int64_t)sv[ST_EXACT];
+    stats->tiles_support_hot = (int64_t)sv[ST_SUPHOT];
     stats->P = P;
     stats->G = lc.G;
     stats->n_units = (int32_t)n_units;

@@ -1,5 +1,6 @@
 // spin_inst.cu — explicit instantiations of spin_persistent for one (MODE, SUP) pair,
-// selected with -DINST_MODE=0|1 -DINST_SUP=0|1 (built four times by build.py).
+// selected with -DINST_MODE=0|1 -DINST_SUP=0|1|2 (built six times by build.py; the
+// adaptive SUP = 2 exists for BRUTE only).
 #include "spin_persistent.cuh"
 
 namespace spin {
@@ -16,6 +17,9 @@ const void* SPIN_CAT(kernel_ptr_, INST_MODE, INST_SUP)(int prune, int G) {
       default: return (const void*)spin_persistent<INST_MODE, 0, 64, INST_SUP>;
     }
   }
+#if INST_SUP == 2
+  return nullptr;
+#else
   switch (G) {
     case 4: return (const void*)spin_persistent<INST_MODE, 1, 4, INST_SUP>;
     case 8: return (const void*)spin_persistent<INST_MODE, 1, 8, INST_SUP>;
@@ -23,6 +27,7 @@ const void* SPIN_CAT(kernel_ptr_, INST_MODE, INST_SUP)(int prune, int G) {
     case 32: return (const void*)spin_persistent<INST_MODE, 1, 32, INST_SUP>;
     default: return (const void*)spin_persistent<INST_MODE, 1, 64, INST_SUP>;
   }
+#endif
 }
 
 }  // namespace spin

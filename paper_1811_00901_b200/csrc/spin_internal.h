@@ -36,10 +36,13 @@ struct KParams {
   double b, cos_As;          // cos_As = -inf disables the support test
   double A;                  // W/2
   double mid, Qmax;          // beta window centre, alpha^2 bound: region is |beta-mid|<=h, q<=Qmax
-  double Eq_hot;             // hot-loop bound on |q''_fp32 - q''| (added to Qmax - C per centre)
-  float c_test, h_test;      // hot loop: s >= c_test, |beta''| <= h_test
+  double rho2;               // hot loop: squared radius of the sphere about the (rounded)
+                             // window centre that contains the region
+  double E_sph;              // hot-loop bound on the fp32 error of the sphere margin
+  double Eq_hot;             // CELLS hot loop: bound on |q''_fp32 - q''| (added to Qmax - C)
+  float c_test, h_test;      // hot loop: s >= c_test (support), CELLS |beta''| <= h_test
   int32_t has_support;
-  int32_t support_in_hot;    // 1: hot loop tests the support (default); 0: accept path only
+  int32_t support_in_hot;    // 1: hot loop tests the support; 0: accept path only; 2: adaptive (BRUTE)
   // accept path, fp32 stage
   float c_f;                 // (float)cos_As, its rounding is inside Es_a
   float inv_b, inv_b2, Af;
@@ -72,7 +75,7 @@ struct KParams {
 };
 
 enum StatSlot {
-  ST_VISITED = 0, ST_CAND = 1, ST_ACC = 2, ST_F64 = 3, ST_EXACT = 4, ST_NSLOTS = 8
+  ST_VISITED = 0, ST_CAND = 1, ST_ACC = 2, ST_F64 = 3, ST_EXACT = 4, ST_SUPHOT = 5, ST_NSLOTS = 8
 };
 
 // Launch configuration chosen by the planner.

@@ -10,9 +10,12 @@ const void* kernel_ptr_0_0(int prune, int G);
 const void* kernel_ptr_0_1(int prune, int G);
 const void* kernel_ptr_1_0(int prune, int G);
 const void* kernel_ptr_1_1(int prune, int G);
+const void* kernel_ptr_0_2(int prune, int G);
+const void* kernel_ptr_1_2(int prune, int G);
 static const void* kernel_for(int mode, int prune, int G, int sup) {
-  if (mode == 0) return sup ? kernel_ptr_0_1(prune, G) : kernel_ptr_0_0(prune, G);
-  return sup ? kernel_ptr_1_1(prune, G) : kernel_ptr_1_0(prune, G);
+  if (prune == 1 && sup == 2) sup = 1;   // adaptive placement is BRUTE-only
+  if (mode == 0) return sup == 2 ? kernel_ptr_0_2(prune, G) : sup ? kernel_ptr_0_1(prune, G) : kernel_ptr_0_0(prune, G);
+  return sup == 2 ? kernel_ptr_1_2(prune, G) : sup ? kernel_ptr_1_1(prune, G) : kernel_ptr_1_0(prune, G);
 }
 
 LaunchCfg choose_launch(int W, int mode, int prune) {

@@ -41,7 +41,7 @@ namespace spin {
 
 constexpr int NT = SPIN_NT;       // threads per CTA (one CTA per SM)
 constexpr int NWARP = NT / 32;
-constexpr int KP = SPIN_KP;       // points per thread (register blocking), 2 or 4
+constexpr int KP = SPIN_KP;       // points per thread (register blocking)
 constexpr int LOGKP = KP == 4 ? 2 : 1;
 constexpr int CB_MAX = 32 / KP;   // centres per mask batch: CB * KP <= 32 bits
 __host__ __device__ constexpr int cb_of(int G) { return G < CB_MAX ? G : CB_MAX; }
@@ -50,7 +50,7 @@ __host__ __device__ constexpr int cb_of(int G) { return G < CB_MAX ? G : CB_MAX;
 __host__ __device__ constexpr int qcap_of(int prune) { return prune ? 1024 : 512; }
 constexpr int ROWCAP = NT;        // CELLS: grid rows staged per batch
 
-static_assert(CB_MAX * KP == 32, "mask is one u32");
+static_assert(CB_MAX * KP == 32 && KP == 4, "mask is one u32: bit (k << 3) | c");
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -70,20 +70,6 @@ __device__ __forceinline__ int cell_coord(float x, float o, float inv_h, int dim
   float t = __fmul_rn(__fsub_rn(x, o), inv_h);
   t = fminf(fmaxf(t, 0.0f), (float)(dim - 1));
   return (int)floorf(t);
-}
-
-// The conservative pair test as ONE predicate chain plus one predicated OR:
-// pass = (s >= c) && (|beta''| <= h) && (q'' <= Qt)  (NaN compares false).
-__device__ __forceinline__ unsigned pair_bit(unsigned mask, float s, float c, float abe, float h,
-                                             float q, float qt, unsigned bit) {
-  asm("{\n\t.reg .pred p;\n\t"
-      "setp.ge.f32 p, %1, %2;\n\t"
-      "setp.le.and.f32 p, %3, %4, p;\n\t"
-      "setp.le.and.f32 p, %5, %6, p;\n\t"
-      "@p or.b32 %0, %0, %7;\n\t}"
-      : "+r"(mask)
-      : "f"(s), "f"(c), "f"(abe), "f"(h), "f"(q), "f"(qt), "r"(bit));
-  return mask;
 }
 
 // Packed fp32 (sm_100a FFMA2 / FMUL2): two points per instruction, a scalar centre
@@ -108,7 +94,15 @@ __device__ __forceinline__ f2 mul2(f2 a, f2 b) {
 __device__ __forceinline__ void up2(f2 v, float& lo, float& hi) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
 }
-// pass = (s >= c) && (|beta''| <= h) && (-q'' >= -Qt): one predicate chain + one OR
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ void up2u(f2 v, unsigned& lo, unsigned& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+}
+// CELLS (cylinder test): pass = (s >= c) && (|beta''| <= h) && (-q'' >= -Qt)
 __device__ __forceinline__ unsigned pair_bit_n(unsigned mask, float s, float c, float abe, float h,
                                                float qn, float nqt, unsigned bit) {
   asm("{\n\t.reg .pred p;\n\t"
@@ -120,8 +114,7 @@ __device__ __forceinline__ unsigned pair_bit_n(unsigned mask, float s, float c, 
       : "f"(s), "f"(c), "f"(abe), "f"(h), "f"(qn), "f"(nqt), "r"(bit));
   return mask;
 }
-
-// Region-only test (support decided later): (|beta''| <= h) && (-q'' >= -Qt)
+// CELLS, support decided later: (|beta''| <= h) && (-q'' >= -Qt)
 __device__ __forceinline__ unsigned pair_bit_r(unsigned mask, float abe, float h, float qn,
                                                float nqt, unsigned bit) {
   asm("{\n\t.reg .pred p;\n\t"
@@ -131,6 +124,29 @@ __device__ __forceinline__ unsigned pair_bit_r(unsigned mask, float abe, float h
       : "+r"(mask)
       : "f"(abe), "f"(h), "f"(qn), "f"(nqt), "r"(bit));
   return mask;
+}
+// BRUTE, support and sphere: pass = (s >= c) && (m >= 0), one predicate chain + one OR
+__device__ __forceinline__ unsigned pair_bit_sm(unsigned mask, float s, float c, float m,
+                                                unsigned bit) {
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.ge.f32 p, %1, %2;\n\t"
+      "setp.ge.and.f32 p, %3, 0f00000000, p;\n\t"
+      "@p or.b32 %0, %0, %4;\n\t}"
+      : "+r"(mask)
+      : "f"(s), "f"(c), "f"(m), "r"(bit));
+  return mask;
+}
+// sphere only: the sign bytes of the four margins m0..m3 of one centre (sign-replicating
+// PRMT: 0xff where negative), ANDed with the centre's bit in every byte, ORed into the
+// mask as "rejected" bits (three PRMT + one LOP3 for four pairs; callers invert)
+__device__ __forceinline__ unsigned reject_bits4(unsigned rej, unsigned m0, unsigned m1,
+                                                 unsigned m2, unsigned m3, unsigned K) {
+  unsigned a, b, c, d;
+  asm("prmt.b32 %0, %1, %2, 0xfbfb;" : "=r"(a) : "r"(m0), "r"(m1));
+  asm("prmt.b32 %0, %1, %2, 0xfbfb;" : "=r"(b) : "r"(m2), "r"(m3));
+  asm("prmt.b32 %0, %1, %2, 0x7610;" : "=r"(c) : "r"(a), "r"(b));
+  asm("lop3.b32 %0, %1, %2, %3, 0xea;" : "=r"(d) : "r"(c), "r"(K), "r"(rej));
+  return d;
 }
 
 // ------------------------------------------------------------------ smem layout
@@ -168,7 +184,7 @@ __host__ __device__ inline Layout make_layout(int G, int W, int mode, int prune)
 
 // ------------------------------------------------------------------ counters
 struct Ctr {
-  unsigned cand, acc, f64, exact;
+  unsigned cand, acc, f64, exact, srej;   // srej: candidates the support test rejected
 };
 
 // BILINEAR accumulator: 2^-23 fixed point.  The 32-bit low words live in shared
@@ -211,6 +227,7 @@ static __device__ __noinline__ SlowOut slow_pair(float4 P4, float4 N4, float4 X4
 //   2: some decision is not certified in fp32 -> slow_pair (fp64, then exact).
 struct Dec {
   int status;
+  int sup_out;  // certainly rejected by the support test
   int bin;      // NEAREST: k*W + l; BILINEAR: i0*W + j0
   float a, c;   // BILINEAR fractional offsets along k and l
 };
@@ -236,6 +253,7 @@ __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const f
   Dec r;
   r.a = 0.f;
   r.c = 0.f;
+  r.sup_out = sup_out;
   if (MODE == 0) {
     // the self pair (d == 0): beta = q = 0 exactly, k = ceil(W/2) (or floor), l = 0 (#8)
     const bool self = (fabsf(d0) + fabsf(d1) + fabsf(d2) == 0.f) & (p.self_fast != 0);
@@ -314,7 +332,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   __shared__ int s_chunk;
   __shared__ int s_total, s_live;
   __shared__ int s_rng[6];
-  __shared__ unsigned long long s_ctr[5];
+  __shared__ unsigned long long s_ctr[6];
 
   const int W = p.W;
   const int WW = W * W;
@@ -342,9 +360,18 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   uint32_t* gHi = p.hi_scratch + (size_t)blockIdx.x * G * hiWords;   // zero outside groups
   if (tid == 0) s_carry = 0;
 
-  if (tid < 5) s_ctr[tid] = 0ull;
+  if (tid < 6) s_ctr[tid] = 0ull;
   const unsigned long long t0 = gtimer();
-  Ctr ct{0, 0, 0, 0};
+  Ctr ct{0, 0, 0, 0, 0};
+  // SUP = 2 (BRUTE, adaptive support placement, per warp): a warp starts with the support
+  // test in the accept path and moves it into its hot loop when, in one tile, the
+  // candidates the test rejects exceed 1/SUP_RATIO of the tile's pairs; it re-probes
+  // after SUP_PROBE tiles.  Images are identical either way.
+  constexpr unsigned SUP_RATIO = 64;
+  constexpr int SUP_PROBE = 16;
+  bool sup_on = false;
+  int sup_count = 0;
+  unsigned sup_tiles = 0;
   int units_done = 0;
   unsigned long long visited = 0;
   bool first = true;
@@ -366,7 +393,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       // ---- a7: group setup (tempSpinImage, init, P = OP[i])
       if (tid < G) {
         const int slot = tid;
-        float4 A4 = make_float4(0.f, 0.f, 0.f, 0.f), B4 = make_float4(0.f, 0.f, 0.f, INFINITY);
+        float4 A4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 B4 = make_float4(0.f, 0.f, 0.f, PRUNE == 0 ? -INFINITY : INFINITY);
         float4 P4 = make_float4(0.f, 0.f, 0.f, 0.f), N4 = make_float4(0.f, 0.f, 0.f, 0.f);
         int mm = -1;
         if (slot < gcount) {
@@ -376,16 +404,30 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           if (c >= 0 && c < p.N) {
             P4 = __ldg(&p.cpos[c]);
             N4 = __ldg(&p.cnrm[c]);
-            const double px = P4.x, py = P4.y, pz = P4.z, nx = N4.x, ny = N4.y, nz = N4.z;
-            const double np = nx * px + ny * py + nz * pz;
             const double mid = p.mid;
-            const double C = (px * px + py * py + pz * pz) + 2.0 * mid * np + mid * mid;
-            const double Qt = p.Qmax - C + p.Eq_hot + 1e-12 * (fabs(C) + p.Qmax);
-            A4 = make_float4(N4.x, N4.y, N4.z, __double2float_rn(-np - mid));
-            // negated t-chain: -t = 2(p + mid n).x - |x|^2, tested as -q'' >= -Qt
-            B4 = make_float4(__double2float_rn(2.0 * (px + mid * nx)),
-                             __double2float_rn(2.0 * (py + mid * ny)),
-                             __double2float_rn(2.0 * (pz + mid * nz)), __double2float_rd(-Qt));
+            if (PRUNE == 0) {
+              // BRUTE: sphere of radius rho about c~ = B/2, B = fl(2(p + mid n)) (DESIGN.md
+              // 7.1): K = rho^2 - |c~|^2 + 2E rounded up, so the fp32 margin
+              // B.x - |x|^2 + K is positive for every pair of the region
+              const float Bx = __double2float_rn(2.0 * ((double)P4.x + mid * N4.x));
+              const float By = __double2float_rn(2.0 * ((double)P4.y + mid * N4.y));
+              const float Bz = __double2float_rn(2.0 * ((double)P4.z + mid * N4.z));
+              const double cx = 0.5 * Bx, cy = 0.5 * By, cz = 0.5 * Bz;
+              const double K = p.rho2 - (cx * cx + cy * cy + cz * cz) + 2.0 * p.E_sph;
+              A4 = make_float4(N4.x, N4.y, N4.z, 0.f);
+              B4 = make_float4(Bx, By, Bz, __double2float_ru(K));
+            } else {
+              // CELLS: the region cylinder itself, beta'' = n.x - n.p - mid and
+              // -q'' = beta''^2 + 2(p + mid n).x - |x|^2 - C >= -Qt
+              const double px = P4.x, py = P4.y, pz = P4.z, nx = N4.x, ny = N4.y, nz = N4.z;
+              const double np = nx * px + ny * py + nz * pz;
+              const double C = (px * px + py * py + pz * pz) + 2.0 * mid * np + mid * mid;
+              const double Qt = p.Qmax - C + p.Eq_hot + 1e-12 * (fabs(C) + p.Qmax);
+              A4 = make_float4(N4.x, N4.y, N4.z, __double2float_rn(-np - mid));
+              B4 = make_float4(__double2float_rn(2.0 * (px + mid * nx)),
+                               __double2float_rn(2.0 * (py + mid * ny)),
+                               __double2float_rn(2.0 * (pz + mid * nz)), __double2float_rd(-Qt));
+            }
             mm = m;
           } else {
             atomicOr(&p.err_flags[0], 1);
@@ -442,7 +484,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
 
       // ---- a8-a10: stream points, pair test, compact, accept
       // Each thread holds KP points in registers for all G centres.  Per batch of CB
-      // centres the pass bits go to one u32 mask (bit = c*KP + k) stored in smem; once
+      // centres the pass bits go to one u32 mask (bit = k*8 + c) stored in smem; once
       // per tile the warp compacts all its bits into a ring of 16-bit entries
       // (centre slot << 7 | lane << 2 | k) and processes them 32 at a time, reading the
       // point from the warp's staged copy of the tile (no global re-load).
@@ -477,6 +519,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         }
         if (!v0) d0.status = 0;
         ct.cand += (unsigned)v0 + (APL == 2 ? (unsigned)v1 : 0u);
+        if (SUP == 2) ct.srej += (unsigned)(v0 & (d0.sup_out != 0));
         if (d0.status == 2) resolve<MODE>(p, d0, P0, N0, X0, NX0, ct);
         if (APL == 2 && d1.status == 2) resolve<MODE>(p, d1, P1, N1, X1, NX1, ct);
         const int g0 = (int)(e0 >> 7), g1 = (int)(e1 >> 7);
@@ -499,7 +542,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         const int total = __shfl_sync(0xffffffffu, x, 31);
         if (total == 0) return;
         // common case: the whole tile fits the ring and one scan places every entry;
-        // dense tiles go a quarter mask word (2 centres, <= 256 entries) at a time, each
+        // dense tiles go a quarter mask word (one point, <= 8 centres, <= 256 entries) at a time, each
         // appended after the ring was drained to < 64 pending entries (QCAP >= 512).
         static_assert(QCAP >= 64 + 256, "ring too small for the dense path");
         const bool dense = total > QCAP - 64;
@@ -515,7 +558,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
                   const int bit = __ffs(m) - 1;
                   m &= m - 1u;
                   sQ[pos & (QCAP - 1)] =
-                      (uint16_t)(((w * CB + (bit >> LOGKP)) << 7) | (lane << LOGKP) | (bit & (KP - 1)));
+                      (uint16_t)(((w * CB + (bit & 7)) << 7) | (lane << LOGKP) | (bit >> 3));
                   ++pos;
                 }
               }
@@ -532,12 +575,12 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
               }
               const int t2 = __shfl_sync(0xffffffffu, x2, 31);
               unsigned pos = qtail + (unsigned)(x2 - c2);
-              const int cbase = (ci >> 2) * CB + (8 / KP) * quarter;
+              const int cbase = (ci >> 2) * CB;   // quarter = point k, bits = centres
               while (m) {
                 const int bit = __ffs(m) - 1;
                 m &= m - 1u;
                 sQ[pos & (QCAP - 1)] =
-                    (uint16_t)(((cbase + (bit >> LOGKP)) << 7) | (lane << LOGKP) | (bit & (KP - 1)));
+                    (uint16_t)(((cbase + bit) << 7) | (lane << LOGKP) | quarter);
                 ++pos;
               }
               qtail += (unsigned)t2;
@@ -588,6 +631,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           NX2[pr] = r[4]; NY2[pr] = r[5]; NZ2[pr] = r[6];
         }
         const float c_test = p.c_test, h_test = p.h_test;
+        const bool sup_hot = SUP == 1 || (SUP == 2 && sup_on);
 #pragma unroll 1
         for (int cb = 0; cb < G; cb += CB) {
           unsigned mask = 0u;
@@ -595,30 +639,67 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             sMask[(cb / CB) * 32 + lane] = 0u;
             continue;
           }
+          // mask bit (k << 3) | c: point k of this lane, centre cb + c
+          if (PRUNE == 0 && !sup_hot) {
 #pragma unroll
-          for (int c = 0; c < CB; ++c) {
-            const float4 A4 = sA[cb + c];
-            const float4 B4 = sB[cb + c];
+            for (int c = 0; c < CB; ++c) {
+              const float4 B4 = sB[cb + c];
+              unsigned mb[KP];
 #pragma unroll
-            for (int k2 = 0; k2 < KP / 2; ++k2) {
-              // support n.nx; beta'' = n.x - n.p - mid;
-              // -q'' = beta''^2 + 2(p + mid n).x - |x|^2 = C - q
-              f2 s2 = 0ull;
-              if (SUP) s2 = fma2(bc2(A4.x), NX2[k2], fma2(bc2(A4.y), NY2[k2], mul2(bc2(A4.z), NZ2[k2])));
-              const f2 be2 = fma2(bc2(A4.x), X2[k2], fma2(bc2(A4.y), Y2[k2], fma2(bc2(A4.z), Z2[k2], bc2(A4.w))));
-              const f2 tn2 = fma2(bc2(B4.x), X2[k2], fma2(bc2(B4.y), Y2[k2], fma2(bc2(B4.z), Z2[k2], NXX2[k2])));
-              const f2 qn2 = fma2(be2, be2, tn2);
-              float s0, s1, b0, b1, q0, q1;
-              up2(s2, s0, s1);
-              up2(be2, b0, b1);
-              up2(qn2, q0, q1);
-              const int bit = c * KP + 2 * k2;
-              if (SUP) {
-                mask = pair_bit_n(mask, s0, c_test, fabsf(b0), h_test, q0, B4.w, 1u << bit);
-                mask = pair_bit_n(mask, s1, c_test, fabsf(b1), h_test, q1, B4.w, 1u << (bit + 1));
-              } else {
-                mask = pair_bit_r(mask, fabsf(b0), h_test, q0, B4.w, 1u << bit);
-                mask = pair_bit_r(mask, fabsf(b1), h_test, q1, B4.w, 1u << (bit + 1));
+              for (int k2 = 0; k2 < KP / 2; ++k2) {
+                // sphere margin m = 2c~.x - |x|^2 + K >= 0 for every pair of the region
+                // (bounded)
+                const f2 m2 = add2(fma2(bc2(B4.x), X2[k2], fma2(bc2(B4.y), Y2[k2],
+                                   fma2(bc2(B4.z), Z2[k2], bc2(B4.w)))), NXX2[k2]);
+                up2u(m2, mb[2 * k2], mb[2 * k2 + 1]);
+              }
+              mask = reject_bits4(mask, mb[0], mb[1], mb[2], mb[3], 0x01010101u << c);
+            }
+            mask = ~mask & (0x01010101u * ((1u << CB) - 1u));
+          } else if (PRUNE == 0) {
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+              const float4 A4 = sA[cb + c];
+              const float4 B4 = sB[cb + c];
+#pragma unroll
+              for (int k2 = 0; k2 < KP / 2; ++k2) {
+                // support n.nx >= c and the sphere margin
+                const f2 s2 = fma2(bc2(A4.x), NX2[k2], fma2(bc2(A4.y), NY2[k2], mul2(bc2(A4.z), NZ2[k2])));
+                const f2 m2 = add2(fma2(bc2(B4.x), X2[k2], fma2(bc2(B4.y), Y2[k2],
+                                   fma2(bc2(B4.z), Z2[k2], bc2(B4.w)))), NXX2[k2]);
+                float s0, s1, q0, q1;
+                up2(s2, s0, s1);
+                up2(m2, q0, q1);
+                mask = pair_bit_sm(mask, s0, c_test, q0, 1u << ((2 * k2) * 8 + c));
+                mask = pair_bit_sm(mask, s1, c_test, q1, 1u << ((2 * k2 + 1) * 8 + c));
+              }
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+              const float4 A4 = sA[cb + c];
+              const float4 B4 = sB[cb + c];
+#pragma unroll
+              for (int k2 = 0; k2 < KP / 2; ++k2) {
+                // support n.nx; beta'' = n.x - n.p - mid;
+                // -q'' = beta''^2 + 2(p + mid n).x - |x|^2 = C - q
+                f2 s2 = 0ull;
+                if (SUP) s2 = fma2(bc2(A4.x), NX2[k2], fma2(bc2(A4.y), NY2[k2], mul2(bc2(A4.z), NZ2[k2])));
+                const f2 be2 = fma2(bc2(A4.x), X2[k2], fma2(bc2(A4.y), Y2[k2], fma2(bc2(A4.z), Z2[k2], bc2(A4.w))));
+                const f2 tn2 = fma2(bc2(B4.x), X2[k2], fma2(bc2(B4.y), Y2[k2], fma2(bc2(B4.z), Z2[k2], NXX2[k2])));
+                const f2 qn2 = fma2(be2, be2, tn2);
+                float s0, s1, b0, b1, q0, q1;
+                up2(s2, s0, s1);
+                up2(be2, b0, b1);
+                up2(qn2, q0, q1);
+                const unsigned bit0 = 1u << ((2 * k2) * 8 + c), bit1 = 1u << ((2 * k2 + 1) * 8 + c);
+                if (SUP) {
+                  mask = pair_bit_n(mask, s0, c_test, fabsf(b0), h_test, q0, B4.w, bit0);
+                  mask = pair_bit_n(mask, s1, c_test, fabsf(b1), h_test, q1, B4.w, bit1);
+                } else {
+                  mask = pair_bit_r(mask, fabsf(b0), h_test, q0, B4.w, bit0);
+                  mask = pair_bit_r(mask, fabsf(b1), h_test, q1, B4.w, bit1);
+                }
               }
             }
           }
@@ -626,6 +707,19 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         }
         __syncwarp();
         if (p.debug_skip < 2) compact_and_accept();
+        if (SUP == 2) {
+          if (!sup_on) {
+            const unsigned r = __reduce_add_sync(0xffffffffu, ct.srej);
+            if (r * SUP_RATIO > (unsigned)(32 * KP * gcount)) {
+              sup_on = true;
+              sup_count = SUP_PROBE;
+            }
+          } else {
+            ++sup_tiles;
+            if (--sup_count == 0) sup_on = false;
+          }
+          ct.srej = 0u;
+        }
         __syncwarp();
       };
 
@@ -764,6 +858,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   atomicAdd(&s_ctr[2], (unsigned long long)ct.f64);
   atomicAdd(&s_ctr[3], (unsigned long long)ct.exact);
   if (tid == 0) atomicAdd(&s_ctr[4], visited);
+  if (lane == 0 && sup_tiles) atomicAdd(&s_ctr[5], (unsigned long long)sup_tiles);
   __syncthreads();
   if (tid == 0) {
     atomicAdd(&p.stats[ST_CAND], s_ctr[0]);
@@ -771,6 +866,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
     atomicAdd(&p.stats[ST_F64], s_ctr[2]);
     atomicAdd(&p.stats[ST_EXACT], s_ctr[3]);
     atomicAdd(&p.stats[ST_VISITED], s_ctr[4]);
+    if (s_ctr[5]) atomicAdd(&p.stats[ST_SUPHOT], s_ctr[5]);
     p.cta_t0[blockIdx.x] = t0;
     p.cta_t1[blockIdx.x] = t1;
     p.cta_units[blockIdx.x] = units_done;

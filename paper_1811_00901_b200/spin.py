@@ -22,6 +22,7 @@ STATIC, SS, GSS, FAC = 0, 1, 2, 3
 NEAREST, BILINEAR = 0, 1
 BRUTE, CELLS = 0, 1
 F_LITERAL_HALF_WIDTH, F_FLOOR_BINS, F_NO_SORT, F_NO_FAST_CERT, F_SUPPORT_LAST = 0x1, 0x2, 0x4, 0x8, 0x10
+F_SUPPORT_FIRST = 0x20
 SCHEDULES = {"STATIC": STATIC, "SS": SS, "GSS": GSS, "FAC": FAC}
 MODES = {"nearest": NEAREST, "bilinear": BILINEAR}
 PRUNES = {"brute": BRUTE, "cells": CELLS}
@@ -41,7 +42,8 @@ class Stats(C.Structure):
                 ("exact_fallbacks", C.c_int64), ("P", C.c_int32), ("G", C.c_int32),
                 ("n_units", C.c_int32), ("n_chunks", C.c_int32),
                 ("h_cta_start_ns", C.POINTER(C.c_uint64)), ("h_cta_end_ns", C.POINTER(C.c_uint64)),
-                ("h_cta_units", C.POINTER(C.c_int32)), ("cta_capacity", C.c_int32)]
+                ("h_cta_units", C.POINTER(C.c_int32)), ("cta_capacity", C.c_int32),
+                ("tiles_support_hot", C.c_int64)]
 
 
 _vp = C.c_void_p

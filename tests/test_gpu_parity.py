@@ -174,6 +174,40 @@ def test_exact_ties_dyadic(spin, torch, flags):
             assert st_g["fp64_fallbacks"] > 0 and st_g["exact_fallbacks"] > 0
 
 
+def test_region_corners(spin, torch):
+    """Points on and 1-2 ulps around the corners and rims of the region cylinder (beta at
+    both window edges, alpha at its bound) about an off-origin centre with an oblique
+    normal: the pairs closest to the BRUTE hot loop's bounding sphere."""
+    rng = np.random.default_rng(11)
+    for W, b in ((16, 0.02), (5, 0.1), (32, 0.01)):
+        for mode in ("nearest", "bilinear"):
+            p0 = np.array([0.31, -0.22, 0.7])
+            n0 = rng.normal(size=3)
+            n0 /= np.linalg.norm(n0)
+            t1 = np.cross(n0, [0.3, 0.5, 0.8])
+            t1 /= np.linalg.norm(t1)
+            t2 = np.cross(n0, t1)
+            if mode == "nearest":
+                ulo, uhi, vmax = -1.0, W - 1.0, W - 1.0
+            else:
+                ulo, uhi, vmax = 0.0, W - 1.0, W - 1.0
+            xs = [p0]
+            for u in (ulo, uhi, 0.5 * (ulo + uhi)):
+                beta = (W / 2 - u) * b
+                for ang in np.linspace(0, 2 * np.pi, 7, endpoint=False):
+                    for a in (vmax * b, 0.5 * vmax * b):
+                        x = p0 + beta * n0 + a * (np.cos(ang) * t1 + np.sin(ang) * t2)
+                        x32 = x.astype(np.float32)
+                        for d in (-2, -1, 0, 1, 2):
+                            xs.append(x32 + d * np.spacing(x32) * np.sign(x32 - p0))
+            X = np.asarray(xs, np.float32)
+            Nn = np.tile(n0.astype(np.float32), (len(X), 1))
+            for c in (-math.inf, 0.5):
+                gpu = run_gpu(spin, torch, X, Nn, [0], W, b, c, mode)
+                ora, st = oracle(X, Nn, [0], W, b, c, mode)
+                check(gpu, ora, st, mode, f"corners W={W} {mode} c={c}")
+
+
 def test_near_threshold_ulps(spin, torch):
     """Points 1 fp32 ulp either side of every row / column edge."""
     W, b = 16, 0.02
@@ -403,6 +437,37 @@ def test_host_path_pipelined_d2h(spin, torch):
         assert_nearest_exact(h[pick] if False else eng.generate_host(cen, 16, 0.02, 0.5)[pick], ora, "piped host")
     finally:
         eng.close()
+
+
+@pytest.mark.gpu
+def test_support_placement_same_images(spin, torch):
+    """BRUTE support placement: adaptive (default), SPIN_F_SUPPORT_FIRST (every pair, P:166
+    order) and SPIN_F_SUPPORT_LAST give identical images.  Random normals make the support
+    test reject most sphere candidates, so the adaptive CTAs must move it into the hot loop
+    (tiles_support_hot > 0); a smooth surface keeps it in the accept path."""
+    P, Nn = clouds.clustered(20000, 23)
+    rng = np.random.default_rng(5)
+    Nr = rng.normal(size=Nn.shape)
+    Nr = (Nr / np.linalg.norm(Nr, axis=1, keepdims=True)).astype(np.float32)
+    cen = clouds.sample_centres(20000, 3000, 24)
+    for mode in ("nearest", "bilinear"):
+        a, sa = run_gpu(spin, torch, P, Nr, cen, 16, 0.01, 0.5, mode, stats=True)
+        b, sb = run_gpu(spin, torch, P, Nr, cen, 16, 0.01, 0.5, mode, stats=True, flags=spin.F_SUPPORT_FIRST)
+        a16 = run_gpu(spin, torch, P, Nr, cen, 16, 0.01, 0.5, mode, P=16)
+        np.testing.assert_array_equal(a, a16, err_msg=mode)
+        c = run_gpu(spin, torch, P, Nr, cen, 16, 0.01, 0.5, mode, flags=spin.F_SUPPORT_LAST)
+        np.testing.assert_array_equal(a, b, err_msg=mode)
+        np.testing.assert_array_equal(a, c, err_msg=mode)
+        assert sa["tiles_support_hot"] > 0, sa
+        assert sb["tiles_support_hot"] == 0          # the forced variant does not count
+        ora, st = oracle(P, Nr, cen[:40], 16, 0.01, 0.5, mode)
+        check(a[:40], ora, st, mode, f"adaptive support {mode}")
+    Ps, Ns = clouds.sphere(20000, 25)
+    cs = clouds.sample_centres(20000, 2000, 26)
+    a, sa = run_gpu(spin, torch, Ps, Ns, cs, 16, 0.01, 0.5, "nearest", stats=True)
+    b = run_gpu(spin, torch, Ps, Ns, cs, 16, 0.01, 0.5, "nearest", flags=spin.F_SUPPORT_FIRST)
+    np.testing.assert_array_equal(a, b)
+    assert sa["tiles_support_hot"] == 0, sa
 
 
 @pytest.mark.parametrize("prune", ["brute", "cells"])

@@ -1,0 +1,150 @@
+// Pair-test formulations of the hot loop in isolation: 8 centres x 4
+// points (two packed pairs) per thread per mask word, centre constants from shared memory.
+//   V0 cyl_setp   : support + beta window + alpha bound, one predicate chain per pair and
+//                   a predicated OR (the kernel as of round 1)
+//   V1 sph_lop    : support + bounding sphere of the cylinder, margins OR'ed by LOP3, sign
+//                   bytes gathered with PRMT (sign-replicate) and merged with one LOP3 per centre
+//   V2 sph_sat    : support folded into the sphere margin with a saturated FMA (one margin)
+//   V3 sphonly    : sphere only (support decided later)
+//   V4 cyl_nosup  : beta window + alpha bound predicate chain (support decided later)
+//   V5 sph_setp   : support + sphere, predicate chain
+#include <cstdio>
+#include <cuda_runtime.h>
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk2(float a, float b) { f2 r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b)); return r; }
+__device__ __forceinline__ f2 bc2(float a) { return pk2(a, a); }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) { f2 d; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c)); return d; }
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) { f2 d; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ f2 add2(f2 a, f2 b) { f2 d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ void up2(f2 v, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
+__device__ __forceinline__ void up2u(f2 v, unsigned& lo, unsigned& hi) { asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v)); }
+__device__ __forceinline__ unsigned pbit3(unsigned mask, float s, float c, float abe, float h, float qn, float nqt, unsigned bit) {
+  asm("{\n\t.reg .pred p;\n\tsetp.ge.f32 p, %1, %2;\n\tsetp.le.and.f32 p, %3, %4, p;\n\tsetp.ge.and.f32 p, %5, %6, p;\n\t@p or.b32 %0, %0, %7;\n\t}"
+      : "+r"(mask) : "f"(s), "f"(c), "f"(abe), "f"(h), "f"(qn), "f"(nqt), "r"(bit));
+  return mask;
+}
+__device__ __forceinline__ unsigned pbit2(unsigned mask, float a, float ta, float b, float tb, unsigned bit) {
+  asm("{\n\t.reg .pred p;\n\tsetp.ge.f32 p, %1, %2;\n\tsetp.ge.and.f32 p, %3, %4, p;\n\t@p or.b32 %0, %0, %5;\n\t}"
+      : "+r"(mask) : "f"(a), "f"(ta), "f"(b), "f"(tb), "r"(bit));
+  return mask;
+}
+__device__ __forceinline__ unsigned lop_or(unsigned a, unsigned b) { unsigned d; asm("lop3.b32 %0, %1, %2, 0, 0xfc;" : "=r"(d) : "r"(a), "r"(b)); return d; }
+// sign bytes of v0..v3 (0xff where negative) into bytes 0..3, AND with K, OR into mask
+__device__ __forceinline__ unsigned gather4(unsigned mask, unsigned v0, unsigned v1, unsigned v2, unsigned v3, unsigned K) {
+  unsigned a, b, c, d;
+  asm("prmt.b32 %0, %1, %2, 0xfbfb;" : "=r"(a) : "r"(v0), "r"(v1));
+  asm("prmt.b32 %0, %1, %2, 0xfbfb;" : "=r"(b) : "r"(v2), "r"(v3));
+  asm("prmt.b32 %0, %1, %2, 0x7610;" : "=r"(c) : "r"(a), "r"(b));
+  asm("lop3.b32 %0, %1, %2, %3, 0xea;" : "=r"(d) : "r"(c), "r"(K), "r"(mask));
+  return d;
+}
+
+template <int V, int NTH>
+__global__ void __launch_bounds__(NTH, 1) k(unsigned* out, float ct, float ht, int iters) {
+  constexpr int NP = 2;
+  __shared__ float4 sA[64], sB[64];
+  __shared__ float4 sT[8 * 32];
+  for (int i = threadIdx.x; i < 8 * 32; i += NTH) sT[i] = make_float4(i * 1e-5f, 0.1f, -0.2f + i * 1e-6f, 0.3f);
+  if (threadIdx.x < 64) {
+    sA[threadIdx.x] = make_float4(0.3f + threadIdx.x * 1e-3f, 0.4f, 0.5f, -0.1f);
+    sB[threadIdx.x] = make_float4(0.2f, 0.1f, 0.3f + threadIdx.x * 1e-3f, -0.05f);
+  }
+  __syncthreads();
+  unsigned acc = 0;
+  for (int it = 0; it < iters; ++it) {
+    f2 X[NP], Y[NP], Z[NP], NXX[NP], NX[NP], NY[NP], NZ[NP];
+#pragma unroll
+    for (int pr = 0; pr < NP; ++pr) {
+      f2 r[8];
+      const float4* base = sT + (pr * 4) * 32 + (threadIdx.x & 31);
+      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r[0]), "=l"(r[1]) : "r"((unsigned)__cvta_generic_to_shared(base)));
+      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r[2]), "=l"(r[3]) : "r"((unsigned)__cvta_generic_to_shared(base + 32)));
+      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r[4]), "=l"(r[5]) : "r"((unsigned)__cvta_generic_to_shared(base + 64)));
+      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r[6]), "=l"(r[7]) : "r"((unsigned)__cvta_generic_to_shared(base + 96)));
+      X[pr] = r[0]; Y[pr] = r[1]; Z[pr] = r[2]; NXX[pr] = r[3]; NX[pr] = r[4]; NY[pr] = r[5]; NZ[pr] = r[6];
+    }
+#pragma unroll 1
+    for (int cb = 0; cb < 64; cb += 8) {
+      unsigned mask = 0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 A4 = sA[cb + c], B4 = sB[cb + c];
+        unsigned v[4];
+#pragma unroll
+        for (int k2 = 0; k2 < NP; ++k2) {
+          const int bit = c * 4 + 2 * k2;
+          if (V == 0 || V == 4) {
+            f2 s2 = 0ull;
+            if (V == 0) s2 = fma2(bc2(A4.x), NX[k2], fma2(bc2(A4.y), NY[k2], mul2(bc2(A4.z), NZ[k2])));
+            const f2 be2 = fma2(bc2(A4.x), X[k2], fma2(bc2(A4.y), Y[k2], fma2(bc2(A4.z), Z[k2], bc2(A4.w))));
+            const f2 tn2 = fma2(bc2(B4.x), X[k2], fma2(bc2(B4.y), Y[k2], fma2(bc2(B4.z), Z[k2], NXX[k2])));
+            const f2 qn2 = fma2(be2, be2, tn2);
+            float s0, s1, b0, b1, q0, q1;
+            up2(s2, s0, s1); up2(be2, b0, b1); up2(qn2, q0, q1);
+            if (V == 0) {
+              mask = pbit3(mask, s0, ct, fabsf(b0), ht, q0, B4.w, 1u << bit);
+              mask = pbit3(mask, s1, ct, fabsf(b1), ht, q1, B4.w, 1u << (bit + 1));
+            } else {
+              mask = pbit2(mask, -fabsf(b0), -ht, q0, B4.w, 1u << bit);
+              mask = pbit2(mask, -fabsf(b1), -ht, q1, B4.w, 1u << (bit + 1));
+            }
+          } else {
+            // sphere margin 2c'.x - |x|^2 + K  (K per centre, innermost)
+            const f2 sp2 = add2(fma2(bc2(B4.x), X[k2], fma2(bc2(B4.y), Y[k2], fma2(bc2(B4.z), Z[k2], bc2(B4.w)))), NXX[k2]);
+            if (V == 3) {
+              up2u(sp2, v[2 * k2], v[2 * k2 + 1]);
+            } else if (V == 2) {
+              // sigma = sat(BIG*(n.nx - c) + 1): 1 when supported, 0 when certainly not
+              const f2 sp = fma2(bc2(A4.y), NY[k2], fma2(bc2(A4.z), NZ[k2], bc2(A4.w)));
+              float nx0, nx1, r0, r1;
+              up2(NX[k2], nx0, nx1); up2(sp, r0, r1);
+              const f2 sg = pk2(__saturatef(fmaf(A4.x, nx0, r0)), __saturatef(fmaf(A4.x, nx1, r1)));
+              const f2 cm = fma2(sg, sp2, bc2(-ht));
+              up2u(cm, v[2 * k2], v[2 * k2 + 1]);
+            } else {
+              const f2 s2 = fma2(bc2(A4.x), NX[k2], fma2(bc2(A4.y), NY[k2], fma2(bc2(A4.z), NZ[k2], bc2(A4.w))));
+              if (V == 1) {
+                unsigned a0, a1, b0, b1;
+                up2u(s2, a0, a1); up2u(sp2, b0, b1);
+                v[2 * k2] = lop_or(a0, b0); v[2 * k2 + 1] = lop_or(a1, b1);
+              } else {
+                float s0, s1, q0, q1;
+                up2(s2, s0, s1); up2(sp2, q0, q1);
+                mask = pbit2(mask, s0, 0.f, q0, 0.f, 1u << bit);
+                mask = pbit2(mask, s1, 0.f, q1, 0.f, 1u << (bit + 1));
+              }
+            }
+          }
+        }
+        if (V == 1 || V == 2 || V == 3) mask = gather4(mask, v[0], v[1], v[2], v[3], 0x01010101u << c);
+      }
+      acc += mask;
+    }
+  }
+  if (acc == 0x12345u) out[0] = acc;
+}
+
+int main() {
+  unsigned* d; cudaMalloc(&d, 64);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  auto run = [&](auto kern, int nth, const char* name) {
+    const int iters = 2000, blocks = 148;
+    kern<<<blocks, nth>>>(d, 0.5f, 0.2f, 10);
+    cudaEventRecord(e0);
+    kern<<<blocks, nth>>>(d, 0.5f, 0.2f, iters);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    double pairs = (double)iters * 64 * 4 * nth * blocks;
+    printf("{\"variant\":\"%s\",\"threads\":%d,\"pairs_per_s\":%.3e,\"fp32_frac_20flop\":%.3f}\n", name, nth,
+           pairs / (ms * 1e-3), pairs * 20 / (ms * 1e-3) / 74.45e12);
+  };
+  for (int r = 0; r < 2; ++r) {
+    run(k<0, 768>, 768, "V0_cyl_setp");
+    run(k<1, 768>, 768, "V1_sph_lop");
+    run(k<2, 768>, 768, "V2_sph_sat");
+    run(k<3, 768>, 768, "V3_sphonly");
+    run(k<4, 768>, 768, "V4_cyl_nosup");
+    run(k<5, 768>, 768, "V5_sph_setp");
+  }
+  return 0;
+}
