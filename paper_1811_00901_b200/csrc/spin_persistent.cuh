@@ -192,16 +192,14 @@ struct Ctr {
 // words (two bins per u32) in a per-CTA global scratch that is zero between groups,
 // and raise a shared flag so that only groups with carries read or clear it.
 // round(w * 2^23) for w in [0,1] is the mantissa of 1 + w.
-__device__ __forceinline__ void add_fixed(uint32_t* lo, uint32_t* hi, int bin, float w,
-                                          int32_t* err, int* carry_flag) {
-  const uint32_t v = __float_as_uint(w + 1.0f) - 0x3f800000u;
-  const uint32_t old = atomicAdd(&lo[bin], v);
-  if (old + v < old) {
-    const uint32_t sh = (uint32_t)(bin & 1) * 16u;
-    const uint32_t prev = atomicAdd(&hi[bin >> 1], 1u << sh);
-    if (((prev >> sh) & 0xffffu) == 0xffffu) atomicOr(&err[1], 1);
-    *carry_flag = 1;
-  }
+__device__ __forceinline__ uint32_t fixed23(float w) {
+  return __float_as_uint(w + 1.0f) - 0x3f800000u;
+}
+static __device__ __noinline__ void carry_fixed(uint32_t* hi, int bin, int32_t* err, int* carry_flag) {
+  const uint32_t sh = (uint32_t)(bin & 1) * 16u;
+  const uint32_t prev = atomicAdd(&hi[bin >> 1], 1u << sh);
+  if (((prev >> sh) & 0xffffu) == 0xffffu) atomicOr(&err[1], 1);
+  *carry_flag = 1;
 }
 
 // ------------------------------------------------------------------ accept path
@@ -285,7 +283,11 @@ __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const f
     const bool wu = !(fabsf(wval - lim) > p.Ew_a);
     const bool out = (!uu & !((uval > 0.f) & (uval < Wm1))) | (!wu & !(wval < lim));
     r.status = (sup_out | (!unc0 & out)) ? 0 : ((unc0 | uu | wu) ? 2 : 1);
-    const float v = sqrtf(fmaxf(wval, 0.0f));
+    // v only places the splat (continuous in v across bin edges), so the approximate
+    // square root (MUFU, ~2 ulp) is within the BILINEAR tolerance; the region edge was
+    // decided on w above
+    float v;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(v) : "f"(fmaxf(wval, 0.0f)));
     const float fi = fminf(fmaxf(rint_magic(uval - 0.5f), 0.0f), Wm1 - 1.0f);
     const float fj = fminf(fmaxf(rint_magic(v - 0.5f), 0.0f), Wm1 - 1.0f);
     r.a = fminf(fmaxf(uval - fi, 0.0f), 1.0f);
@@ -315,10 +317,20 @@ __device__ __forceinline__ void apply(const KParams& p, const Dec& d, uint32_t* 
     atomicAdd(&img[d.bin], 1u);
   } else {
     const int W = p.W;
-    add_fixed(img, hi, d.bin, (1.0f - d.a) * (1.0f - d.c), p.err_flags, carry_flag);
-    add_fixed(img, hi, d.bin + W, d.a * (1.0f - d.c), p.err_flags, carry_flag);
-    add_fixed(img, hi, d.bin + 1, (1.0f - d.a) * d.c, p.err_flags, carry_flag);
-    add_fixed(img, hi, d.bin + W + 1, d.a * d.c, p.err_flags, carry_flag);
+    // four u32 adds; a wrapped low word (at most one per 512 units of weight in a bin) is
+    // carried into its 16-bit high word on one shared, rarely taken branch
+    const int b0 = d.bin, b1 = d.bin + W, b2 = d.bin + 1, b3 = d.bin + W + 1;
+    const uint32_t v0 = fixed23((1.0f - d.a) * (1.0f - d.c)), v1 = fixed23(d.a * (1.0f - d.c));
+    const uint32_t v2 = fixed23((1.0f - d.a) * d.c), v3 = fixed23(d.a * d.c);
+    const uint32_t o0 = atomicAdd(&img[b0], v0), o1 = atomicAdd(&img[b1], v1);
+    const uint32_t o2 = atomicAdd(&img[b2], v2), o3 = atomicAdd(&img[b3], v3);
+    const bool c0 = o0 + v0 < o0, c1 = o1 + v1 < o1, c2 = o2 + v2 < o2, c3 = o3 + v3 < o3;
+    if (c0 | c1 | c2 | c3) {
+      if (c0) carry_fixed(hi, b0, p.err_flags, carry_flag);
+      if (c1) carry_fixed(hi, b1, p.err_flags, carry_flag);
+      if (c2) carry_fixed(hi, b2, p.err_flags, carry_flag);
+      if (c3) carry_fixed(hi, b3, p.err_flags, carry_flag);
+    }
   }
 }
 
