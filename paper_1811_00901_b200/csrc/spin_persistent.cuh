@@ -35,6 +35,9 @@
 #ifndef SPIN_KP
 #define SPIN_KP 4
 #endif
+#ifndef SPIN_APL_BRUTE
+#define SPIN_APL_BRUTE 1      // BRUTE candidates per lane per accept pass
+#endif
 #include "spin_exact.cuh"
 
 namespace spin {
@@ -56,6 +59,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+__device__ __forceinline__ unsigned msb(unsigned m) {   // m != 0
+  unsigned b;
+  asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(m));
+  return b;
 }
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -503,12 +511,12 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       unsigned qhead = 0, qtail = 0;
       constexpr int NWD = G / CB;                      // mask words per lane per tile
       // candidate operands: centre slot gs, point (source lane, k) from the staged tile
+      // entry = (mask word w << 10) | (source lane << 5) | mask bit (k << 3 | c)
       auto load_entry = [&](unsigned e, float4& P4, float4& N4, float4& X4, float4& NX4) {
-        const int gs = (int)(e >> 7);
-        const int src = (int)(e & 127u);
+        const int gs = (int)(e >> 10) * CB + (int)(e & 7u);
         P4 = sP[gs];
         N4 = sN[gs];
-        const int sl = src >> LOGKP, kk = src & (KP - 1);           // source lane, point k
+        const int sl = (int)(e >> 5) & 31, kk = (int)(e >> 3) & 3;   // source lane, point k
         const float* rec = reinterpret_cast<const float*>(sT + (kk >> 1) * 32 + sl) + (kk & 1);
         constexpr int RS = (KP / 2) * 32 * 4;                       // floats between records
         X4 = make_float4(rec[0], rec[2], rec[RS], 0.f);
@@ -516,7 +524,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       };
       // CELLS (dense, latency-bound) takes two candidates per lane per pass so that the
       // two independent decisions interleave; BRUTE keeps one (fewer live registers).
-      constexpr int APL = PRUNE == 1 ? 2 : 1;
+      constexpr int APL = PRUNE == 1 ? 2 : SPIN_APL_BRUTE;
       auto process_pair = [&](unsigned e0, bool v0, unsigned e1, bool v1) {
         if (p.debug_skip) return;
         float4 P0, N0, X0, NX0, P1, N1, X1, NX1;
@@ -534,7 +542,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         if (SUP == 2) ct.srej += (unsigned)(v0 & (d0.sup_out != 0));
         if (d0.status == 2) resolve<MODE>(p, d0, P0, N0, X0, NX0, ct);
         if (APL == 2 && d1.status == 2) resolve<MODE>(p, d1, P1, N1, X1, NX1, ct);
-        const int g0 = (int)(e0 >> 7), g1 = (int)(e1 >> 7);
+        const int g0 = (int)(e0 >> 10) * CB + (int)(e0 & 7u), g1 = (int)(e1 >> 10) * CB + (int)(e1 & 7u);
         if (d0.status) { ++ct.acc; apply<MODE>(p, d0, sImg + g0 * WW, gHi + g0 * hiWords, &s_carry); }
         if (APL == 2 && d1.status) {
           ++ct.acc;
@@ -553,6 +561,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         }
         const int total = __shfl_sync(0xffffffffu, x, 31);
         if (total == 0) return;
+        qhead = qtail = 0u;   // the ring is empty between tiles
         // common case: the whole tile fits the ring and one scan places every entry;
         // dense tiles go a quarter mask word (one point, <= 8 centres, <= 256 entries) at a time, each
         // appended after the ring was drained to < 64 pending entries (QCAP >= 512).
@@ -562,19 +571,19 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         for (int ci = 0;;) {
           if (ci < nchunks) {
             if (!dense) {
-              unsigned pos = qtail + (unsigned)(x - cnt);
+              // no wrap: total <= QCAP - 64 entries from slot 0
+              uint16_t* q = sQ + (x - cnt);
 #pragma unroll
               for (int w = 0; w < NWD; ++w) {
                 unsigned m = sMask[w * 32 + lane];
+                const unsigned eb = ((unsigned)w << 10) | ((unsigned)lane << 5);
                 while (m) {
-                  const int bit = __ffs(m) - 1;
-                  m &= m - 1u;
-                  sQ[pos & (QCAP - 1)] =
-                      (uint16_t)(((w * CB + (bit & 7)) << 7) | (lane << LOGKP) | (bit >> 3));
-                  ++pos;
+                  const unsigned bit = msb(m);   // highest set bit (one FLO)
+                  m ^= 1u << bit;
+                  *q++ = (uint16_t)(eb | bit);
                 }
               }
-              qtail += (unsigned)total;
+              qtail = (unsigned)total;
             } else {
               const int quarter = ci & 3;
               unsigned m = (sMask[(ci >> 2) * 32 + lane] >> (8 * quarter)) & 0xffu;
@@ -587,12 +596,12 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
               }
               const int t2 = __shfl_sync(0xffffffffu, x2, 31);
               unsigned pos = qtail + (unsigned)(x2 - c2);
-              const int cbase = (ci >> 2) * CB;   // quarter = point k, bits = centres
+              // quarter = point k, bits = centres
+              const unsigned eb = ((unsigned)(ci >> 2) << 10) | ((unsigned)lane << 5) | ((unsigned)quarter << 3);
               while (m) {
-                const int bit = __ffs(m) - 1;
-                m &= m - 1u;
-                sQ[pos & (QCAP - 1)] =
-                    (uint16_t)(((cbase + bit) << 7) | (lane << LOGKP) | quarter);
+                const unsigned bit = msb(m);
+                m ^= 1u << bit;
+                sQ[pos & (QCAP - 1)] = (uint16_t)(eb | bit);
                 ++pos;
               }
               qtail += (unsigned)t2;
