@@ -318,8 +318,8 @@ __device__ __forceinline__ void resolve(const KParams& p, Dec& d, const float4 P
 }
 
 // Splat an accepted pair into its image (tempSpinImage[k,l]++).
-template <int MODE>
-__device__ __forceinline__ void apply(const KParams& p, const Dec& d, uint32_t* img, uint32_t* hi,
+template <int MODE, int G>
+__device__ __forceinline__ void apply(const KParams& p, const Dec& d, uint32_t* img, int slot,
                                       int* carry_flag) {
   if (MODE == 0) {
     atomicAdd(&img[d.bin], 1u);
@@ -332,12 +332,15 @@ __device__ __forceinline__ void apply(const KParams& p, const Dec& d, uint32_t* 
     const uint32_t v2 = fixed23((1.0f - d.a) * d.c), v3 = fixed23(d.a * d.c);
     const uint32_t o0 = atomicAdd(&img[b0], v0), o1 = atomicAdd(&img[b1], v1);
     const uint32_t o2 = atomicAdd(&img[b2], v2), o3 = atomicAdd(&img[b3], v3);
-    const bool c0 = o0 + v0 < o0, c1 = o1 + v1 < o1, c2 = o2 + v2 < o2, c3 = o3 + v3 < o3;
-    if (c0 | c1 | c2 | c3) {
-      if (c0) carry_fixed(hi, b0, p.err_flags, carry_flag);
-      if (c1) carry_fixed(hi, b1, p.err_flags, carry_flag);
-      if (c2) carry_fixed(hi, b2, p.err_flags, carry_flag);
-      if (c3) carry_fixed(hi, b3, p.err_flags, carry_flag);
+    // v <= 2^23, so a wrap needs old >= 2^32 - 2^23: one screen for all four, the exact
+    // test on the rare branch
+    if (max(max(o0, o1), max(o2, o3)) >= 0xff800000u) {
+      const int hiWords = (W * W + 1) / 2;
+      uint32_t* hi = p.hi_scratch + ((size_t)blockIdx.x * G + slot) * hiWords;
+      if (o0 + v0 < o0) carry_fixed(hi, b0, p.err_flags, carry_flag);
+      if (o1 + v1 < o1) carry_fixed(hi, b1, p.err_flags, carry_flag);
+      if (o2 + v2 < o2) carry_fixed(hi, b2, p.err_flags, carry_flag);
+      if (o3 + v3 < o3) carry_fixed(hi, b3, p.err_flags, carry_flag);
     }
   }
 }
@@ -543,10 +546,10 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         if (d0.status == 2) resolve<MODE>(p, d0, P0, N0, X0, NX0, ct);
         if (APL == 2 && d1.status == 2) resolve<MODE>(p, d1, P1, N1, X1, NX1, ct);
         const int g0 = (int)(e0 >> 10) * CB + (int)(e0 & 7u), g1 = (int)(e1 >> 10) * CB + (int)(e1 & 7u);
-        if (d0.status) { ++ct.acc; apply<MODE>(p, d0, sImg + g0 * WW, gHi + g0 * hiWords, &s_carry); }
+        if (d0.status) { ++ct.acc; apply<MODE, G>(p, d0, sImg + g0 * WW, g0, &s_carry); }
         if (APL == 2 && d1.status) {
           ++ct.acc;
-          apply<MODE>(p, d1, sImg + g1 * WW, gHi + g1 * hiWords, &s_carry);
+          apply<MODE, G>(p, d1, sImg + g1 * WW, g1, &s_carry);
         }
       };
       auto compact_and_accept = [&]() {
