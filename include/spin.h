@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SPIN_ABI_VERSION 2
+#define SPIN_ABI_VERSION 3
 
 typedef struct spin_ctx* spin_handle;
 typedef struct CUstream_st* spin_stream; /* identical to cudaStream_t */
@@ -83,6 +83,13 @@ typedef struct {
   int32_t gss_min_chunk; /* GSS minimum chunk in units; 0 -> 1 (#16)                      */
   int32_t fac_divisor;   /* FAC: chunk = ceil(R_batch / (fac_divisor * P)); 0 -> 2 (#15)   */
   uint32_t flags;        /* SPIN_F_* */
+  /* Heterogeneous-worker emulation (the paper's Type1/Type2 runs; SURVEY
+   * §8(f) NEXT-1).  Timing only: images are identical for every setting. */
+  int32_t slow_ctas;     /* CTAs 0 .. slow_ctas-1 are slow workers; 0 -> none              */
+  float slowdown;        /* their time multiplier (>= 1; 0 -> 1): after each group a slow
+                            CTA idles (slowdown - 1) x the group's measured compute time  */
+  int32_t slow_first;    /* dynamic schedules: the fast CTAs wait until every slow CTA has
+                            issued its first request (the machine-file order) */
 } spin_chunk_params;
 
 /* Optional per-call statistics.  Passing non-NULL makes spin_generate synchronise

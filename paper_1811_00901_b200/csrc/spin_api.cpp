@@ -431,6 +431,8 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   if (cpar.P < 0 || cpar.unit < 0 || cpar.gss_min_chunk < 0 || cpar.fac_divisor < 0)
     return fail(SPIN_E_INVAL, "negative chunk parameter");
   if (cpar.flags & ~0x3fu) return fail(SPIN_E_INVAL, "unknown flag bits 0x%x", cpar.flags);
+  if (cpar.slow_ctas < 0 || !(cpar.slowdown == 0.0f || (cpar.slowdown >= 1.0f && cpar.slowdown <= 1e6f)))
+    return fail(SPIN_E_INVAL, "slow_ctas must be >= 0 and slowdown 0 or in [1, 1e6]");
   if ((cpar.flags & SPIN_F_SUPPORT_LAST) && (cpar.flags & SPIN_F_SUPPORT_FIRST))
     return fail(SPIN_E_INVAL, "SPIN_F_SUPPORT_LAST and SPIN_F_SUPPORT_FIRST are exclusive");
   if (M > 0 && (!d_centre_idx || !d_out)) return fail(SPIN_E_INVAL, "null d_centre_idx or d_out with M > 0");
@@ -579,6 +581,10 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   p.n_chunks = n_chunks;
   p.unit_images = unit;
   p.is_static = sched == SPIN_STATIC ? 1 : 0;
+  p.slow_ctas = cpar.slowdown > 1.0f ? std::min(cpar.slow_ctas, P) : 0;
+  p.slowdown = cpar.slowdown > 1.0f ? cpar.slowdown : 1.0f;
+  // (the wait needs every slow CTA resident: only for a persistent launch)
+  p.slow_first = (cpar.slow_first && !p.is_static && P <= occ * h->sms) ? 1 : 0;
   p.counter = h->counter;
   p.stats = h->stats;
   p.cta_t0 = h->cta_t0;

@@ -401,8 +401,13 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
 
   for (;;) {
     // ---- a6: request a chunk (PAPER.md:336-342 / 372-377)
-    if (tid == 0) s_chunk = p.is_static ? (first ? (int)blockIdx.x : p.n_chunks)
-                                        : (int)atomicAdd(p.counter, 1u);
+    if (tid == 0) {
+      if (first && p.slow_first && (int)blockIdx.x >= p.slow_ctas) {
+        // heterogeneity emulation: the slow workers request first
+        while (*reinterpret_cast<volatile unsigned*>(p.counter) < (unsigned)p.slow_ctas) __nanosleep(256);
+      }
+      s_chunk = p.is_static ? (first ? (int)blockIdx.x : p.n_chunks) : (int)atomicAdd(p.counter, 1u);
+    }
     __syncthreads();
     const int u = s_chunk;
     first = false;
@@ -413,6 +418,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
 
     for (long long g0 = i0; g0 < i1; g0 += G) {
       const int gcount = (int)min((long long)G, i1 - g0);
+      const unsigned long long tg0 = gtimer();
       // ---- a7: group setup (tempSpinImage, init, P = OP[i])
       if (tid < G) {
         const int slot = tid;
@@ -869,6 +875,12 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           __syncthreads();
           if (tid == 0) s_carry = 0;
         }
+      }
+      if ((int)blockIdx.x < p.slow_ctas && tid == 0) {
+        // heterogeneity emulation: a slow worker takes `slowdown` x the group's time
+        const unsigned long long tg1 = gtimer();
+        const unsigned long long until = tg1 + (unsigned long long)((double)(p.slowdown - 1.0f) * (double)(tg1 - tg0));
+        while (gtimer() < until) __nanosleep(512);
       }
       __syncthreads();
     }

@@ -32,7 +32,8 @@ STATUS = {0: "SPIN_OK", 1: "SPIN_E_INVAL", 2: "SPIN_E_RANGE", 3: "SPIN_E_INPUT",
 
 class ChunkParams(C.Structure):
     _fields_ = [("P", C.c_int32), ("unit", C.c_int32), ("gss_min_chunk", C.c_int32),
-                ("fac_divisor", C.c_int32), ("flags", C.c_uint32)]
+                ("fac_divisor", C.c_int32), ("flags", C.c_uint32),
+                ("slow_ctas", C.c_int32), ("slowdown", C.c_float), ("slow_first", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -170,19 +171,22 @@ class SpinEngine:
         self.N = n
 
     @staticmethod
-    def _params(P, unit, gss_min_chunk, fac_divisor, flags):
-        return ChunkParams(int(P), int(unit), int(gss_min_chunk), int(fac_divisor), int(flags))
+    def _params(P, unit, gss_min_chunk, fac_divisor, flags, slow_ctas=0, slowdown=0.0,
+                slow_first=False):
+        return ChunkParams(int(P), int(unit), int(gss_min_chunk), int(fac_divisor), int(flags),
+                           int(slow_ctas), float(slowdown), int(bool(slow_first)))
 
     def generate(self, centre_idx, W, b, cos_As, schedule="STATIC", mode="nearest", prune="brute",
                  P=0, unit=0, gss_min_chunk=0, fac_divisor=0, flags=0, out=None, stats=False,
-                 cta_capacity=0, stream=None):
-        """Images for device int32 centre_idx [M] into a device fp32 [M, W, W] tensor."""
+                 cta_capacity=0, stream=None, slow_ctas=0, slowdown=0.0, slow_first=False):
+        """Images for device int32 centre_idx [M] into a device fp32 [M, W, W] tensor.
+        slow_ctas / slowdown / slow_first: heterogeneous-worker emulation (timing only)."""
         import torch
         M = int(centre_idx.shape[0])
         assert centre_idx.dtype == torch.int32 and centre_idx.is_cuda
         if out is None:
             out = torch.empty((M, W, W), dtype=torch.float32, device=centre_idx.device)
-        cp = self._params(P, unit, gss_min_chunk, fac_divisor, flags)
+        cp = self._params(P, unit, gss_min_chunk, fac_divisor, flags, slow_ctas, slowdown, slow_first)
         st = Stats()
         t0 = t1 = un = None
         if stats and cta_capacity:

@@ -485,3 +485,35 @@ def test_support_last_same_images(spin, torch, prune):
         ora, st = oracle(P, Nn, cen[:40], 16, 0.01, 0.5, mode, cells=(prune == "cells"))
         check(b if c == 0.5 else run_gpu(spin, torch, P, Nn, cen[:40], 16, 0.01, 0.5, mode, prune=prune,
                                          flags=spin.F_SUPPORT_LAST), ora, st, mode, f"support-last {mode}")
+
+
+def test_heterogeneous_workers_same_images_and_trend(spin, torch):
+    """Heterogeneity emulation (the paper's Type1/Type2 runs):
+    slow CTAs change timing only, never images; with a quarter of the CTAs 4x slower, a
+    dynamic schedule beats STATIC (ideal ratio 4 * (111 + 37/4) / 148 = 3.25, SPEC
+    acceptance #5 asks >= 1.5), and the slow CTAs process fewer units under SS."""
+    P, Nn = clouds.bumpy_sphere(30000, 31)
+    cen = np.arange(30000, dtype=np.int32)
+    eng = spin.SpinEngine(_dev(torch, P), _dev(torch, Nn))
+    try:
+        d_cen = _dev(torch, cen)
+        ref = eng.generate(d_cen, 16, 0.02, 0.5, schedule="STATIC").clone()
+        times = {}
+        for sched in ("STATIC", "SS", "GSS", "FAC"):
+            for slow_first in (False, True):
+                kw = dict(schedule=sched, P=148, slow_ctas=37, slowdown=4.0, slow_first=slow_first)
+                out, st = eng.generate(d_cen, 16, 0.02, 0.5, stats=True, cta_capacity=148, **kw)
+                torch.cuda.synchronize()
+                assert torch.equal(out, ref), (sched, slow_first)
+                ts = []
+                for _ in range(3):
+                    _, st = eng.generate(d_cen, 16, 0.02, 0.5, stats=True, cta_capacity=148, **kw)
+                    ts.append(st["elapsed_ms"])
+                times[(sched, slow_first)] = (float(np.median(ts)), st)
+        t_static = times[("STATIC", False)][0]
+        t_ss, st_ss = times[("SS", False)]
+        assert t_static / t_ss >= 1.5, times
+        u = st_ss["cta_units"]
+        assert u[:37].mean() < 0.6 * u[37:].mean(), u
+    finally:
+        eng.close()

@@ -37,8 +37,15 @@ def main(argv=None):
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--P", default="0")
     ap.add_argument("--units", default="0,1")
-    ap.add_argument("--policies", default="STATIC,SS,GSS,FAC")
+    ap.add_argument("--policies", default="STATIC,SS,GSS,FAC",
+                    help="STATIC,SS,GSS,FAC and HW (one CTA per unit, the hardware block "
+                         "scheduler as the dealer: the non-persistent control of SURVEY 8(d))")
     ap.add_argument("--no-sort", action="store_true")
+    # heterogeneous-worker emulation: CTAs 0..slow-1 run `slowdown` x slower
+    ap.add_argument("--slow", type=int, default=0, help="number of slow CTAs")
+    ap.add_argument("--slowdown", type=float, default=0.0)
+    ap.add_argument("--slow-first", action="store_true", help="slow CTAs request first (P:449, P:564)")
+    ap.add_argument("--steps-tag", default="")
     args = ap.parse_args(argv)
 
     import torch
@@ -56,13 +63,20 @@ def main(argv=None):
     flags = spin.F_NO_SORT if args.no_sort else 0
     ref = None
     results = {}
+    lastP = 0
     for Pn in [int(x) for x in args.P.split(",")]:
         for unit in [int(x) for x in args.units.split(",")]:
             for pol in args.policies.split(","):
                 if pol == "SS" and unit == 1 and len(cen) > 20000:
                     continue   # one image per request: G-fold wasted slots, skip at scale
-                kw = dict(schedule=pol, mode=mode, prune=cfg["prune"], P=Pn, unit=unit,
-                          flags=flags, out=out)
+                sched, Pp = pol, Pn
+                if pol == "HW":   # non-persistent control: STATIC with one unit per CTA
+                    G0 = eng.generate(d_cen[:1], W, cfg["b"], cfg["cos_As"], mode=mode, prune=cfg["prune"],
+                                      stats=True)[1]["G"]
+                    sched, Pp = "STATIC", -(-len(cen) // (unit or G0))
+                kw = dict(schedule=sched, mode=mode, prune=cfg["prune"], P=Pp, unit=unit,
+                          flags=flags, out=out, slow_ctas=args.slow, slowdown=args.slowdown,
+                          slow_first=args.slow_first)
                 eng.generate(d_cen, W, cfg["b"], cfg["cos_As"], **kw)   # warm-up
                 times, busy_max_over_mean, busy_cov, finish_cov = [], [], [], []
                 st = None
@@ -70,8 +84,9 @@ def main(argv=None):
                     _, st = eng.generate(d_cen, W, cfg["b"], cfg["cos_As"], stats=True,
                                          cta_capacity=4096, **kw)
                     times.append(st["elapsed_ms"])
-                    t0 = st["cta_start_ns"][:st["P"]].astype(np.float64)
-                    t1 = st["cta_end_ns"][:st["P"]].astype(np.float64)
+                    npc = min(st["P"], 4096)
+                    t0 = st["cta_start_ns"][:npc].astype(np.float64)
+                    t1 = st["cta_end_ns"][:npc].astype(np.float64)
                     fin = t1 - t0.min()
                     busy = t1 - t0
                     busy_max_over_mean.append(busy.max() / busy.mean())
@@ -83,9 +98,13 @@ def main(argv=None):
                 elif mode == "nearest" or True:
                     assert torch.equal(out, ref), f"{pol} P={Pn} unit={unit} changed the images"
                 q = quartiles(times)
-                key = (pol, st["P"], unit or st["G"])
+                if pol != "HW":
+                    lastP = st["P"]
+                key = (pol, lastP if pol == "HW" else st["P"], unit or st["G"])
                 results[key] = q
                 print(json.dumps({"config": cfg["name"], "W": W, "mode": mode, "policy": pol,
+                                  "slow_ctas": args.slow, "slowdown": args.slowdown,
+                                  "slow_first": args.slow_first,
                                   "P": st["P"], "unit": unit or st["G"], "G": st["G"],
                                   "n_chunks": st["n_chunks"], "ms": q,
                                   "parallel_cost_cta_s": st["P"] * q["median"] * 1e-3,
