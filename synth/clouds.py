@@ -185,6 +185,12 @@ CONFIGS = {
             deg=90.0, cos_As=0.0, mode="bilinear", prune="brute", centres="iota"),
     5: dict(name="C5-clustered4M", kind="clustered", N=4_000_000, M=500_000, W=8, b=0.005,
             deg=60.0, cos_As=0.5, mode="nearest", prune="cells", centres="random", density_span=100.0),
+    # the paper's own workload shape -- an ~826K-point closed surface
+    # standing in for the Ramesses mesh (not available), W = 5, B = 0.1, S = 2 pi
+    # (support test disabled), paper-N = 10% of the points; b taken as an
+    # absolute length (reading #11), counts (Alg. 1 increments) with real W/2 (#3)
+    6: dict(name="P6-paper826k", kind="bumpy", N=826_000, M=82_600, W=5, b=0.1, deg=360.0,
+            cos_As=float("-inf"), mode="nearest", prune="brute", centres="iota"),
 }
 
 

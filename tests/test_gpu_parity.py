@@ -398,6 +398,21 @@ def test_config4_full_sampled(spin, torch):
     _full(spin, torch, 4, "bilinear", "brute", 12, sched="SS")
 
 
+def test_config6_paper_shape_sampled(spin, torch):
+    """NEXT-3, the paper's workload shape (826K-point surface, W = 5, b = 0.1, no support
+    test, 10% of the points as centres), in full on the GPU, sampled against the oracle;
+    plus the literal-formula reading (#2) on the same subsample."""
+    gpu, st = _full(spin, torch, 6, "nearest", "brute", 16, sched="SS")
+    cfg = clouds.CONFIGS[6]
+    P, Nn = clouds.make_cloud(6)
+    pick = clouds.subsample(cfg["M"], 8, 206)
+    cen = clouds.make_centres(6, cfg["N"])[pick]
+    lit = run_gpu(spin, torch, P, Nn, cen, cfg["W"], cfg["b"], cfg["cos_As"], "nearest",
+                  flags=spin.F_LITERAL_HALF_WIDTH)
+    ora, so = oracle(P, Nn, cen, cfg["W"], cfg["b"], cfg["cos_As"], "nearest", flags=1)
+    check(lit, ora, so, "nearest", "P6 literal")
+
+
 @pytest.mark.parametrize("W", [8, 24])
 def test_config5_full_sampled(spin, torch, W):
     _full(spin, torch, 5, "nearest", "cells", 20, W=W, sched="GSS")
