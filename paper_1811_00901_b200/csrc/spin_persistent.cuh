@@ -371,6 +371,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   int* sRowO = reinterpret_cast<int*>(smem + L.oRowO);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool skip_accept = p.debug_skip != 0;   // measurement knob (SPIN_DEBUG_SKIP)
   constexpr int QCAP = qcap_of(PRUNE);
   uint16_t* sQ = reinterpret_cast<uint16_t*>(smem + L.oQ) + warp * QCAP;
   // staged tile of this warp in pair layout: record r (0..3) of point pair pr (0..KP/2-1)
@@ -535,7 +536,6 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       // two independent decisions interleave; BRUTE keeps one (fewer live registers).
       constexpr int APL = PRUNE == 1 ? 2 : SPIN_APL_BRUTE;
       auto process_pair = [&](unsigned e0, bool v0, unsigned e1, bool v1) {
-        if (p.debug_skip) return;
         float4 P0, N0, X0, NX0, P1, N1, X1, NX1;
         load_entry(e0, P0, N0, X0, NX0);
         Dec d0 = decide<MODE>(p, P0, N0, X0, NX0);
@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             const unsigned e1 = APL == 2 ? sQ[(qhead + 32u + lane) & (QCAP - 1)] : 0u;
             __syncwarp();
             qhead += n;
-            if (v0) process_pair(v0 ? e0 : 0u, v0, v1 ? e1 : 0u, v1);
+            if (v0 && !skip_accept) process_pair(v0 ? e0 : 0u, v0, v1 ? e1 : 0u, v1);
           }
           if (!more) break;
         }
@@ -662,15 +662,15 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         }
         const float c_test = p.c_test, h_test = p.h_test;
         const bool sup_hot = SUP == 1 || (SUP == 2 && sup_on);
+        // a partial group skips its empty batches (their mask words are zero)
+        const int cb_end = ((gcount + CB - 1) / CB) * CB;
+        for (int cb = cb_end; cb < G; cb += CB) sMask[(cb / CB) * 32 + lane] = 0u;
+        // mask bit (k << 3) | c: point k of this lane, centre cb + c; one loop per variant
+        // so the variant branch is taken once per tile, not once per batch
+        if (PRUNE == 0 && !sup_hot) {
 #pragma unroll 1
-        for (int cb = 0; cb < G; cb += CB) {
-          unsigned mask = 0u;
-          if (cb >= gcount) {            // a partial group skips its empty slots
-            sMask[(cb / CB) * 32 + lane] = 0u;
-            continue;
-          }
-          // mask bit (k << 3) | c: point k of this lane, centre cb + c
-          if (PRUNE == 0 && !sup_hot) {
+          for (int cb = 0; cb < cb_end; cb += CB) {
+            unsigned rej = 0u;
 #pragma unroll
             for (int c = 0; c < CB; ++c) {
               const float4 B4 = sB[cb + c];
@@ -683,10 +683,14 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
                                    fma2(bc2(B4.z), Z2[k2], bc2(B4.w)))), NXX2[k2]);
                 up2u(m2, mb[2 * k2], mb[2 * k2 + 1]);
               }
-              mask = reject_bits4(mask, mb[0], mb[1], mb[2], mb[3], 0x01010101u << c);
+              rej = reject_bits4(rej, mb[0], mb[1], mb[2], mb[3], 0x01010101u << c);
             }
-            mask = ~mask & (0x01010101u * ((1u << CB) - 1u));
-          } else if (PRUNE == 0) {
+            sMask[(cb / CB) * 32 + lane] = ~rej & (0x01010101u * ((1u << CB) - 1u));
+          }
+        } else if (PRUNE == 0) {
+#pragma unroll 1
+          for (int cb = 0; cb < cb_end; cb += CB) {
+            unsigned mask = 0u;
 #pragma unroll
             for (int c = 0; c < CB; ++c) {
               const float4 A4 = sA[cb + c];
@@ -704,7 +708,12 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
                 mask = pair_bit_sm(mask, s1, c_test, q1, 1u << ((2 * k2 + 1) * 8 + c));
               }
             }
-          } else {
+            sMask[(cb / CB) * 32 + lane] = mask;
+          }
+        } else {
+#pragma unroll 1
+          for (int cb = 0; cb < cb_end; cb += CB) {
+            unsigned mask = 0u;
 #pragma unroll
             for (int c = 0; c < CB; ++c) {
               const float4 A4 = sA[cb + c];
@@ -732,8 +741,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
                 }
               }
             }
+            sMask[(cb / CB) * 32 + lane] = mask;
           }
-          sMask[(cb / CB) * 32 + lane] = mask;
         }
         __syncwarp();
         if (p.debug_skip < 2) compact_and_accept();
