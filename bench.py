@@ -42,6 +42,9 @@ def parse(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="spin", choices=["spin", "reference"])
     ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="weak: every GPU runs the full workload (default); strong: the "
+                         "configured centres are split across GPUs")
     ap.add_argument("--mode", default=None, choices=[None, "nearest", "bilinear"])
     ap.add_argument("--schedule", default="SS", choices=["STATIC", "SS", "GSS", "FAC"])
     ap.add_argument("--W", type=int, default=None)
@@ -75,6 +78,16 @@ def dist_init(backend):
     return dist
 
 
+def allreduce_sum(x: float, device=None) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def allreduce_max(x: float, device=None) -> float:
     import torch
     import torch.distributed as dist
@@ -91,11 +104,17 @@ def barrier():
         dist.barrier()
 
 
-def rank_centres(cfg_id: int, n_points: int, rank: int):
+def rank_centres(cfg_id: int, n_points: int, rank: int, world: int = 1, strong: bool = False):
     """Weak scaling: every rank runs the full workload; centres rotated by rank so ranks
-    do not duplicate each other's images when M < N (images are independent)."""
+    do not duplicate each other's images when M < N (images are independent).
+    Strong scaling (the paper's fixed 80K images): rank r takes the r-th
+    contiguous block of the configured centres (STATIC across GPUs, no collective)."""
     from synth import clouds
     cen = clouds.make_centres(cfg_id, n_points)
+    if strong:
+        q, r = divmod(len(cen), world)
+        a = rank * q + min(rank, r)
+        return cen[a:a + q + (rank < r)]
     if rank:
         cen = ((cen.astype(np.int64) + rank * 7919) % n_points).astype(np.int32)
     return cen
@@ -244,7 +263,8 @@ def run_spin(args):
         cfg["W"] = args.W
     W, b, c, mode, prune = cfg["W"], cfg["b"], cfg["cos_As"], args.mode or cfg["mode"], cfg["prune"]
     P, Nn = clouds.make_cloud(args.config)
-    cen = rank_centres(args.config, cfg["N"], rank)
+    strong = args.scaling == "strong"
+    cen = rank_centres(args.config, cfg["N"], rank, world, strong)
     M, N = len(cen), len(P)
     stream = torch.cuda.current_stream()
     eng = spin.SpinEngine(torch.from_numpy(P).to(dev), torch.from_numpy(Nn).to(dev))
@@ -293,6 +313,7 @@ def run_spin(args):
     # secondary (same run): the support test on every pair in the hot loop, the paper's
     # order (P:166 before P:169-171) -- identical images; reported beside the main line
     alt = None
+    pairs_all_est = allreduce_sum(pairs_step, dev)
     if args.support == "auto" and cfg["cos_As"] > -math.inf:
         akw = dict(kw, flags=spin.F_SUPPORT_FIRST)
         for _ in range(2):
@@ -308,16 +329,17 @@ def run_spin(args):
         torch.cuda.synchronize()
         a_ms = allreduce_max(sum(e0.elapsed_time(e1) for e0, e1 in aev), dev) / args.steps
         _, ast = eng.generate(d_cen, W, b, c, stats=True, **akw)
-        alt = {"flag": "SPIN_F_SUPPORT_FIRST", "value": pairs_step * world / (a_ms * 1e-3),
+        alt = {"flag": "SPIN_F_SUPPORT_FIRST", "value": pairs_all_est / (a_ms * 1e-3),
                "unit": UNIT, "ms_per_step": a_ms, "kernel_ms": ast["elapsed_ms"],
                "fp32_frac_algorithmic_20flop": pairs_step * FLOP_PER_PAIR / (ast["elapsed_ms"] * 1e-3)
                                                / (FP32_PEAK_TFLOPS * 1e12),
                "pairs_candidate": ast["pairs_candidate"],
                "note": "support test n.n_x >= cos_As on every pair in the hot loop; images identical"}
 
-    pairs_all = pairs_step * world
+    pairs_all = allreduce_sum(pairs_step, dev)       # = pairs_step * world for weak scaling
+    M_all = int(allreduce_sum(M, dev))
     value = pairs_all * args.steps / (total_ms * 1e-3)
-    images_per_s = M * world * args.steps / (total_ms * 1e-3)
+    images_per_s = M_all * args.steps / (total_ms * 1e-3)
 
     # ---- e2e through the public host-buffer API: cloud + centres H2D, images D2H
     e2e = None
@@ -339,7 +361,7 @@ def run_spin(args):
         e2e_s = allreduce_max(time.perf_counter() - t0, dev)
         e2e = {"value": pairs_all * args.e2e_steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(24 * N + 4 * M), "d2h_bytes_per_step": int(4 * M * W * W),
-               "images_per_s": M * world * args.e2e_steps / e2e_s,
+               "images_per_s": M_all * args.e2e_steps / e2e_s,
                "timing": "host wall clock around load_cloud + generate_host (which syncs)"}
 
     cpu = None
@@ -350,7 +372,7 @@ def run_spin(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg["name"], "N": N, "M": M, "W": W, "b": b, "cos_As": c,
                    "mode": mode, "prune": prune, "schedule": args.schedule,
                    "P": st0["P"], "G": st0["G"], "unit": args.unit or st0["G"],
@@ -359,7 +381,8 @@ def run_spin(args):
                                     "last": "candidates only"}[args.support],
                    "tiles_support_hot": st0["tiles_support_hot"],
                    "n_chunks": st0["n_chunks"], "l2": "flushed (256 MB write) before every step",
-                   "parallelism": f"replicas x{world} (independent images, no collective)"},
+                   "parallelism": (f"replicas x{world}" if args.scaling == "weak" else f"centre shards x{world}")
+                                  + " (independent images, no collective)"},
         "images_per_s": images_per_s,
         "fp32_peak_frac": value / world * FLOP_PER_PAIR / (FP32_PEAK_TFLOPS * 1e12),
         "roofline": {"bound": "alu", "achieved": achieved_tflops, "peak": FP32_PEAK_TFLOPS,

@@ -29,9 +29,11 @@ def _worker(rank, world, port, q):
     import bench
     bench.dist_init("gloo")
     t = bench.allreduce_max(float(rank * 10 + 1))
+    s = bench.allreduce_sum(float(rank + 1))
     bench.barrier()
     cen = bench.rank_centres(3, 1_000_000, rank)[:1000]
-    q.put((rank, t, cen.tolist()))
+    strong = bench.rank_centres(1, 2000, rank, world, strong=True)
+    q.put((rank, t, cen.tolist(), s, strong.tolist()))
     dist.destroy_process_group()
 
 
@@ -48,8 +50,12 @@ def test_gloo_two_ranks_max_and_distinct_shards():
         p.join(60)
         assert p.exitcode == 0
     assert res[0][1] == res[1][1] == 11.0          # max over ranks
+    assert res[0][3] == res[1][3] == 3.0           # sum over ranks (pairs, images)
     a, b = np.asarray(res[0][2]), np.asarray(res[1][2])
     assert not np.array_equal(a, b)               # ranks run distinct images
+    # strong scaling: the configured centres split into disjoint contiguous shards
+    s0, s1 = res[0][4], res[1][4]
+    assert s0 + s1 == list(range(2000)) and len(s0) == len(s1) == 1000
 
 
 def test_reference_arm_json_line():
