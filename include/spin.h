@@ -209,6 +209,33 @@ void spin_destroy(spin_handle h);
 const char* spin_last_error(void);
 int32_t spin_abi_version(void);
 
+/* ---- Host-side ingestion: the paper's OP = read3DPoints(OF)
+ * (Alg. 3).  Pure host code, no device and no handle needed; errors set
+ * spin_last_error with the file and line. */
+
+/* spin_read_xyzn — an xyzn text file: one oriented point per line, six reals
+ * "x y z nx ny nz", blank lines and '#' comments skipped, file order kept (indices are
+ * the paper's i of OP[i]).  Normals are normalised in double, then rounded to fp32.
+ *   points, normals: caller fp32 [cap][3], or both NULL to count only; *n_out = points.
+ *   SPIN_E_INPUT: malformed line, non-finite value, zero normal (names the line), empty
+ *   cloud; SPIN_E_RANGE: more than cap points; SPIN_E_INVAL: null path / unreadable. */
+spin_status spin_read_xyzn(const char* path, float* points, float* normals, int64_t cap,
+                           int64_t* n_out);
+
+/* spin_read_off — an ASCII OFF triangle mesh ("OFF", "nv nf ne", nv vertex lines, nf
+ * lines "3 i j k").  vertices: fp32 [vcap][3], faces: int32 [fcap][3]; pass NULL for
+ * either to read only the counts *nv_out, *nf_out.  SPIN_E_INPUT on a malformed or
+ * non-triangle face or an index outside [0, nv). */
+spin_status spin_read_off(const char* path, float* vertices, int64_t vcap, int32_t* faces,
+                          int64_t fcap, int64_t* nv_out, int64_t* nf_out);
+
+/* spin_vertex_normals — per-vertex unit normals of a triangle mesh: the normalised sum
+ * of the incident faces' un-normalised normals (e1 x e2, so area-weighted), accumulated
+ * in double.  normals: caller fp32 [nv][3].  SPIN_E_INPUT if a vertex has no incident
+ * face or only zero-area ones, or a face index is out of range. */
+spin_status spin_vertex_normals(const float* vertices, int64_t nv, const int32_t* faces,
+                                int64_t nf, float* normals);
+
 #ifdef __cplusplus
 }
 #endif

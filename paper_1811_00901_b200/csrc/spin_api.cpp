@@ -36,6 +36,23 @@ spin_status fail(spin_status st, const char* fmt, ...) {
   g_err = buf;
   return st;
 }
+}  // namespace
+
+// shared with spin_io.cpp (host-side ingestion): same thread-local last-error text
+namespace spin {
+spin_status io_fail(spin_status st, const char* fmt, ...);
+}
+spin_status spin::io_fail(spin_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+namespace {
 spin_status cuda_fail(cudaError_t e, const char* what) {
   return fail(SPIN_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }

@@ -67,9 +67,54 @@ _lib.spin_abi_version.restype = C.c_int32
 for _f in ("spin_create", "spin_load_cloud", "spin_generate", "spin_generate_host", "spin_chunk_sequence"):
     getattr(_lib, _f).restype = C.c_int
 
+_lib.spin_read_xyzn.argtypes = [C.c_char_p, _vp, _vp, C.c_int64, C.POINTER(C.c_int64)]
+_lib.spin_read_off.argtypes = [C.c_char_p, _vp, C.c_int64, _vp, C.c_int64,
+                               C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+_lib.spin_vertex_normals.argtypes = [_vp, C.c_int64, _vp, C.c_int64, _vp]
+for _f in ("spin_read_xyzn", "spin_read_off", "spin_vertex_normals"):
+    getattr(_lib, _f).restype = C.c_int
+
 EXPORTS = ["spin_create", "spin_load_cloud", "spin_generate", "spin_generate_host",
            "spin_chunk_sequence", "spin_region_radius", "spin_cos_from_degrees", "spin_default_P",
-           "spin_destroy", "spin_last_error", "spin_abi_version"]
+           "spin_destroy", "spin_last_error", "spin_abi_version",
+           "spin_read_xyzn", "spin_read_off", "spin_vertex_normals"]
+
+
+def read_xyzn(path):
+    """spin_read_xyzn: (points fp32 [N,3], unit normals fp32 [N,3]) in file order."""
+    n = C.c_int64()
+    _check(_lib.spin_read_xyzn(os.fsencode(path), None, None, 0, C.byref(n)))
+    P = np.empty((n.value, 3), np.float32)
+    Nn = np.empty((n.value, 3), np.float32)
+    _check(_lib.spin_read_xyzn(os.fsencode(path), P.ctypes.data, Nn.ctypes.data, n.value, C.byref(n)))
+    return P, Nn
+
+
+def read_off(path):
+    """spin_read_off: (vertices fp32 [nv,3], triangles int32 [nf,3])."""
+    nv, nf = C.c_int64(), C.c_int64()
+    _check(_lib.spin_read_off(os.fsencode(path), None, 0, None, 0, C.byref(nv), C.byref(nf)))
+    V = np.empty((nv.value, 3), np.float32)
+    F = np.empty((nf.value, 3), np.int32)
+    _check(_lib.spin_read_off(os.fsencode(path), V.ctypes.data, nv.value, F.ctypes.data, nf.value,
+                              C.byref(nv), C.byref(nf)))
+    return V, F
+
+
+def vertex_normals(V, F):
+    """spin_vertex_normals: area-weighted unit vertex normals fp32 [nv,3]."""
+    V = np.ascontiguousarray(V, np.float32)
+    F = np.ascontiguousarray(F, np.int32)
+    out = np.empty_like(V)
+    _check(_lib.spin_vertex_normals(V.ctypes.data, len(V), F.ctypes.data if len(F) else None,
+                                    len(F), out.ctypes.data))
+    return out
+
+
+def load_mesh_cloud(path):
+    """An oriented point cloud from an OFF mesh: its vertices with area-weighted normals."""
+    V, F = read_off(path)
+    return V, vertex_normals(V, F)
 
 
 class SpinError(RuntimeError):
