@@ -622,7 +622,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   if (prune == SPIN_BRUTE) {
     p.pos = h->pos;
     p.nrm = h->nrm;
-    p.n_tiles = (int32_t)(((h->N + tile_points() - 1) / tile_points()));
+    p.n_tiles = (int32_t)((h->N + lc.threads * KP_POINTS - 1) / (lc.threads * KP_POINTS));
   } else {
     const float R = f32_up(rg.R * (1.0 + 1e-6) + 1e-30);
     spin_status st = ensure_grid(h, R, s, &grid_ms);

@@ -84,13 +84,14 @@ enum StatSlot {
 // Launch configuration chosen by the planner.
 struct LaunchCfg {
   int G;           // images per group (4 .. 64)
-  int threads;     // NT
+  int threads;     // threads per CTA (768, or 512 for G = 32 at W > 24)
   size_t smem;     // dynamic shared memory bytes
 };
 
 // ---- launchers implemented in spin_kernels.cu
 LaunchCfg choose_launch(int W, int mode, int prune);
-int tile_points();   // points per CTA tile (NT x KP)
+int tile_points();   // cloud padding: a multiple of every CTA tile (threads x KP points)
+constexpr int KP_POINTS = 4;   // points per thread (register blocking; SPIN_KP)
 int occupancy_blocks(const LaunchCfg& lc, int W, int mode, int prune);
 cudaError_t launch_spin(const LaunchCfg& lc, int mode, int prune, int grid, const KParams& p,
                         cudaStream_t s);

@@ -6,36 +6,47 @@
 namespace spin {
 
 // ------------------------------------------------------------------ dispatch
-const void* kernel_ptr_0_0(int prune, int G);
-const void* kernel_ptr_0_1(int prune, int G);
-const void* kernel_ptr_1_0(int prune, int G);
-const void* kernel_ptr_1_1(int prune, int G);
-const void* kernel_ptr_0_2(int prune, int G);
-const void* kernel_ptr_1_2(int prune, int G);
-static const void* kernel_for(int mode, int prune, int G, int sup) {
+const void* kernel_ptr_0_0(int prune, int G, int nt);
+const void* kernel_ptr_0_1(int prune, int G, int nt);
+const void* kernel_ptr_1_0(int prune, int G, int nt);
+const void* kernel_ptr_1_1(int prune, int G, int nt);
+const void* kernel_ptr_0_2(int prune, int G, int nt);
+const void* kernel_ptr_1_2(int prune, int G, int nt);
+static const void* kernel_for(int mode, int prune, int G, int sup, int nt) {
   if (prune == 1 && sup == 2) sup = 1;   // adaptive placement is BRUTE-only
-  if (mode == 0) return sup == 2 ? kernel_ptr_0_2(prune, G) : sup ? kernel_ptr_0_1(prune, G) : kernel_ptr_0_0(prune, G);
-  return sup == 2 ? kernel_ptr_1_2(prune, G) : sup ? kernel_ptr_1_1(prune, G) : kernel_ptr_1_0(prune, G);
+  if (mode == 0)
+    return sup == 2 ? kernel_ptr_0_2(prune, G, nt) : sup ? kernel_ptr_0_1(prune, G, nt) : kernel_ptr_0_0(prune, G, nt);
+  return sup == 2 ? kernel_ptr_1_2(prune, G, nt) : sup ? kernel_ptr_1_1(prune, G, nt) : kernel_ptr_1_0(prune, G, nt);
 }
 
 LaunchCfg choose_launch(int W, int mode, int prune) {
-  // One 768-thread CTA per SM.  Images live in shared memory (NEAREST 4 B/bin,
-  // BILINEAR 6 B/bin); take the largest G in {64, 32, 16, 8, 4} whose layout fits.
+  // One CTA per SM.  Images live in shared memory (NEAREST 4 B/bin, BILINEAR 6 B/bin);
+  // take the largest G in {64, 32, 16, 8, 4} whose 768-thread layout fits.  When that
+  // G is below 32 (BRUTE, W > 24), a 512-thread CTA with G = 32 is taken instead: its
+  // smaller staged tile frees the room, and tile reuse by 32 centres beats the extra
+  // warps (C4: 524 -> 469 ms).
+  constexpr int LIMIT = 220 * 1024;
   int G = 64;
   if (prune == 1) G = 32;   // CELLS: larger groups grow the visited box (measured: 32 best)
-  if (const char* g = std::getenv("SPIN_DEBUG_G")) G = std::atoi(g);   // measurement knob
-  while (G > 4 && make_layout(G, W, mode, prune).total > 220 * 1024) G >>= 1;
+  const char* dg = std::getenv("SPIN_DEBUG_G");   // measurement knob
+  if (dg) G = std::atoi(dg);
+  while (G > 4 && make_layout(G, W, mode, prune, NT_DEFAULT).total > LIMIT) G >>= 1;
   LaunchCfg lc;
   lc.G = G;
-  lc.threads = NT;
-  lc.smem = make_layout(G, W, mode, prune).total;
+  lc.threads = NT_DEFAULT;
+  if (prune == 0 && G < 32 && !dg && make_layout(32, W, mode, prune, 512).total <= LIMIT) {
+    lc.G = 32;
+    lc.threads = 512;
+  }
+  lc.smem = make_layout(lc.G, W, mode, prune, lc.threads).total;
   return lc;
 }
 
-int tile_points() { return NT * KP; }
+// cloud padding: a multiple of every CTA tile (768 x 4 and 512 x 4 points)
+int tile_points() { return 6144; }
 
 int occupancy_blocks(const LaunchCfg& lc, int W, int mode, int prune) {
-  const void* f = kernel_for(mode, prune, lc.G, 1);
+  const void* f = kernel_for(mode, prune, lc.G, 1, lc.threads);
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.smem);
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, lc.threads, lc.smem) != cudaSuccess)
@@ -46,7 +57,7 @@ int occupancy_blocks(const LaunchCfg& lc, int W, int mode, int prune) {
 
 cudaError_t launch_spin(const LaunchCfg& lc, int mode, int prune, int grid, const KParams& p,
                         cudaStream_t s) {
-  const void* f = kernel_for(mode, prune, lc.G, p.support_in_hot);
+  const void* f = kernel_for(mode, prune, lc.G, p.support_in_hot, lc.threads);
   cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.smem);
   if (e != cudaSuccess) return e;
   void* args[] = {(void*)&p};

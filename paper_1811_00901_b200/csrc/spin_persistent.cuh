@@ -42,8 +42,7 @@
 
 namespace spin {
 
-constexpr int NT = SPIN_NT;       // threads per CTA (one CTA per SM)
-constexpr int NWARP = NT / 32;
+constexpr int NT_DEFAULT = SPIN_NT;   // threads per CTA (one CTA per SM); 512 for G = 32 at W > 24
 constexpr int KP = SPIN_KP;       // points per thread (register blocking)
 constexpr int LOGKP = KP == 4 ? 2 : 1;
 constexpr int CB_MAX = 32 / KP;   // centres per mask batch: CB * KP <= 32 bits
@@ -51,9 +50,8 @@ __host__ __device__ constexpr int cb_of(int G) { return G < CB_MAX ? G : CB_MAX;
 // per-warp candidate ring of u16 entries (power of two): BRUTE tiles hold few candidates
 // (~2% of pairs), CELLS tiles in dense clusters many
 __host__ __device__ constexpr int qcap_of(int prune) { return prune ? 1024 : 512; }
-constexpr int ROWCAP = NT;        // CELLS: grid rows staged per batch
 
-static_assert(CB_MAX * KP == 32 && KP == 4, "mask is one u32: bit (k << 3) | c");
+static_assert(CB_MAX * KP == 32 && KP == 4 && KP == KP_POINTS, "mask is one u32: bit (k << 3) | c");
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -162,7 +160,8 @@ struct Layout {
   size_t oA, oB, oP, oN, oM, oImg, oHi, oQ, oTP, oTN, oMask, oRowS, oRowO, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
-__host__ __device__ inline Layout make_layout(int G, int W, int mode, int prune) {
+__host__ __device__ inline Layout make_layout(int G, int W, int mode, int prune, int nt) {
+  const int NWARP = nt / 32, ROWCAP = nt;   // CELLS: grid rows staged per batch = threads
   Layout L;
   size_t o = 0;
   L.oA = o; o += 16 * (size_t)G;
@@ -349,8 +348,10 @@ __device__ __forceinline__ void apply(const KParams& p, const Dec& d, uint32_t* 
 // SUP = 1: the hot loop evaluates the support test for every pair (the paper's order,
 // P:166 before P:169-171); SUP = 0: the hot loop tests the region only and the support
 // test is decided in the accept path (SPIN_F_SUPPORT_LAST, or no support test at all).
-template <int MODE, int PRUNE, int G, int SUP>
+template <int MODE, int PRUNE, int G, int SUP, int NT>
 __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__ KParams p) {
+  constexpr int NWARP = NT / 32;
+  constexpr int ROWCAP = NT;        // CELLS: grid rows staged per batch
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_chunk;
   __shared__ int s_total, s_live;
@@ -359,7 +360,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
 
   const int W = p.W;
   const int WW = W * W;
-  const Layout L = make_layout(G, W, MODE, PRUNE);
+  const Layout L = make_layout(G, W, MODE, PRUNE, NT);
   float4* sA = reinterpret_cast<float4*>(smem + L.oA);
   float4* sB = reinterpret_cast<float4*>(smem + L.oB);
   float4* sP = reinterpret_cast<float4*>(smem + L.oP);
