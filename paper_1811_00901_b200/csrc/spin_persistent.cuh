@@ -561,8 +561,13 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       };
       auto compact_and_accept = [&]() {
         int cnt = 0;
+        unsigned wm = 0u;   // this lane's nonzero mask words
 #pragma unroll
-        for (int w = 0; w < NWD; ++w) cnt += __popc(sMask[w * 32 + lane]);
+        for (int w = 0; w < NWD; ++w) {
+          const unsigned mw = sMask[w * 32 + lane];
+          cnt += __popc(mw);
+          wm |= (unsigned)(mw != 0u) << w;
+        }
         int x = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -583,14 +588,33 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             if (!dense) {
               // no wrap: total <= QCAP - 64 entries from slot 0
               uint16_t* q = sQ + (x - cnt);
-#pragma unroll
-              for (int w = 0; w < NWD; ++w) {
-                unsigned m = sMask[w * 32 + lane];
-                const unsigned eb = ((unsigned)w << 10) | ((unsigned)lane << 5);
-                while (m) {
-                  const unsigned bit = msb(m);   // highest set bit (one FLO)
+              if (PRUNE == 0) {
+                // sparse (BRUTE, ~0.7 bits per lane word): one flat loop over this lane's
+                // set bits, so the warp trip count is the largest per-lane count, not the
+                // sum over words of per-word maxima
+                unsigned m = 0u, eb = 0u;
+                for (int left = cnt; left > 0; --left) {
+                  if (m == 0u) {                  // next nonzero word of this lane
+                    const unsigned w = msb(wm);
+                    wm ^= 1u << w;
+                    m = sMask[w * 32 + lane];
+                    eb = (w << 10) | ((unsigned)lane << 5);
+                  }
+                  const unsigned bit = msb(m);    // highest set bit (one FLO)
                   m ^= 1u << bit;
                   *q++ = (uint16_t)(eb | bit);
+                }
+              } else {
+                // dense (CELLS): word by word
+#pragma unroll
+                for (int w = 0; w < NWD; ++w) {
+                  unsigned m = sMask[w * 32 + lane];
+                  const unsigned eb = ((unsigned)w << 10) | ((unsigned)lane << 5);
+                  while (m) {
+                    const unsigned bit = msb(m);
+                    m ^= 1u << bit;
+                    *q++ = (uint16_t)(eb | bit);
+                  }
                 }
               }
               qtail = (unsigned)total;
