@@ -174,7 +174,7 @@ struct spin_ctx {
   uint64_t grid_version = 0;
   float grid_h = 0.f;
   int dx = 0, dy = 0, dz = 0;
-  float ox = 0, oy = 0, oz = 0, inv_h = 0;
+  float ox = 0, oy = 0, oz = 0, inv_h = 0, h_cell = 0;
   int32_t* cell_start = nullptr; int64_t cell_start_cap = 0;
   float4* spos = nullptr; int64_t spos_cap = 0;
   float4* snrm = nullptr; int64_t snrm_cap = 0;
@@ -286,6 +286,7 @@ spin_status ensure_grid(spin_ctx* h, float R, cudaStream_t s, double* build_ms) 
   h->oy = h->aabb[1];
   h->oz = h->aabb[2];
   h->inv_h = (float)(1.0 / hh);
+  h->h_cell = (float)hh;
   auto dim = [&](float lo, float hi) {
     const float t = (hi - lo) * h->inv_h;  // same rounding as the device cell_coord
     return (int)std::floor(t) + 1;
@@ -633,6 +634,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
     p.dimx = h->dx; p.dimy = h->dy; p.dimz = h->dz;
     p.ox = h->ox; p.oy = h->oy; p.oz = h->oz;
     p.inv_h = h->inv_h;
+    p.h_cell = h->h_cell;
     p.R_up = R;
     if (!(flags & SPIN_F_NO_SORT)) {
       int shift = 0;

@@ -64,6 +64,7 @@ struct KParams {
   int32_t dimx, dimy, dimz;
   float ox, oy, oz, inv_h;                 // cell = floor((x - o) * inv_h)
   float R_up;                              // region radius rounded up
+  float h_cell;                            // cell edge (1 / inv_h, as the host chose it)
   int32_t row_cap;
 
   // ---- instrumentation (a13) and errors

@@ -821,8 +821,34 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             const int row = rb + tid;
             const int cz = cz0 + row / ny, cy = cy0 + row % ny;
             const int base = (cz * p.dimy + cy) * p.dimx;
-            start = p.cell_start[base + cx0];
-            len = p.cell_start[base + cx1 + 1] - start;
+            // x-cells of this row that some live centre's R-sphere can reach: the hull
+            // of the chords over the group (every region point lies in its centre's
+            // sphere), bounds widened by s against the rounding of the cell mapping
+            const float hc = p.h_cell;
+            const float ylo = cy == 0 ? -INFINITY : fmaf((float)cy, hc, p.oy);
+            const float yhi = cy == p.dimy - 1 ? INFINITY : fmaf((float)(cy + 1), hc, p.oy);
+            const float zlo = cz == 0 ? -INFINITY : fmaf((float)cz, hc, p.oz);
+            const float zhi = cz == p.dimz - 1 ? INFINITY : fmaf((float)(cz + 1), hc, p.oz);
+            const float R2 = p.R_up * p.R_up * 1.000001f;
+            int xl = cx1 + 1, xh = cx0 - 1;
+            for (int g = 0; g < G; ++g) {
+              if (sM[g] < 0) continue;
+              const float4 P4 = sP[g];
+              const float s = 4e-6f * (fabsf(P4.y) + fabsf(P4.z) + fabsf(p.oy) + fabsf(p.oz) + 2.f * hc) + 1e-30f;
+              const float dy = fmaxf(0.f, fmaxf(ylo - P4.y, P4.y - yhi) - s);
+              const float dz = fmaxf(0.f, fmaxf(zlo - P4.z, P4.z - zhi) - s);
+              const float d2 = fmaf(dy, dy, dz * dz) * 0.999999f;
+              if (!(d2 <= R2)) continue;
+              const float hx = sqrtf(R2 - d2) * 1.000001f + s;
+              xl = min(xl, cell_coord(__fsub_rd(P4.x, hx), p.ox, p.inv_h, p.dimx));
+              xh = max(xh, cell_coord(__fadd_ru(P4.x, hx), p.ox, p.inv_h, p.dimx));
+            }
+            xl = max(xl, cx0);
+            xh = min(xh, cx1);
+            if (xl <= xh) {
+              start = p.cell_start[base + xl];
+              len = p.cell_start[base + xh + 1] - start;
+            }
           }
           // block exclusive scan of len over NT threads
           int v = len;
