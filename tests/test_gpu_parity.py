@@ -386,12 +386,13 @@ def _full(spin, torch, cfg_id, mode, prune, n_check, W=None, sched="STATIC"):
 
 @pytest.mark.parametrize("mode", ["nearest", "bilinear"])
 def test_config2_full_sampled(spin, torch, mode):
-    _full(spin, torch, 2, mode, "brute", 40, sched="GSS")
+    """C2 in full in bench.py's launch configuration (SS, unit G, default P and flags)."""
+    _full(spin, torch, 2, mode, "brute", 40, sched="SS")
 
 
 def test_config3_full_sampled(spin, torch):
     for mode in ("bilinear", "nearest"):
-        _full(spin, torch, 3, mode, "cells", 30, sched="FAC")
+        _full(spin, torch, 3, mode, "cells", 30, sched="SS")
 
 
 def test_config4_full_sampled(spin, torch):
@@ -415,7 +416,7 @@ def test_config6_paper_shape_sampled(spin, torch):
 
 @pytest.mark.parametrize("W", [8, 24])
 def test_config5_full_sampled(spin, torch, W):
-    _full(spin, torch, 5, "nearest", "cells", 20, W=W, sched="GSS")
+    _full(spin, torch, 5, "nearest", "cells", 20, W=W, sched="SS")
 
 
 def test_bilinear_fixed_point_carries(spin, torch):
