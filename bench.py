@@ -42,6 +42,10 @@ def parse(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="spin", choices=["spin", "reference"])
     ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--dealer", choices=("local", "shared"), default="local",
+                    help="shared: ONE schedule of the configured centres dealt to every GPU's "
+                         "CTAs from one counter on GPU 0 (CUDA IPC / NVLink peer atomics; the "
+                         "paper's master-worker across nodes); implies --scaling strong")
     ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
                     help="weak: every GPU runs the full workload (default); strong: the "
                          "configured centres are split across GPUs")
@@ -76,6 +80,17 @@ def dist_init(backend):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group(backend=backend, rank=rank, world_size=world)
     return dist
+
+
+def share_dealer(spin, rank: int, world: int):
+    """A shared dealer counter on rank 0, mapped by every other rank through its CUDA IPC
+    handle (broadcast over torch.distributed)."""
+    import torch.distributed as dist
+    d = spin.Dealer() if rank == 0 else None
+    obj = [d.ipc_handle() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(obj, src=0)
+    return d if rank == 0 else spin.Dealer.open(obj[0])
 
 
 def allreduce_sum(x: float, device=None) -> float:
@@ -263,8 +278,11 @@ def run_spin(args):
         cfg["W"] = args.W
     W, b, c, mode, prune = cfg["W"], cfg["b"], cfg["cos_As"], args.mode or cfg["mode"], cfg["prune"]
     P, Nn = clouds.make_cloud(args.config)
+    if args.dealer == "shared":
+        args.scaling = "strong"
     strong = args.scaling == "strong"
-    cen = rank_centres(args.config, cfg["N"], rank, world, strong)
+    # with a shared dealer every rank holds every centre; the dealer splits the work
+    cen = rank_centres(args.config, cfg["N"], rank, world, strong and args.dealer == "local")
     M, N = len(cen), len(P)
     stream = torch.cuda.current_stream()
     eng = spin.SpinEngine(torch.from_numpy(P).to(dev), torch.from_numpy(Nn).to(dev))
@@ -272,13 +290,35 @@ def run_spin(args):
     out = torch.empty((M, W, W), dtype=torch.float32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # > 126 MB L2
     flags = {"auto": 0, "first": spin.F_SUPPORT_FIRST, "last": spin.F_SUPPORT_LAST}[args.support]
+    dealer = None
+    if args.dealer == "shared":
+        dealer = share_dealer(spin, rank, world)
+        grid = args.P or spin.default_P(W, mode, prune)
+        shared_kw = dict(P=grid * world, grid=grid, cta_offset=rank * grid, shared_counter=dealer.ptr)
+
+    def prestep():
+        """Shared dealer: GPU 0 zeroes the counter, then every rank passes a barrier (the
+        counter must be reset before any rank deals from it)."""
+        if dealer is not None:
+            if rank == 0:
+                dealer.reset(stream)
+            torch.cuda.synchronize()
+            barrier()
+
+    def gen(*a, pre=True, **k):
+        if dealer is not None:
+            if pre:
+                prestep()
+            k = dict(k, **shared_kw)
+        return eng.generate(*a, **k)
+
     kw = dict(schedule=args.schedule, mode=mode, prune=prune, P=args.P, unit=args.unit, out=out,
               flags=flags)
 
     # warm-up (the first call also builds the CELLS grid, which is then cached)
-    _, st0 = eng.generate(d_cen, W, b, c, stats=True, **kw)
+    _, st0 = gen(d_cen, W, b, c, stats=True, **kw)
     for _ in range(max(0, args.warmup - 1)):
-        eng.generate(d_cen, W, b, c, **kw)
+        gen(d_cen, W, b, c, **kw)
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, L2 flushed before each, events on the launching stream
@@ -290,8 +330,9 @@ def run_spin(args):
     torch.cuda.synchronize()
     for e0, e1 in evs:
         flush.zero_()
+        prestep()                       # shared dealer only: reset + barrier, outside the events
         e0.record(stream)
-        eng.generate(d_cen, W, b, c, **kw)
+        gen(d_cen, W, b, c, pre=False, **kw)
         e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -304,7 +345,7 @@ def run_spin(args):
     kern_ms = []
     for _ in range(3):
         flush.zero_()
-        _, st = eng.generate(d_cen, W, b, c, stats=True, **kw)
+        _, st = gen(d_cen, W, b, c, stats=True, **kw)
         kern_ms.append(st["elapsed_ms"])
     kern = statistics.median(kern_ms)
     pairs_step = st0["pairs_visited"]
@@ -313,22 +354,23 @@ def run_spin(args):
     # secondary (same run): the support test on every pair in the hot loop, the paper's
     # order (P:166 before P:169-171) -- identical images; reported beside the main line
     alt = None
-    pairs_all_est = allreduce_sum(pairs_step, dev)
+    pairs_all_est = allreduce_sum(pairs_step, dev) if dealer is None else pairs_step
     if args.support == "auto" and cfg["cos_As"] > -math.inf:
         akw = dict(kw, flags=spin.F_SUPPORT_FIRST)
         for _ in range(2):
-            eng.generate(d_cen, W, b, c, **akw)
+            gen(d_cen, W, b, c, **akw)
         torch.cuda.synchronize()
         aev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
         for e0, e1 in aev:
             flush.zero_()
+            prestep()
             e0.record(stream)
-            eng.generate(d_cen, W, b, c, **akw)
+            gen(d_cen, W, b, c, pre=False, **akw)
             e1.record(stream)
         torch.cuda.synchronize()
         a_ms = allreduce_max(sum(e0.elapsed_time(e1) for e0, e1 in aev), dev) / args.steps
-        _, ast = eng.generate(d_cen, W, b, c, stats=True, **akw)
+        _, ast = gen(d_cen, W, b, c, stats=True, **akw)
         alt = {"flag": "SPIN_F_SUPPORT_FIRST", "value": pairs_all_est / (a_ms * 1e-3),
                "unit": UNIT, "ms_per_step": a_ms, "kernel_ms": ast["elapsed_ms"],
                "fp32_frac_algorithmic_20flop": pairs_step * FLOP_PER_PAIR / (ast["elapsed_ms"] * 1e-3)
@@ -336,8 +378,11 @@ def run_spin(args):
                "pairs_candidate": ast["pairs_candidate"],
                "note": "support test n.n_x >= cos_As on every pair in the hot loop; images identical"}
 
-    pairs_all = allreduce_sum(pairs_step, dev)       # = pairs_step * world for weak scaling
-    M_all = int(allreduce_sum(M, dev))
+    if dealer is None:
+        pairs_all = allreduce_sum(pairs_step, dev)   # = pairs_step * world for weak scaling
+        M_all = int(allreduce_sum(M, dev))
+    else:
+        pairs_all, M_all = pairs_step, M             # one schedule of M images over all ranks
     value = pairs_all * args.steps / (total_ms * 1e-3)
     images_per_s = M_all * args.steps / (total_ms * 1e-3)
 
@@ -381,8 +426,12 @@ def run_spin(args):
                                     "last": "candidates only"}[args.support],
                    "tiles_support_hot": st0["tiles_support_hot"],
                    "n_chunks": st0["n_chunks"], "l2": "flushed (256 MB write) before every step",
-                   "parallelism": (f"replicas x{world}" if args.scaling == "weak" else f"centre shards x{world}")
-                                  + " (independent images, no collective)"},
+                   "parallelism": (f"replicas x{world} (independent images, no collective)"
+                                   if args.scaling == "weak" else
+                                   f"centre shards x{world} (independent images, no collective)"
+                                   if dealer is None else
+                                   f"one schedule dealt to x{world} GPUs from a shared counter "
+                                   "(CUDA IPC / peer atomics; no data collective)")},
         "images_per_s": images_per_s,
         "fp32_peak_frac": value / world * FLOP_PER_PAIR / (FP32_PEAK_TFLOPS * 1e12),
         "roofline": {"bound": "alu", "achieved": achieved_tflops, "peak": FP32_PEAK_TFLOPS,

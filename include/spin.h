@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SPIN_ABI_VERSION 3
+#define SPIN_ABI_VERSION 4
 
 typedef struct spin_ctx* spin_handle;
 typedef struct CUstream_st* spin_stream; /* identical to cudaStream_t */
@@ -90,6 +90,17 @@ typedef struct {
                             CTA idles (slowdown - 1) x the group's measured compute time  */
   int32_t slow_first;    /* dynamic schedules: the fast CTAs wait until every slow CTA has
                             issued its first request (the machine-file order) */
+  /* One schedule across several devices (the paper's master-worker
+   * over many nodes): every device runs spin_generate on the SAME centres with
+   * the same P (the total worker count) and one shared dealer counter.  Each device
+   * writes only the images of the chunks its CTAs took; the rest of its d_out is left
+   * untouched (zero it and sum, or gather, across devices). */
+  int32_t grid;          /* CTAs launched on this device; 0 -> P                          */
+  int32_t cta_offset;    /* global worker index of this device's CTA 0 (STATIC: CTA c takes
+                            block c); cta_offset + grid <= P                              */
+  uint32_t* d_counter;   /* shared dealer: a u32 in device, peer or IPC-mapped memory that
+                            the caller zeroes before the call on every device; NULL -> the
+                            handle's own counter (reset by every call)                     */
 } spin_chunk_params;
 
 /* Optional per-call statistics.  Passing non-NULL makes spin_generate synchronise
@@ -102,7 +113,7 @@ typedef struct {
   int64_t pairs_accepted;   /* pairs that contributed (NEAREST: sum of all counts)         */
   int64_t fp64_fallbacks;   /* decisions the fp32 stage could not certify                  */
   int64_t exact_fallbacks;  /* decisions the fp64 stage could not certify (exact stage)    */
-  int32_t P;                /* resident CTAs used                                          */
+  int32_t P;                /* CTAs launched on this device (the grid)                      */
   int32_t G;                /* images per CTA group                                        */
   int32_t n_units;          /* scheduling units                                            */
   int32_t n_chunks;         /* chunks in the schedule                                      */
@@ -176,7 +187,8 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
  * of >= 8 MB of images the D2H copy is pipelined with the kernel: the kernel counts
  * finished images per output segment (16 segments) and a handle-owned copy stream
  * waits on each counter (cuStreamWaitValue32, resolved through
- * cudaGetDriverEntryPoint) before copying that segment.
+ * cudaGetDriverEntryPoint) before copying that segment.  A shared dealer
+ * (cp->d_counter) is rejected with SPIN_E_INVAL: multi-device runs use spin_generate.
  */
 spin_status spin_generate_host(spin_handle h, const int32_t* h_centre_idx, int64_t M,
                                int32_t W, double b, double cos_As, spin_schedule sched,
@@ -208,6 +220,21 @@ int32_t spin_default_P(int32_t W, spin_mode mode, spin_prune prune);
 void spin_destroy(spin_handle h);
 const char* spin_last_error(void);
 int32_t spin_abi_version(void);
+
+/* ---- Shared dealer across devices / processes: the paper's
+ * master as one u32 counter that every device's CTAs increment with
+ * atomicAdd, over NVLink peer memory or CUDA IPC.  The counter is a plain cudaMalloc
+ * of its own (so its IPC handle maps exactly this allocation). */
+spin_status spin_dealer_alloc(uint32_t** d_counter);          /* on the current device, zeroed */
+/* the 64-byte CUDA IPC handle of a counter from spin_dealer_alloc, for another process */
+spin_status spin_dealer_ipc_handle(const uint32_t* d_counter, unsigned char handle[64]);
+/* map another process's counter into this one (peer access enabled lazily) */
+spin_status spin_dealer_ipc_open(const unsigned char handle[64], uint32_t** d_counter);
+/* zero the counter on `stream` (before every schedule; order it before every device's
+ * spin_generate, e.g. with a barrier after a synchronize) */
+spin_status spin_dealer_reset(uint32_t* d_counter, spin_stream stream);
+/* release: opened != 0 unmaps an IPC mapping, else frees the allocation */
+spin_status spin_dealer_free(uint32_t* d_counter, int32_t opened);
 
 /* ---- Host-side ingestion: the paper's OP = read3DPoints(OF)
  * (Alg. 3).  Pure host code, no device and no handle needed; errors set

@@ -446,7 +446,8 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
     return fail(SPIN_E_INVAL, "cos_As=%g must be in [-1, 1] or -inf", cos_As);
   spin_chunk_params cpar{};
   if (cp) cpar = *cp;
-  if (cpar.P < 0 || cpar.unit < 0 || cpar.gss_min_chunk < 0 || cpar.fac_divisor < 0)
+  if (cpar.P < 0 || cpar.unit < 0 || cpar.gss_min_chunk < 0 || cpar.fac_divisor < 0 ||
+      cpar.grid < 0 || cpar.cta_offset < 0)
     return fail(SPIN_E_INVAL, "negative chunk parameter");
   if (cpar.flags & ~0x3fu) return fail(SPIN_E_INVAL, "unknown flag bits 0x%x", cpar.flags);
   if (cpar.slow_ctas < 0 || !(cpar.slowdown == 0.0f || (cpar.slowdown >= 1.0f && cpar.slowdown <= 1e6f)))
@@ -466,8 +467,11 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   const LaunchCfg lc = choose_launch(W, (int)mode, (int)prune);
   const int occ = occupancy_blocks(lc, W, (int)mode, (int)prune);
   if (occ <= 0) return fail(SPIN_E_CUDA, "kernel does not fit on the device (smem %zu)", lc.smem);
-  const int P = cpar.P > 0 ? cpar.P : occ * h->sms;
+  const int P = cpar.P > 0 ? cpar.P : occ * h->sms;     // workers of the schedule
   if (P > 1 << 20) return fail(SPIN_E_INVAL, "P=%d too large", P);
+  const int grid = cpar.grid > 0 ? cpar.grid : P;       // CTAs on this device
+  if ((int64_t)cpar.cta_offset + grid > P)
+    return fail(SPIN_E_INVAL, "cta_offset %d + grid %d exceeds P %d", cpar.cta_offset, grid, P);
   const int unit = cpar.unit > 0 ? cpar.unit : lc.G;
   const int64_t n_units = (M + unit - 1) / unit;
   const int gmin = cpar.gss_min_chunk ? cpar.gss_min_chunk : 1;
@@ -483,20 +487,20 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
     std::copy(key, key + 6, h->bounds_key);
   }
   const int n_chunks = (int)h->bounds_h.size() - 1;
-  if (h->cta_cap < P) {
+  if (h->cta_cap < grid) {
     if (h->cta_t0) cudaFree(h->cta_t0);
     if (h->cta_t1) cudaFree(h->cta_t1);
     if (h->cta_units) cudaFree(h->cta_units);
     h->cta_t0 = h->cta_t1 = nullptr;
     h->cta_units = nullptr;
     h->cta_cap = 0;
-    if (cudaMalloc((void**)&h->cta_t0, P * sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMalloc((void**)&h->cta_t1, P * sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMalloc((void**)&h->cta_units, P * sizeof(int32_t)) != cudaSuccess) {
+    if (cudaMalloc((void**)&h->cta_t0, grid * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc((void**)&h->cta_t1, grid * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc((void**)&h->cta_units, grid * sizeof(int32_t)) != cudaSuccess) {
       cudaGetLastError();
       return fail(SPIN_E_NOMEM, "per-CTA instrumentation allocation failed");
     }
-    h->cta_cap = P;
+    h->cta_cap = grid;
   }
 
   // ---- a2: region constants and certified thresholds
@@ -599,18 +603,19 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   p.n_chunks = n_chunks;
   p.unit_images = unit;
   p.is_static = sched == SPIN_STATIC ? 1 : 0;
-  p.slow_ctas = cpar.slowdown > 1.0f ? std::min(cpar.slow_ctas, P) : 0;
+  p.cta_offset = cpar.cta_offset;
+  p.slow_ctas = cpar.slowdown > 1.0f ? std::min(cpar.slow_ctas, grid) : 0;
   p.slowdown = cpar.slowdown > 1.0f ? cpar.slowdown : 1.0f;
   // (the wait needs every slow CTA resident: only for a persistent launch)
-  p.slow_first = (cpar.slow_first && !p.is_static && P <= occ * h->sms) ? 1 : 0;
-  p.counter = h->counter;
+  p.slow_first = (cpar.slow_first && !p.is_static && grid <= occ * h->sms && !cpar.d_counter) ? 1 : 0;
+  p.counter = cpar.d_counter ? cpar.d_counter : h->counter;
   p.stats = h->stats;
   p.cta_t0 = h->cta_t0;
   p.cta_t1 = h->cta_t1;
   p.cta_units = h->cta_units;
   p.err_flags = h->err;
   if (mode == SPIN_BILINEAR) {
-    const int64_t need = (int64_t)P * lc.G * ((W * W + 1) / 2);
+    const int64_t need = (int64_t)grid * lc.G * ((W * W + 1) / 2);
     if (need > h->hi_cap) {
       spin_status st = ensure(h->hi_scratch, h->hi_cap, need, "carry scratch");
       if (st != SPIN_OK) return st;
@@ -672,10 +677,10 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   }
 
   // ---- a6-a13: the persistent launch
-  CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned), s), "memset");
+  if (!cpar.d_counter) CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned), s), "memset");
   CK(cudaMemsetAsync(h->stats, 0, ST_NSLOTS * sizeof(unsigned long long), s), "memset");
   CK(cudaEventRecord(h->ev0, s), "event");
-  CK(launch_spin(lc, (int)mode, (int)prune, P, p, s), "spin kernel launch");
+  CK(launch_spin(lc, (int)mode, (int)prune, grid, p, s), "spin kernel launch");
   CK(cudaEventRecord(h->ev1, s), "event");
   CK(cudaMemcpyAsync(h->h_err, h->err, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "err readback");
   CK(cudaMemsetAsync(h->err, 0, 2 * sizeof(int32_t), s), "memset");
@@ -700,11 +705,11 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
     stats->fp64_fallbacks = (int64_t)sv[ST_F64];
     stats->exact_fallbacks = (int64_t)sv[ST_EXACT];
     stats->tiles_support_hot = (int64_t)sv[ST_SUPHOT];
-    stats->P = P;
+    stats->P = grid;
     stats->G = lc.G;
     stats->n_units = (int32_t)n_units;
     stats->n_chunks = n_chunks;
-    const int nc = std::min(P, stats->cta_capacity);
+    const int nc = std::min(grid, stats->cta_capacity);
     if (nc > 0) {
       if (stats->h_cta_start_ns) CK(cudaMemcpy(stats->h_cta_start_ns, h->cta_t0, nc * 8, cudaMemcpyDeviceToHost), "cta");
       if (stats->h_cta_end_ns) CK(cudaMemcpy(stats->h_cta_end_ns, h->cta_t1, nc * 8, cudaMemcpyDeviceToHost), "cta");
@@ -717,6 +722,46 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   return SPIN_OK;
 }
 
+spin_status spin_dealer_alloc(uint32_t** d_counter) {
+  if (!d_counter) return fail(SPIN_E_INVAL, "null d_counter");
+  *d_counter = nullptr;
+  CK(cudaMalloc((void**)d_counter, 256), "dealer alloc");
+  CK(cudaMemset(*d_counter, 0, 256), "dealer zero");
+  return SPIN_OK;
+}
+
+spin_status spin_dealer_ipc_handle(const uint32_t* d_counter, unsigned char handle[64]) {
+  if (!d_counter || !handle) return fail(SPIN_E_INVAL, "null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handle size");
+  cudaIpcMemHandle_t hd;
+  CK(cudaIpcGetMemHandle(&hd, (void*)d_counter), "dealer ipc handle");
+  std::memcpy(handle, &hd, 64);
+  return SPIN_OK;
+}
+
+spin_status spin_dealer_ipc_open(const unsigned char handle[64], uint32_t** d_counter) {
+  if (!d_counter || !handle) return fail(SPIN_E_INVAL, "null argument");
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle, 64);
+  void* p = nullptr;
+  CK(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess), "dealer ipc open");
+  *d_counter = (uint32_t*)p;
+  return SPIN_OK;
+}
+
+spin_status spin_dealer_reset(uint32_t* d_counter, spin_stream stream) {
+  if (!d_counter) return fail(SPIN_E_INVAL, "null d_counter");
+  CK(cudaMemsetAsync(d_counter, 0, sizeof(uint32_t), (cudaStream_t)stream), "dealer reset");
+  return SPIN_OK;
+}
+
+spin_status spin_dealer_free(uint32_t* d_counter, int32_t opened) {
+  if (!d_counter) return SPIN_OK;
+  if (opened) CK(cudaIpcCloseMemHandle(d_counter), "dealer ipc close");
+  else CK(cudaFree(d_counter), "dealer free");
+  return SPIN_OK;
+}
+
 spin_status spin_generate_host(spin_handle h, const int32_t* h_centre_idx, int64_t M, int32_t W,
                                double b, double cos_As, spin_schedule sched,
                                const spin_chunk_params* cp, spin_mode mode, spin_prune prune,
@@ -726,6 +771,8 @@ spin_status spin_generate_host(spin_handle h, const int32_t* h_centre_idx, int64
   if (M == 0) return spin_generate(h, nullptr, 0, W, b, cos_As, sched, cp, mode, prune, nullptr, stats, stream);
   if (!h_centre_idx || !h_out) return fail(SPIN_E_INVAL, "null host buffer");
   if (W < 1 || W > 64) return fail(SPIN_E_INVAL, "W=%d outside [1, 64]", W);
+  if (cp && cp->d_counter)
+    return fail(SPIN_E_INVAL, "a shared dealer (d_counter) needs device buffers: use spin_generate");
   cudaStream_t s = (cudaStream_t)stream;
   spin_status st;
   if ((st = ensure(h->cidx, h->cidx_cap, M, "centre scratch")) != SPIN_OK) return st;

@@ -42,6 +42,7 @@ struct KParams {
   double Eq_hot;             // CELLS hot loop: bound on |q''_fp32 - q''| (added to Qmax - C)
   float c_test, h_test;      // hot loop: s >= c_test (support), CELLS |beta''| <= h_test
   int32_t has_support;
+  int32_t cta_offset;        // global worker index of CTA 0 (STATIC block assignment)
   int32_t slow_ctas;         // heterogeneity emulation: CTAs below this index are slow
   float slowdown;            // their per-group time multiplier (>= 1)
   int32_t slow_first;        // fast CTAs wait for the slow CTAs' first requests

@@ -408,7 +408,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         // heterogeneity emulation: the slow workers request first
         while (*reinterpret_cast<volatile unsigned*>(p.counter) < (unsigned)p.slow_ctas) __nanosleep(256);
       }
-      s_chunk = p.is_static ? (first ? (int)blockIdx.x : p.n_chunks) : (int)atomicAdd(p.counter, 1u);
+      s_chunk = p.is_static ? (first ? p.cta_offset + (int)blockIdx.x : p.n_chunks)
+                            : (int)atomicAdd(p.counter, 1u);
     }
     __syncthreads();
     const int u = s_chunk;

@@ -33,7 +33,8 @@ STATUS = {0: "SPIN_OK", 1: "SPIN_E_INVAL", 2: "SPIN_E_RANGE", 3: "SPIN_E_INPUT",
 class ChunkParams(C.Structure):
     _fields_ = [("P", C.c_int32), ("unit", C.c_int32), ("gss_min_chunk", C.c_int32),
                 ("fac_divisor", C.c_int32), ("flags", C.c_uint32),
-                ("slow_ctas", C.c_int32), ("slowdown", C.c_float), ("slow_first", C.c_int32)]
+                ("slow_ctas", C.c_int32), ("slowdown", C.c_float), ("slow_first", C.c_int32),
+                ("grid", C.c_int32), ("cta_offset", C.c_int32), ("d_counter", C.c_void_p)]
 
 
 class Stats(C.Structure):
@@ -74,10 +75,54 @@ _lib.spin_vertex_normals.argtypes = [_vp, C.c_int64, _vp, C.c_int64, _vp]
 for _f in ("spin_read_xyzn", "spin_read_off", "spin_vertex_normals"):
     getattr(_lib, _f).restype = C.c_int
 
+_lib.spin_dealer_alloc.argtypes = [C.POINTER(_vp)]
+_lib.spin_dealer_ipc_handle.argtypes = [_vp, C.c_char_p]
+_lib.spin_dealer_ipc_open.argtypes = [C.c_char_p, C.POINTER(_vp)]
+_lib.spin_dealer_reset.argtypes = [_vp, _vp]
+_lib.spin_dealer_free.argtypes = [_vp, C.c_int32]
+for _f in ("spin_dealer_alloc", "spin_dealer_ipc_handle", "spin_dealer_ipc_open",
+           "spin_dealer_reset", "spin_dealer_free"):
+    getattr(_lib, _f).restype = C.c_int
+
+
+class Dealer:
+    """A shared dealer counter (spin_dealer_*): `Dealer()` allocates one on the current
+    device; `Dealer.open(handle)` maps another process's through CUDA IPC.  `.ptr` is the
+    device address to pass as generate(shared_counter=...)."""
+
+    def __init__(self, _ptr=None, _opened=False):
+        if _ptr is None:
+            p = _vp()
+            _check(_lib.spin_dealer_alloc(C.byref(p)))
+            _ptr = p.value
+        self.ptr, self._opened = _ptr, _opened
+
+    @classmethod
+    def open(cls, handle: bytes):
+        p = _vp()
+        _check(_lib.spin_dealer_ipc_open(C.create_string_buffer(bytes(handle), 64), C.byref(p)))
+        return cls(p.value, True)
+
+    def ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        _check(_lib.spin_dealer_ipc_handle(self.ptr, buf))
+        return buf.raw
+
+    def reset(self, stream=None):
+        _check(_lib.spin_dealer_reset(self.ptr, _stream(stream)))
+
+    def close(self):
+        if self.ptr:
+            _check(_lib.spin_dealer_free(self.ptr, int(self._opened)))
+            self.ptr = None
+
+
 EXPORTS = ["spin_create", "spin_load_cloud", "spin_generate", "spin_generate_host",
            "spin_chunk_sequence", "spin_region_radius", "spin_cos_from_degrees", "spin_default_P",
            "spin_destroy", "spin_last_error", "spin_abi_version",
-           "spin_read_xyzn", "spin_read_off", "spin_vertex_normals"]
+           "spin_read_xyzn", "spin_read_off", "spin_vertex_normals",
+           "spin_dealer_alloc", "spin_dealer_ipc_handle", "spin_dealer_ipc_open",
+           "spin_dealer_reset", "spin_dealer_free"]
 
 
 def read_xyzn(path):
@@ -217,21 +262,26 @@ class SpinEngine:
 
     @staticmethod
     def _params(P, unit, gss_min_chunk, fac_divisor, flags, slow_ctas=0, slowdown=0.0,
-                slow_first=False):
+                slow_first=False, grid=0, cta_offset=0, d_counter=None):
         return ChunkParams(int(P), int(unit), int(gss_min_chunk), int(fac_divisor), int(flags),
-                           int(slow_ctas), float(slowdown), int(bool(slow_first)))
+                           int(slow_ctas), float(slowdown), int(bool(slow_first)), int(grid),
+                           int(cta_offset), d_counter)
 
     def generate(self, centre_idx, W, b, cos_As, schedule="STATIC", mode="nearest", prune="brute",
                  P=0, unit=0, gss_min_chunk=0, fac_divisor=0, flags=0, out=None, stats=False,
-                 cta_capacity=0, stream=None, slow_ctas=0, slowdown=0.0, slow_first=False):
+                 cta_capacity=0, stream=None, slow_ctas=0, slowdown=0.0, slow_first=False,
+                 grid=0, cta_offset=0, shared_counter=None):
         """Images for device int32 centre_idx [M] into a device fp32 [M, W, W] tensor.
-        slow_ctas / slowdown / slow_first: heterogeneous-worker emulation (timing only)."""
+        slow_ctas / slowdown / slow_first: heterogeneous-worker emulation (timing only).
+        grid / cta_offset / shared_counter (device address of a zeroed u32): one schedule
+        dealt across devices; only this device's chunks are written to `out`."""
         import torch
         M = int(centre_idx.shape[0])
         assert centre_idx.dtype == torch.int32 and centre_idx.is_cuda
         if out is None:
             out = torch.empty((M, W, W), dtype=torch.float32, device=centre_idx.device)
-        cp = self._params(P, unit, gss_min_chunk, fac_divisor, flags, slow_ctas, slowdown, slow_first)
+        cp = self._params(P, unit, gss_min_chunk, fac_divisor, flags, slow_ctas, slowdown, slow_first,
+                          grid, cta_offset, shared_counter)
         st = Stats()
         t0 = t1 = un = None
         if stats and cta_capacity:

@@ -1,0 +1,82 @@
+"""GPU test of the shared dealer: one schedule dealt to two
+processes through a counter mapped with CUDA IPC.  Run on one GPU (both processes share
+it; neither waits on the other: each CTA only grabs chunks until the table is
+exhausted), it exercises the same dealing and partial-output contract a multi-GPU run
+uses.  The partial images of the two processes must sum to the single-process images
+(NEAREST counts: exact), every chunk dealt exactly once."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SCHEDS = ("SS", "STATIC", "GSS", "FAC")
+
+
+def _worker(rank, handle, barrier, q):
+    sys.path.insert(0, ROOT)
+    import torch
+    from paper_1811_00901_b200 import spin
+    from synth import clouds
+    torch.cuda.set_device(0)
+    P, Nn = clouds.bumpy_sphere(20000, 41)
+    cen = torch.arange(20000, dtype=torch.int32, device="cuda")
+    eng = spin.SpinEngine(torch.from_numpy(P).cuda(), torch.from_numpy(Nn).cuda())
+    dealer = spin.Dealer.open(handle)
+    res = {}
+    for sched in SCHEDS:
+        barrier.wait()                      # the parent has reset the counter
+        out = torch.zeros((20000, 16, 16), dtype=torch.float32, device="cuda")
+        _, st = eng.generate(cen, 16, 0.02, 0.5, schedule=sched, mode="nearest", out=out,
+                             P=2 * 148, grid=148, cta_offset=rank * 148,
+                             shared_counter=dealer.ptr, stats=True, cta_capacity=148)
+        torch.cuda.synchronize()
+        res[sched] = (out.cpu().numpy(), int(st["cta_units"].sum()))
+        barrier.wait()
+    dealer.close()
+    eng.close()
+    q.put((rank, res))
+
+
+def test_shared_dealer_two_processes():
+    import torch
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    sys.path.insert(0, ROOT)
+    from paper_1811_00901_b200 import spin
+    from synth import clouds
+    P, Nn = clouds.bumpy_sphere(20000, 41)
+    eng = spin.SpinEngine(torch.from_numpy(P).cuda(), torch.from_numpy(Nn).cuda())
+    ref = eng.generate(torch.arange(20000, dtype=torch.int32, device="cuda"), 16, 0.02, 0.5,
+                       schedule="SS", mode="nearest").cpu().numpy()
+    n_units = -(-20000 // 64)
+    dealer = spin.Dealer()
+    ctx = mp.get_context("spawn")
+    barrier, q = ctx.Barrier(3), ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, dealer.ipc_handle(), barrier, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    try:
+        for _ in SCHEDS:
+            dealer.reset()
+            torch.cuda.synchronize()
+            barrier.wait()                  # workers start this schedule
+            barrier.wait()                  # workers done
+        res = dict(q.get(timeout=300) for _ in range(2))
+    finally:
+        for p in procs:
+            p.join(120)
+    assert all(p.exitcode == 0 for p in procs)
+    for sched in SCHEDS:
+        a, ua = res[0][sched]
+        b, ub = res[1][sched]
+        np.testing.assert_array_equal(a + b, ref, err_msg=sched)
+        assert ua + ub == n_units, (sched, ua, ub)
+        # disjoint: an image written by both would double its counts
+        assert not np.any((a.reshape(20000, -1).sum(1) > 0) & (b.reshape(20000, -1).sum(1) > 0))
+    dealer.close()
+    eng.close()

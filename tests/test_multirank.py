@@ -33,7 +33,23 @@ def _worker(rank, world, port, q):
     bench.barrier()
     cen = bench.rank_centres(3, 1_000_000, rank)[:1000]
     strong = bench.rank_centres(1, 2000, rank, world, strong=True)
-    q.put((rank, t, cen.tolist(), s, strong.tolist()))
+
+    class FakeDealer:            # the IPC calls need a GPU; the handle exchange does not
+        def __init__(self, h=b"H" * 64):
+            self.h = h
+
+        def ipc_handle(self):
+            return self.h
+
+        @classmethod
+        def open(cls, h):
+            return cls(b"opened:" + h[:8])
+
+    class FakeSpin:
+        Dealer = FakeDealer
+
+    d = bench.share_dealer(FakeSpin, rank, world)
+    q.put((rank, t, cen.tolist(), s, strong.tolist(), d.h))
     dist.destroy_process_group()
 
 
@@ -56,6 +72,8 @@ def test_gloo_two_ranks_max_and_distinct_shards():
     # strong scaling: the configured centres split into disjoint contiguous shards
     s0, s1 = res[0][4], res[1][4]
     assert s0 + s1 == list(range(2000)) and len(s0) == len(s1) == 1000
+    # shared dealer: rank 0 owns the counter, rank 1 maps rank 0's handle
+    assert res[0][5] == b"H" * 64 and res[1][5] == b"opened:HHHHHHHH"
 
 
 def test_reference_arm_json_line():
