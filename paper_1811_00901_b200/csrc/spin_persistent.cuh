@@ -38,6 +38,9 @@
 #ifndef SPIN_APL_BRUTE
 #define SPIN_APL_BRUTE 1      // BRUTE candidates per lane per accept pass
 #endif
+#ifndef SPIN_APL_BRUTE512
+#define SPIN_APL_BRUTE512 1   // the same for the 512-thread (W = 32) variant
+#endif
 #include "spin_exact.cuh"
 
 namespace spin {
@@ -536,7 +539,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       };
       // CELLS (dense, latency-bound) takes two candidates per lane per pass so that the
       // two independent decisions interleave; BRUTE keeps one (fewer live registers).
-      constexpr int APL = PRUNE == 1 ? 2 : SPIN_APL_BRUTE;
+      constexpr int APL = PRUNE == 1 ? 2 : (NT == 512 ? SPIN_APL_BRUTE512 : SPIN_APL_BRUTE);
       auto process_pair = [&](unsigned e0, bool v0, unsigned e1, bool v1) {
         float4 P0, N0, X0, NX0, P1, N1, X1, NX1;
         load_entry(e0, P0, N0, X0, NX0);
