@@ -660,6 +660,19 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
                              h->inv_h, h->dx, h->dy, h->dz, shift, bits, h->ckeys, h->counts,
                              h->cstarts, h->cursor, h->scan_tmp, h->order, s),
          "centre order");
+      if (cpar.d_counter) {
+        // a shared dealer needs the SAME chunk -> images map on every device; the device
+        // scatter orders centres within a bucket by atomic arrival, so re-derive the
+        // order as a stable counting sort of the same keys on the host (M ints each way)
+        std::vector<int32_t> keys((size_t)M), ord((size_t)M), cnt((size_t)nb + 1, 0);
+        CK(cudaMemcpyAsync(keys.data(), h->ckeys, M * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "keys");
+        CK(cudaStreamSynchronize(s), "keys");
+        for (int64_t m = 0; m < M; ++m) ++cnt[(size_t)keys[m] + 1];
+        for (int64_t k = 0; k < nb; ++k) cnt[(size_t)k + 1] += cnt[(size_t)k];
+        for (int64_t m = 0; m < M; ++m) ord[(size_t)cnt[(size_t)keys[m]]++] = (int32_t)m;
+        CK(cudaMemcpyAsync(h->order, ord.data(), M * sizeof(int32_t), cudaMemcpyHostToDevice, s), "order");
+        CK(cudaStreamSynchronize(s), "order");   // ord is a temporary
+      }
       p.order = h->order;
     }
   }

@@ -14,6 +14,7 @@ pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SCHEDS = ("SS", "STATIC", "GSS", "FAC")
+PRUNES = ("brute", "cells")
 
 
 def _worker(rank, handle, barrier, q):
@@ -27,15 +28,16 @@ def _worker(rank, handle, barrier, q):
     eng = spin.SpinEngine(torch.from_numpy(P).cuda(), torch.from_numpy(Nn).cuda())
     dealer = spin.Dealer.open(handle)
     res = {}
-    for sched in SCHEDS:
-        barrier.wait()                      # the parent has reset the counter
-        out = torch.zeros((20000, 16, 16), dtype=torch.float32, device="cuda")
-        _, st = eng.generate(cen, 16, 0.02, 0.5, schedule=sched, mode="nearest", out=out,
-                             P=2 * 148, grid=148, cta_offset=rank * 148,
-                             shared_counter=dealer.ptr, stats=True, cta_capacity=148)
-        torch.cuda.synchronize()
-        res[sched] = (out.cpu().numpy(), int(st["cta_units"].sum()))
-        barrier.wait()
+    for prune in PRUNES:
+        for sched in SCHEDS:
+            barrier.wait()                      # the parent has reset the counter
+            out = torch.zeros((20000, 16, 16), dtype=torch.float32, device="cuda")
+            _, st = eng.generate(cen, 16, 0.02, 0.5, schedule=sched, mode="nearest", out=out,
+                                 prune=prune, P=2 * 148, grid=148, cta_offset=rank * 148,
+                                 shared_counter=dealer.ptr, stats=True, cta_capacity=148)
+            torch.cuda.synchronize()
+            res[(prune, sched)] = (out.cpu().numpy(), int(st["cta_units"].sum()), st["G"])
+            barrier.wait()
     dealer.close()
     eng.close()
     q.put((rank, res))
@@ -53,7 +55,6 @@ def test_shared_dealer_two_processes():
     eng = spin.SpinEngine(torch.from_numpy(P).cuda(), torch.from_numpy(Nn).cuda())
     ref = eng.generate(torch.arange(20000, dtype=torch.int32, device="cuda"), 16, 0.02, 0.5,
                        schedule="SS", mode="nearest").cpu().numpy()
-    n_units = -(-20000 // 64)
     dealer = spin.Dealer()
     ctx = mp.get_context("spawn")
     barrier, q = ctx.Barrier(3), ctx.Queue()
@@ -61,7 +62,7 @@ def test_shared_dealer_two_processes():
     for p in procs:
         p.start()
     try:
-        for _ in SCHEDS:
+        for _ in range(len(PRUNES) * len(SCHEDS)):
             dealer.reset()
             torch.cuda.synchronize()
             barrier.wait()                  # workers start this schedule
@@ -71,11 +72,11 @@ def test_shared_dealer_two_processes():
         for p in procs:
             p.join(120)
     assert all(p.exitcode == 0 for p in procs)
-    for sched in SCHEDS:
-        a, ua = res[0][sched]
-        b, ub = res[1][sched]
-        np.testing.assert_array_equal(a + b, ref, err_msg=sched)
-        assert ua + ub == n_units, (sched, ua, ub)
+    for key in res[0]:
+        a, ua, G = res[0][key]
+        b, ub, _ = res[1][key]
+        np.testing.assert_array_equal(a + b, ref, err_msg=str(key))
+        assert ua + ub == -(-20000 // G), (key, ua, ub)
         # disjoint: an image written by both would double its counts
         assert not np.any((a.reshape(20000, -1).sum(1) > 0) & (b.reshape(20000, -1).sum(1) > 0))
     dealer.close()
