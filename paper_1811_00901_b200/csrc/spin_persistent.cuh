@@ -520,9 +520,9 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       // ---- a8-a10: stream points, pair test, compact, accept
       // Each thread holds KP points in registers for all G centres.  Per batch of CB
       // centres the pass bits go to one u32 mask (bit = k*8 + c) stored in smem; once
-      // per tile the warp compacts all its bits into a ring of 16-bit entries
-      // (centre slot << 7 | lane << 2 | k) and processes them 32 at a time, reading the
-      // point from the warp's staged copy of the tile (no global re-load).
+      // per tile the warp compacts all its bits into 16-bit entries (mask word, source
+      // lane, mask bit) and processes them 32 at a time, reading the point from the
+      // warp's staged copy of the tile (no global re-load).
       unsigned qhead = 0, qtail = 0;
       constexpr int NWD = G / CB;                      // mask words per lane per tile
       // candidate operands: centre slot gs, point (source lane, k) from the staged tile
