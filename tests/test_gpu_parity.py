@@ -208,6 +208,23 @@ def test_region_corners(spin, torch):
                 check(gpu, ora, st, mode, f"corners W={W} {mode} c={c}")
 
 
+@pytest.mark.parametrize("offset,scale", [((300.0, -200.0, 500.0), 1.0), ((0.0, 0.0, 0.0), 1e-3),
+                                          ((1e4, 0.0, 0.0), 1.0)])
+def test_far_from_origin_and_tiny_scale(spin, torch, offset, scale):
+    """Clouds far from the origin (|x| up to 1e4: the fp32 hot-loop bounds grow with |x|,
+    so the filter loosens and more decisions go to fp64 / exact) and at a tiny scale
+    (1e-3): results stay oracle-exact (NEAREST) / within tolerance (BILINEAR)."""
+    P0, Nn = clouds.bumpy_sphere(3000, 13)
+    P = (P0.astype(np.float64) * scale + np.asarray(offset)).astype(np.float32)
+    cen = np.arange(0, 3000, 97, dtype=np.int32)
+    b = 0.02 * scale
+    for mode in ("nearest", "bilinear"):
+        for prune in ("brute", "cells"):
+            gpu = run_gpu(spin, torch, P, Nn, cen, 16, b, 0.5, mode, prune=prune)
+            ora, st = oracle(P, Nn, cen, 16, b, 0.5, mode)
+            check(gpu, ora, st, mode, f"offset={offset} scale={scale} {mode} {prune}")
+
+
 def test_near_threshold_ulps(spin, torch):
     """Points 1 fp32 ulp either side of every row / column edge."""
     W, b = 16, 0.02
