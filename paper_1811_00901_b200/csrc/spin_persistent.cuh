@@ -712,7 +712,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         // mask bit (k << 3) | c: point k of this lane, centre cb + c; one loop per variant
         // so the variant branch is taken once per tile, not once per batch
         if (PRUNE == 0 && !sup_hot) {
-#pragma unroll 1
+#pragma unroll 2
           for (int cb = 0; cb < cb_end; cb += CB) {
             unsigned rej = 0u;
 #pragma unroll

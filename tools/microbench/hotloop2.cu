@@ -39,7 +39,7 @@ __device__ __forceinline__ unsigned gather4(unsigned mask, unsigned v0, unsigned
   return d;
 }
 
-template <int V, int NTH>
+template <int V, int NTH, int UNR = 1>
 __global__ void __launch_bounds__(NTH, 1) k(unsigned* out, float ct, float ht, int iters) {
   constexpr int NP = 2;
   __shared__ float4 sA[64], sB[64];
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(NTH, 1) k(unsigned* out, float ct, float ht, i
       asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r[6]), "=l"(r[7]) : "r"((unsigned)__cvta_generic_to_shared(base + 96)));
       X[pr] = r[0]; Y[pr] = r[1]; Z[pr] = r[2]; NXX[pr] = r[3]; NX[pr] = r[4]; NY[pr] = r[5]; NZ[pr] = r[6];
     }
-#pragma unroll 1
+#pragma unroll UNR
     for (int cb = 0; cb < 64; cb += 8) {
       unsigned mask = 0;
 #pragma unroll
@@ -139,6 +139,10 @@ int main() {
            pairs / (ms * 1e-3), pairs * 20 / (ms * 1e-3) / 74.45e12);
   };
   for (int r = 0; r < 2; ++r) {
+    run(k<3, 768, 2>, 768, "V3_sphonly_unroll2");
+    run(k<3, 768, 8>, 768, "V3_sphonly_unroll8");
+    run(k<3, 1024>, 1024, "V3_sphonly_1024");
+    run(k<3, 512>, 512, "V3_sphonly_512");
     run(k<0, 768>, 768, "V0_cyl_setp");
     run(k<1, 768>, 768, "V1_sph_lop");
     run(k<2, 768>, 768, "V2_sph_sat");
