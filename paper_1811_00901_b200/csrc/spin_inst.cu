@@ -15,6 +15,7 @@ const void* SPIN_CAT(kernel_ptr_, INST_MODE, INST_SUP)(int prune, int G, int nt)
       case 4: return (const void*)spin_persistent<INST_MODE, 0, 4, INST_SUP, D>;
       case 8: return (const void*)spin_persistent<INST_MODE, 0, 8, INST_SUP, D>;
       case 16: return (const void*)spin_persistent<INST_MODE, 0, 16, INST_SUP, D>;
+      case 24: return (const void*)spin_persistent<INST_MODE, 0, 24, INST_SUP, D>;
       case 32: return (const void*)spin_persistent<INST_MODE, 0, 32, INST_SUP, D>;
       default: return (const void*)spin_persistent<INST_MODE, 0, 64, INST_SUP, D>;
     }

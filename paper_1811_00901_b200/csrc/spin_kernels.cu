@@ -26,17 +26,30 @@ LaunchCfg choose_launch(int W, int mode, int prune) {
   // smaller staged tile frees the room, and tile reuse by 32 centres beats the extra
   // warps (C4: 524 -> 469 ms).
   constexpr int LIMIT = 220 * 1024;
-  int G = 64;
-  if (prune == 1) G = 32;   // CELLS: larger groups grow the visited box (measured: 32 best)
-  const char* dg = std::getenv("SPIN_DEBUG_G");   // measurement knob
-  if (dg) G = std::atoi(dg);
-  while (G > 4 && make_layout(G, W, mode, prune, NT_DEFAULT).total > LIMIT) G >>= 1;
   LaunchCfg lc;
-  lc.G = G;
   lc.threads = NT_DEFAULT;
-  if (prune == 0 && G < 32 && !dg && make_layout(32, W, mode, prune, 512).total <= LIMIT) {
-    lc.G = 32;
-    lc.threads = 512;
+  const char* dg = std::getenv("SPIN_DEBUG_G");   // measurement knobs
+  const char* dn = std::getenv("SPIN_DEBUG_NT");
+  if (dg) {
+    lc.G = std::atoi(dg);
+    if (dn) lc.threads = std::atoi(dn);
+  } else if (prune == 1) {
+    // CELLS: larger groups grow the visited box (measured: 32 best)
+    int G = 32;
+    while (G > 4 && make_layout(G, W, mode, prune, NT_DEFAULT).total > LIMIT) G >>= 1;
+    lc.G = G;
+  } else {
+    // BRUTE, in order of preference (measured on C2 / C4): 768 threads with G = 64 or
+    // 32; 768 threads with G = 24 (W = 32: C4 451 ms vs 467 ms for 512 threads with
+    // G = 32 and 524 ms for 768 threads with G = 16); 512 threads with G = 32; then
+    // 768 threads with smaller G
+    static const int pref[][2] = {{768, 64}, {768, 32}, {768, 24}, {512, 32},
+                                  {768, 16}, {768, 8}, {768, 4}};
+    for (const auto& c : pref) {
+      lc.threads = c[0];
+      lc.G = c[1];
+      if (make_layout(lc.G, W, mode, prune, lc.threads).total <= LIMIT) break;
+    }
   }
   lc.smem = make_layout(lc.G, W, mode, prune, lc.threads).total;
   return lc;

@@ -52,7 +52,11 @@ constexpr int CB_MAX = 32 / KP;   // centres per mask batch: CB * KP <= 32 bits
 __host__ __device__ constexpr int cb_of(int G) { return G < CB_MAX ? G : CB_MAX; }
 // per-warp candidate ring of u16 entries (power of two): BRUTE tiles hold few candidates
 // (~2% of pairs), CELLS tiles in dense clusters many
-__host__ __device__ constexpr int qcap_of(int prune) { return prune ? 1024 : 512; }
+// (G <= 32 BRUTE groups hold ~100 candidates per warp tile: a 256-entry ring frees the
+// shared memory that lets W = 32 run 768-thread CTAs with G = 24)
+__host__ __device__ constexpr int qcap_of(int prune, int G = 64) {
+  return prune ? 1024 : (G <= 32 ? 256 : 512);
+}
 
 static_assert(CB_MAX * KP == 32 && KP == 4 && KP == KP_POINTS, "mask is one u32: bit (k << 3) | c");
 
@@ -175,7 +179,7 @@ __host__ __device__ inline Layout make_layout(int G, int W, int mode, int prune,
   const size_t WW = (size_t)W * W;
   L.oImg = o; o = align16(o + 4 * WW * G);
   L.oHi = o;
-  L.oQ = o; o += 2 * (size_t)qcap_of(prune) * NWARP;
+  L.oQ = o; o += 2 * (size_t)qcap_of(prune, G) * NWARP;
   o = align16(o);
   L.oTP = o; o += 32 * (size_t)32 * KP * NWARP;    // per-warp staged tile, pair layout (32 B/point)
   L.oTN = o;
@@ -376,7 +380,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool skip_accept = p.debug_skip != 0;   // measurement knob (SPIN_DEBUG_SKIP)
-  constexpr int QCAP = qcap_of(PRUNE);
+  constexpr int QCAP = qcap_of(PRUNE, G);
   uint16_t* sQ = reinterpret_cast<uint16_t*>(smem + L.oQ) + warp * QCAP;
   // staged tile of this warp in pair layout: record r (0..3) of point pair pr (0..KP/2-1)
   // of lane l at sT[(r * (KP/2) + pr) * 32 + l]; r0 {x,x',y,y'}, r1 {z,z',-|x|^2,-|x'|^2},
@@ -582,11 +586,12 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         if (total == 0) return;
         qhead = qtail = 0u;   // the ring is empty between tiles
         // common case: the whole tile fits the ring and one scan places every entry;
-        // dense tiles go a quarter mask word (one point, <= 8 centres, <= 256 entries) at a time, each
-        // appended after the ring was drained to < 64 pending entries (QCAP >= 512).
-        static_assert(QCAP >= 64 + 256, "ring too small for the dense path");
+        // dense tiles go CHB bits of a mask word (<= 32 * CHB entries) at a time, each
+        // appended after the ring was drained to < 64 pending entries.
+        constexpr int CHB = QCAP >= 64 + 256 ? 8 : 4;
+        static_assert(QCAP >= 64 + 32 * CHB, "ring too small for the dense path");
         const bool dense = total > QCAP - 64;
-        const int nchunks = dense ? 4 * NWD : 1;
+        const int nchunks = dense ? (32 / CHB) * NWD : 1;
         for (int ci = 0;;) {
           if (ci < nchunks) {
             if (!dense) {
@@ -638,8 +643,9 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
                 return;
               }
             } else {
-              const int quarter = ci & 3;
-              unsigned m = (sMask[(ci >> 2) * 32 + lane] >> (8 * quarter)) & 0xffu;
+              constexpr int CPW = 32 / CHB;               // chunks per mask word
+              const int sub = ci % CPW;
+              unsigned m = (sMask[(ci / CPW) * 32 + lane] >> (CHB * sub)) & ((1u << CHB) - 1u);
               const int c2 = __popc(m);
               int x2 = c2;
 #pragma unroll
@@ -649,8 +655,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
               }
               const int t2 = __shfl_sync(0xffffffffu, x2, 31);
               unsigned pos = qtail + (unsigned)(x2 - c2);
-              // quarter = point k, bits = centres
-              const unsigned eb = ((unsigned)(ci >> 2) << 10) | ((unsigned)lane << 5) | ((unsigned)quarter << 3);
+              // entry = (word, lane, raw mask bit CHB * sub + b)
+              const unsigned eb = ((unsigned)(ci / CPW) << 10) | ((unsigned)lane << 5) | (unsigned)(CHB * sub);
               while (m) {
                 const unsigned bit = msb(m);
                 m ^= 1u << bit;
