@@ -185,7 +185,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
  * fastest; pageable works) and synchronises `stream`.  Device scratch for the
  * centres and images is owned by the handle and grown on demand.  For BRUTE runs
  * of >= 8 MB of images the D2H copy is pipelined with the kernel: the kernel counts
- * finished images per output segment (16 segments) and a handle-owned copy stream
+ * finished images per output segment (~2 MB each, 16 .. 256 segments) and a handle-owned copy stream
  * waits on each counter (cuStreamWaitValue32, resolved through
  * cudaGetDriverEntryPoint) before copying that segment.  A shared dealer
  * (cp->d_counter) is rejected with SPIN_E_INVAL: multi-device runs use spin_generate.

@@ -813,7 +813,9 @@ spin_status spin_generate_host(spin_handle h, const int32_t* h_centre_idx, int64
     }
   }
   const bool piped = pipe && h->stream_wait_ok == 1;
-  const int32_t nseg_target = 16;
+  // ~2 MB segments (16 .. 256): the last one is copied after the kernel ends
+  const int32_t nseg_target = (int32_t)std::min<int64_t>(
+      256, std::max<int64_t>(16, (int64_t)((size_t)M * img_bytes >> 21)));
   const int32_t seg_images = (int32_t)std::max<int64_t>(1, (M + nseg_target - 1) / nseg_target);
   h->pipe_seg_images = piped ? seg_images : 0;
   st = spin_generate(h, h->cidx, M, W, b, cos_As, sched, cp, mode, prune, h->outbuf, stats, stream);
