@@ -8,6 +8,11 @@
 //   V3 sphonly    : sphere only (support decided later)
 //   V4 cyl_nosup  : beta window + alpha bound predicate chain (support decided later)
 //   V5 sph_setp   : support + sphere, predicate chain
+//   V6            : V3 with the final add written as an FMA by 1 (compiles back to FADD2)
+//   V7 fp_only    : V3's FP work without the sign gather (margins accumulated by FADD2)
+//   V8 ffma2_only : four dependent FFMA2 per two pairs, no ALU work (the pipe ceiling of
+//                   this operand pattern)
+//   UNR template argument: unroll of the centre-batch loop (2 is what the kernel uses)
 #include <cstdio>
 #include <cuda_runtime.h>
 typedef unsigned long long f2;
@@ -51,6 +56,7 @@ __global__ void __launch_bounds__(NTH, 1) k(unsigned* out, float ct, float ht, i
   }
   __syncthreads();
   unsigned acc = 0;
+  f2 facc[2] = {0ull, 0ull};
   for (int it = 0; it < iters; ++it) {
     f2 X[NP], Y[NP], Z[NP], NXX[NP], NX[NP], NY[NP], NZ[NP];
 #pragma unroll
@@ -70,6 +76,7 @@ __global__ void __launch_bounds__(NTH, 1) k(unsigned* out, float ct, float ht, i
       for (int c = 0; c < 8; ++c) {
         const float4 A4 = sA[cb + c], B4 = sB[cb + c];
         unsigned v[4];
+        (void)A4;
 #pragma unroll
         for (int k2 = 0; k2 < NP; ++k2) {
           const int bit = c * 4 + 2 * k2;
@@ -93,6 +100,17 @@ __global__ void __launch_bounds__(NTH, 1) k(unsigned* out, float ct, float ht, i
             const f2 sp2 = add2(fma2(bc2(B4.x), X[k2], fma2(bc2(B4.y), Y[k2], fma2(bc2(B4.z), Z[k2], bc2(B4.w)))), NXX[k2]);
             if (V == 3) {
               up2u(sp2, v[2 * k2], v[2 * k2 + 1]);
+            } else if (V == 7) {
+              // FP only: no sign gather (accumulate the margins with FADD2)
+              const f2 sp = add2(fma2(bc2(B4.x), X[k2], fma2(bc2(B4.y), Y[k2], fma2(bc2(B4.z), Z[k2], bc2(B4.w)))), NXX[k2]);
+              facc[k2] = add2(facc[k2], sp);
+            } else if (V == 8) {
+              // FFMA only (3 FFMA2 + FADD2 without the dependent chain tail): chain of 4 FFMA2
+              const f2 sp = fma2(bc2(B4.x), X[k2], fma2(bc2(B4.y), Y[k2], fma2(bc2(B4.z), Z[k2], fma2(bc2(B4.w), NXX[k2], facc[k2]))));
+              facc[k2] = sp;
+            } else if (V == 6) {
+              const f2 sq = fma2(bc2(1.0f), NXX[k2], fma2(bc2(B4.x), X[k2], fma2(bc2(B4.y), Y[k2], fma2(bc2(B4.z), Z[k2], bc2(B4.w)))));
+              up2u(sq, v[2 * k2], v[2 * k2 + 1]);
             } else if (V == 2) {
               // sigma = sat(BIG*(n.nx - c) + 1): 1 when supported, 0 when certainly not
               const f2 sp = fma2(bc2(A4.y), NY[k2], fma2(bc2(A4.z), NZ[k2], bc2(A4.w)));
@@ -116,14 +134,16 @@ __global__ void __launch_bounds__(NTH, 1) k(unsigned* out, float ct, float ht, i
             }
           }
         }
-        if (V == 1 || V == 2 || V == 3) mask = gather4(mask, v[0], v[1], v[2], v[3], 0x01010101u << c);
+        if (V == 1 || V == 2 || V == 3 || V == 6) mask = gather4(mask, v[0], v[1], v[2], v[3], 0x01010101u << c);
       }
       acc += mask;
     }
   }
+  if (V == 7 || V == 8) { float a0, a1, b0, b1; up2(facc[0], a0, a1); up2(facc[1], b0, b1); acc += __float_as_uint(a0 + a1 + b0 + b1); }
   if (acc == 0x12345u) out[0] = acc;
 }
 
+#ifndef HOTLOOP_ONLY_V3
 int main() {
   unsigned* d; cudaMalloc(&d, 64);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -139,6 +159,10 @@ int main() {
            pairs / (ms * 1e-3), pairs * 20 / (ms * 1e-3) / 74.45e12);
   };
   for (int r = 0; r < 2; ++r) {
+    run(k<7, 768>, 768, "V7_fp_only");
+    run(k<8, 768>, 768, "V8_ffma2_only");
+    run(k<6, 768>, 768, "V6_sphonly_ffma2add");
+    run(k<6, 768, 2>, 768, "V6_sphonly_ffma2add_unroll2");
     run(k<3, 768, 2>, 768, "V3_sphonly_unroll2");
     run(k<3, 768, 8>, 768, "V3_sphonly_unroll8");
     run(k<3, 1024>, 1024, "V3_sphonly_1024");
@@ -152,3 +176,4 @@ int main() {
   }
   return 0;
 }
+#endif
