@@ -413,6 +413,11 @@ def run_spin(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_dict(cfg, P, Nn, cen, mode, args.cpu_seconds)
 
+    # CELLS: the implementation-independent work measure (pairs within the region radius
+    # R of their centre), counted by a separate diagnostic kernel after timing
+    in_sphere = None
+    if prune == "cells":
+        in_sphere = eng.count_in_sphere(d_cen, spin.region_radius(W, b, mode))
     launches = 1 if prune == "brute" else 6   # CELLS: 5 centre-ordering kernels + the spin kernel
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -443,7 +448,7 @@ def run_spin(args):
                                     "FFMA microbenchmark measured 72.5 TFLOP/s"},
         "pairs": {"visited": st0["pairs_visited"], "candidate": st0["pairs_candidate"],
                   "accepted": st0["pairs_accepted"], "fp64_fallbacks": st0["fp64_fallbacks"],
-                  "exact_fallbacks": st0["exact_fallbacks"]},
+                  "exact_fallbacks": st0["exact_fallbacks"], "in_sphere": in_sphere},
         "support_first": alt,
         "clocks": clocks,
         "e2e": e2e,

@@ -209,6 +209,14 @@ spin_status spin_chunk_sequence(spin_schedule sched, int64_t n_units, int32_t P,
  * mode, flags): sqrt(alpha_max^2 + |beta|_max^2).  Host-only. */
 double spin_region_radius(int32_t W, double b, spin_mode mode, uint32_t flags);
 
+/* spin_count_in_sphere — the implementation-independent work measure of SURVEY §8(d)
+ * for CELLS: sum over the M centres of #{points x : |x - p| <= R} (R = e.g.
+ * spin_region_radius), counted exactly (double, numpy's operation order) on the
+ * handle's cell grid (built for R if needed).  Diagnostic, not part of spin_generate;
+ * synchronises `stream`. */
+spin_status spin_count_in_sphere(spin_handle h, const int32_t* d_centre_idx, int64_t M, double R,
+                                 int64_t* count, spin_stream stream);
+
 /* spin_cos_from_degrees — cos of an angle in degrees, exact at 0, 60, 90, 120, 180
  * (1, 0.5, 0, -0.5, -1); >= 180 degrees returns -INFINITY (test disabled). */
 double spin_cos_from_degrees(double deg);

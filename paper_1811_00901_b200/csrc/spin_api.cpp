@@ -333,6 +333,31 @@ double spin_cos_from_degrees(double deg) {
   return std::cos(deg * (M_PI / 180.0));
 }
 
+spin_status spin_count_in_sphere(spin_handle h, const int32_t* d_centre_idx, int64_t M, double R,
+                                 int64_t* count, spin_stream stream) {
+  if (!h || !count) return fail(SPIN_E_INVAL, "null handle or count");
+  if (M < 0 || M >= ((int64_t)1 << 31)) return fail(SPIN_E_INVAL, "M=%lld out of range", (long long)M);
+  if (!std::isfinite(R) || R <= 0.0 || R > 1e30) return fail(SPIN_E_INVAL, "R=%g must be positive and finite", R);
+  *count = 0;
+  if (M == 0) return SPIN_OK;
+  if (!d_centre_idx) return fail(SPIN_E_INVAL, "null d_centre_idx");
+  cudaStream_t s = (cudaStream_t)stream;
+  const float R_up = (float)(R * (1.0 + 1e-6));
+  double gms = 0.0;
+  spin_status st = ensure_grid(h, R_up, s, &gms);
+  if (st != SPIN_OK) return st;
+  unsigned long long* d_cnt = (unsigned long long*)h->stats;   // scratch slot, zeroed below
+  CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), s), "memset");
+  CK(launch_count_in_sphere(d_centre_idx, M, h->pos, (int32_t)h->N, h->spos, h->cell_start, h->ox,
+                            h->oy, h->oz, h->inv_h, h->dx, h->dy, h->dz, R, R_up, d_cnt, h->sms, s),
+     "count kernel");
+  unsigned long long c = 0;
+  CK(cudaMemcpyAsync(&c, d_cnt, sizeof c, cudaMemcpyDeviceToHost, s), "count readback");
+  CK(cudaStreamSynchronize(s), "count sync");
+  *count = (int64_t)c;
+  return SPIN_OK;
+}
+
 double spin_region_radius(int32_t W, double b, spin_mode mode, uint32_t flags) {
   return region_of(W, b, (int)mode, flags).R;
 }

@@ -110,6 +110,10 @@ cudaError_t launch_cell_build(const float4* pos, const float4* nrm, int32_t N, i
                               int32_t* cursor, int32_t* scan_tmp, float4* spos, float4* snrm,
                               cudaStream_t s);
 // centre ordering (a5): coarse Morton bucket counting sort
+cudaError_t launch_count_in_sphere(const int32_t* centre_idx, int64_t M, const float4* cpos, int32_t N,
+                                   const float4* spos, const int32_t* cell_start, float ox, float oy,
+                                   float oz, float inv_h, int dx, int dy, int dz, double R, float R_up,
+                                   unsigned long long* count, int sms, cudaStream_t s);
 cudaError_t launch_centre_order(const int32_t* centre_idx, int64_t M, const float4* cpos,
                                 int32_t N, float ox, float oy, float oz, float inv_h, int dx,
                                 int dy, int dz, int shift, int bits, int32_t* keys,

@@ -302,4 +302,52 @@ cudaError_t launch_centre_order(const int32_t* centre_idx, int64_t M, const floa
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ diagnostic: in-sphere pairs
+// SURVEY §8(d)'s implementation-independent CELLS count: pairs with |x - p| <= R, one warp
+// per centre over the grid rows of p's R-box, the test in double with numpy's operation
+// order (no contraction), so the oracle's float64 count is matched exactly.
+__global__ void k_count_in_sphere(const int32_t* __restrict__ centre_idx, int64_t M,
+                                  const float4* __restrict__ cpos, int32_t N,
+                                  const float4* __restrict__ spos, const int32_t* __restrict__ cell_start,
+                                  float ox, float oy, float oz, float inv_h, int dx, int dy, int dz,
+                                  double R, float R_up, unsigned long long* count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const double R2 = R * R;
+  unsigned long long local = 0;
+  for (int64_t m = wid; m < M; m += nw) {
+    const int c = centre_idx[m];
+    if (c < 0 || c >= N) continue;
+    const float4 P4 = cpos[c];
+    const int x0 = cell_coord(__fsub_rd(P4.x, R_up), ox, inv_h, dx), x1 = cell_coord(__fadd_ru(P4.x, R_up), ox, inv_h, dx);
+    const int y0 = cell_coord(__fsub_rd(P4.y, R_up), oy, inv_h, dy), y1 = cell_coord(__fadd_ru(P4.y, R_up), oy, inv_h, dy);
+    const int z0 = cell_coord(__fsub_rd(P4.z, R_up), oz, inv_h, dz), z1 = cell_coord(__fadd_ru(P4.z, R_up), oz, inv_h, dz);
+    for (int z = z0; z <= z1; ++z)
+      for (int y = y0; y <= y1; ++y) {
+        const int base = (z * dy + y) * dx;
+        const int a = cell_start[base + x0], e = cell_start[base + x1 + 1];
+        for (int j = a + lane; j < e; j += 32) {
+          const float4 X = spos[j];
+          const double ddx = __dsub_rn((double)X.x, (double)P4.x);
+          const double ddy = __dsub_rn((double)X.y, (double)P4.y);
+          const double ddz = __dsub_rn((double)X.z, (double)P4.z);
+          const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)), __dmul_rn(ddz, ddz));
+          local += d2 <= R2;
+        }
+      }
+  }
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if (lane == 0 && local) atomicAdd(count, local);
+}
+
+cudaError_t launch_count_in_sphere(const int32_t* centre_idx, int64_t M, const float4* cpos, int32_t N,
+                                   const float4* spos, const int32_t* cell_start, float ox, float oy,
+                                   float oz, float inv_h, int dx, int dy, int dz, double R, float R_up,
+                                   unsigned long long* count, int sms, cudaStream_t s) {
+  k_count_in_sphere<<<sms * 8, 256, 0, s>>>(centre_idx, M, cpos, N, spos, cell_start, ox, oy, oz,
+                                            inv_h, dx, dy, dz, R, R_up, count);
+  return cudaGetLastError();
+}
+
 }  // namespace spin

@@ -117,12 +117,15 @@ class Dealer:
             self.ptr = None
 
 
+_lib.spin_count_in_sphere.argtypes = [_vp, _vp, C.c_int64, C.c_double, C.POINTER(C.c_int64), _vp]
+_lib.spin_count_in_sphere.restype = C.c_int
+
 EXPORTS = ["spin_create", "spin_load_cloud", "spin_generate", "spin_generate_host",
            "spin_chunk_sequence", "spin_region_radius", "spin_cos_from_degrees", "spin_default_P",
            "spin_destroy", "spin_last_error", "spin_abi_version",
            "spin_read_xyzn", "spin_read_off", "spin_vertex_normals",
            "spin_dealer_alloc", "spin_dealer_ipc_handle", "spin_dealer_ipc_open",
-           "spin_dealer_reset", "spin_dealer_free"]
+           "spin_dealer_reset", "spin_dealer_free", "spin_count_in_sphere"]
 
 
 def read_xyzn(path):
@@ -300,6 +303,14 @@ class SpinEngine:
         if stats:
             return out, _stats_dict(st, t0, t1, un)
         return out
+
+    def count_in_sphere(self, centre_idx, R, stream=None) -> int:
+        """spin_count_in_sphere: sum over device int32 centres of #{x : |x - p| <= R}."""
+        n = C.c_int64()
+        M = int(centre_idx.shape[0])
+        _check(_lib.spin_count_in_sphere(self._h, _ptr(centre_idx) if M else None, M, float(R),
+                                         C.byref(n), _stream(stream)))
+        return n.value
 
     def generate_host(self, centre_idx: np.ndarray, W, b, cos_As, schedule="STATIC",
                       mode="nearest", prune="brute", P=0, unit=0, gss_min_chunk=0,

@@ -550,3 +550,22 @@ def test_heterogeneous_workers_same_images_and_trend(spin, torch):
         assert u[:37].mean() < 0.6 * u[37:].mean(), u
     finally:
         eng.close()
+
+
+def test_count_in_sphere_matches_numpy(spin, torch):
+    """spin_count_in_sphere (CELLS work measure independent of the
+    implementation) equals a float64 brute-force count, on a clustered cloud."""
+    P, Nn = clouds.clustered(30000, 51)
+    cen = clouds.sample_centres(30000, 700, 52)
+    R = spin.region_radius(16, 0.01, "bilinear")
+    eng = spin.SpinEngine(_dev(torch, P), _dev(torch, Nn))
+    try:
+        got = eng.count_in_sphere(_dev(torch, cen), R)
+    finally:
+        eng.close()
+    X = P.astype(np.float64)
+    want = 0
+    for c in cen:
+        d = X - X[c]
+        want += int(np.count_nonzero((d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2] <= R * R))
+    assert got == want
