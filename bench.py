@@ -445,7 +445,9 @@ def run_spin(args):
                      "kernel": "spin_persistent", "kernel_ms": kern,
                      "flop_per_pair": FLOP_PER_PAIR,
                      "peak_source": "derived 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md); "
-                                    "FFMA microbenchmark measured 72.5 TFLOP/s"},
+                                    "FFMA microbenchmark measured 72.5 TFLOP/s",
+                     "frac_at_measured_clock": (achieved_tflops / (FP32_PEAK_TFLOPS * clocks["sm_mhz"] / 1965.0)
+                                                if clocks.get("sm_mhz") else None)},
         "pairs": {"visited": st0["pairs_visited"], "candidate": st0["pairs_candidate"],
                   "accepted": st0["pairs_accepted"], "fp64_fallbacks": st0["fp64_fallbacks"],
                   "exact_fallbacks": st0["exact_fallbacks"], "in_sphere": in_sphere},
