@@ -166,6 +166,7 @@ struct spin_ctx {
   int64_t N = 0, Npad = 0, cap = 0;
   float4* pos = nullptr;
   float4* nrm = nullptr;
+  float4* tpos = nullptr;   // BRUTE warp-tile pair layout (2 float4 per point)
   float absmax = 0.f;
   float aabb[6] = {0, 0, 0, 0, 0, 0};
   uint64_t cloud_version = 0;
@@ -228,10 +229,12 @@ spin_status load_cloud(spin_ctx* h, const float* points, const float* normals, i
   if (Npad > h->cap) {
     if (h->pos) cudaFree(h->pos);
     if (h->nrm) cudaFree(h->nrm);
-    h->pos = h->nrm = nullptr;
+    if (h->tpos) cudaFree(h->tpos);
+    h->pos = h->nrm = h->tpos = nullptr;
     h->cap = 0;
     if (cudaMalloc((void**)&h->pos, Npad * sizeof(float4)) != cudaSuccess ||
-        cudaMalloc((void**)&h->nrm, Npad * sizeof(float4)) != cudaSuccess) {
+        cudaMalloc((void**)&h->nrm, Npad * sizeof(float4)) != cudaSuccess ||
+        cudaMalloc((void**)&h->tpos, 2 * Npad * sizeof(float4)) != cudaSuccess) {
       cudaGetLastError();
       return fail(SPIN_E_NOMEM, "cudaMalloc of the cloud (%lld points) failed", (long long)N);
     }
@@ -252,6 +255,7 @@ spin_status load_cloud(spin_ctx* h, const float* points, const float* normals, i
   CK(launch_relayout(h->stage_p, h->stage_n, N, Npad, h->pos, h->nrm, h->red,
                      reinterpret_cast<float*>(h->red + 1), reinterpret_cast<float*>(h->red + 2), s),
      "relayout");
+  CK(launch_pair_layout(h->pos, h->nrm, Npad, h->tpos, s), "pair layout");
   CK(cudaMemcpyAsync(h->h_red, h->red, sizeof init, cudaMemcpyDeviceToHost, s), "readback");
   CK(cudaStreamSynchronize(s), "spin_create sync");
   int32_t red[8];
@@ -431,7 +435,7 @@ spin_status spin_load_cloud(spin_handle h, const float* points, const float* nor
 
 void spin_destroy(spin_handle h) {
   if (!h) return;
-  void* ptrs[] = {h->pos, h->nrm, h->cell_start, h->spos, h->snrm, h->keys, h->counts,
+  void* ptrs[] = {h->pos, h->nrm, h->tpos, h->cell_start, h->spos, h->snrm, h->keys, h->counts,
                   h->cursor, h->scan_tmp, h->ckeys, h->cstarts, h->order, h->bounds,
                   h->counter, h->stats, h->err, h->cta_t0, h->cta_t1, h->cta_units, h->cidx,
                   h->outbuf, h->stage_p, h->stage_n, h->red, h->hi_scratch, h->seg_done};
@@ -654,6 +658,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   if (prune == SPIN_BRUTE) {
     p.pos = h->pos;
     p.nrm = h->nrm;
+    p.tpos = h->tpos;
     p.n_tiles = (int32_t)((h->N + lc.threads * KP_POINTS - 1) / (lc.threads * KP_POINTS));
   } else {
     const float R = f32_up(rg.R * (1.0 + 1e-6) + 1e-30);

@@ -12,6 +12,8 @@ struct KParams {
   // N real points followed by sentinel padding (|x|^2 = +inf never passes).
   const float4* __restrict__ pos;   // {x, y, z, |x|^2}
   const float4* __restrict__ nrm;   // {nx, ny, nz, 0}
+  const float4* __restrict__ tpos;  // BRUTE: the cloud in 128-point warp-tile pair layout
+                                    // (4 KB per chunk, the smem staging layout; TMA source)
   const float4* __restrict__ cpos;  // original-order copies, indexed by centre index
   const float4* __restrict__ cnrm;
   int32_t N;
@@ -99,6 +101,8 @@ cudaError_t launch_spin(const LaunchCfg& lc, int mode, int prune, int grid, cons
                         cudaStream_t s);
 
 // cloud relayout + validation (a1)
+cudaError_t launch_pair_layout(const float4* pos, const float4* nrm, int64_t Npad, float4* tpos,
+                               cudaStream_t s);
 cudaError_t launch_relayout(const float* pts, const float* nrm, int64_t N, int64_t Npad,
                             float4* pos, float4* nrm4, int32_t* bad, float* absmax,
                             float* aabb, cudaStream_t s);

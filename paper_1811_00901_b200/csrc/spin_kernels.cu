@@ -114,6 +114,34 @@ __global__ void k_relayout(const float* __restrict__ pts, const float* __restric
   }
 }
 
+// BRUTE tiles in the shared-memory staging layout, so a warp's 128 points are ONE 4 KB
+// bulk copy: chunk c holds points 128c .. 128c+127; point 128c + 32k + l (lane l, point
+// k of that lane) sits in records r = 0..3 of pair k/2, half k&1:
+//   r0 {x, x', y, y'}  r1 {z, z', -|x|^2, -|x'|^2}  r2 {nx, nx', ny, ny'}  r3 {nz, nz', 0, 0}
+__global__ void k_pair_layout(const float4* __restrict__ pos, const float4* __restrict__ nrm,
+                              int64_t Npad, float* __restrict__ tpos) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= Npad) return;
+  const int64_t c = j >> 7;
+  const int within = (int)(j & 127), k = within >> 5, l = within & 31, pr = k >> 1, hf = k & 1;
+  const float4 a = pos[j], n = nrm[j];
+  float* base = tpos + c * 1024;    // 256 float4 per chunk
+  auto rec = [&](int r) { return base + ((r * 2 + pr) * 32 + l) * 4; };
+  rec(0)[hf] = a.x;
+  rec(0)[2 + hf] = a.y;
+  rec(1)[hf] = a.z;
+  rec(1)[2 + hf] = -a.w;
+  rec(2)[hf] = n.x;
+  rec(2)[2 + hf] = n.y;
+  rec(3)[hf] = n.z;
+  rec(3)[2 + hf] = 0.f;
+}
+cudaError_t launch_pair_layout(const float4* pos, const float4* nrm, int64_t Npad, float4* tpos,
+                               cudaStream_t s) {
+  k_pair_layout<<<(unsigned)((Npad + 255) / 256), 256, 0, s>>>(pos, nrm, Npad, (float*)tpos);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_relayout(const float* pts, const float* nrm, int64_t N, int64_t Npad,
                             float4* pos, float4* nrm4, int32_t* bad, float* absmax, float* aabb,
                             cudaStream_t s) {

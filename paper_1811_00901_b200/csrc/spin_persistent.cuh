@@ -38,6 +38,9 @@
 #ifndef SPIN_APL_BRUTE
 #define SPIN_APL_BRUTE 1      // BRUTE candidates per lane per accept pass
 #endif
+#ifndef SPIN_BRUTE_TMA
+#define SPIN_BRUTE_TMA 1      // BRUTE: stage each warp tile with one 4 KB bulk copy (TMA)
+#endif
 #ifndef SPIN_APL_BRUTE512
 #define SPIN_APL_BRUTE512 1   // the same for the 512-thread (W = 32) variant
 #endif
@@ -70,6 +73,28 @@ __device__ __forceinline__ unsigned msb(unsigned m) {   // m != 0
   asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(m));
   return b;
 }
+// ---- 1-D bulk copy (TMA engine) global -> shared with an mbarrier transaction count
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;"
+               :: "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done) : "r"(b), "r"(phase) : "memory");
+  } while (!done);
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -380,6 +405,17 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool skip_accept = p.debug_skip != 0;   // measurement knob (SPIN_DEBUG_SKIP)
+  // BRUTE BILINEAR stages tiles with one bulk copy (measured: C4 455 -> 435 ms, C2 3.68 ->
+  // 3.66 ms); BRUTE NEAREST keeps per-lane loads (measured faster there: C2 3.39 vs 3.48,
+  // P6 26.9 vs 27.5 ms with the bulk copy)
+  constexpr bool TMA_TILE = PRUNE == 0 && MODE == 1 && SPIN_BRUTE_TMA;
+  __shared__ __align__(8) uint64_t s_tile_bar[NWARP];   // BRUTE: tile bulk-copy barrier per warp
+  unsigned tile_phase = 0;
+  if (TMA_TILE) {
+    if (lane == 0) mbar_init(&s_tile_bar[warp], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+  }
   constexpr int QCAP = qcap_of(PRUNE, G);
   uint16_t* sQ = reinterpret_cast<uint16_t*>(smem + L.oQ) + warp * QCAP;
   // staged tile of this warp in pair layout: record r (0..3) of point pair pr (0..KP/2-1)
@@ -688,8 +724,19 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         // stage the tile in pair layout (also the accept path's copy), then read the
         // records back so each f32x2 operand arrives as an aligned register pair
         f2 X2[KP / 2], Y2[KP / 2], Z2[KP / 2], NXX2[KP / 2], NX2[KP / 2], NY2[KP / 2], NZ2[KP / 2];
+        if (TMA_TILE) {
+          // the warp's 128 points, already in staging layout in HBM (tpos): one bulk copy
+          // into the warp's staged tile; prior generic reads of the buffer are ordered
+          // before the async-proxy write by the proxy fence
+          if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_load(sT, p.tpos + (size_t)(j[0] >> 7) * 256, 4096u, &s_tile_bar[warp]);
+          }
+          mbar_wait(&s_tile_bar[warp], tile_phase);
+          tile_phase ^= 1u;
+        }
 #pragma unroll
-        for (int k = 0; k < KP; k += 2) {
+        for (int k = 0; !TMA_TILE && k < KP; k += 2) {
           const float4 a0 = __ldg(&p.pos[j[k]]), a1 = __ldg(&p.pos[j[k + 1]]);
           const float4 b0 = __ldg(&p.nrm[j[k]]), b1 = __ldg(&p.nrm[j[k + 1]]);
           const int pr = k / 2;
@@ -818,6 +865,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           int j[KP];
 #pragma unroll
           for (int k = 0; k < KP; ++k) j[k] = base + k * NT;
+          if (TMA_TILE) j[0] = t * (NT * KP) + warp * 128;   // the warp's 128-point chunk
           run_tile(j);
         }
       } else {
