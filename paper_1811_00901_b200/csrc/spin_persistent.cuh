@@ -41,6 +41,12 @@
 #ifndef SPIN_BRUTE_TMA
 #define SPIN_BRUTE_TMA 1      // BRUTE: stage each warp tile with one 4 KB bulk copy (TMA)
 #endif
+#ifndef SPIN_TMA_WAIT_ALL
+#define SPIN_TMA_WAIT_ALL 1   // every lane polls the tile mbarrier (0: lane 0 polls, warp barrier)
+#endif
+#ifndef SPIN_TMA_NEAREST
+#define SPIN_TMA_NEAREST 0    // bulk-copy staging for BRUTE NEAREST too
+#endif
 #ifndef SPIN_APL_BRUTE512
 #define SPIN_APL_BRUTE512 1   // the same for the 512-thread (W = 32) variant
 #endif
@@ -408,7 +414,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   // BRUTE BILINEAR stages tiles with one bulk copy (measured: C4 455 -> 435 ms, C2 3.68 ->
   // 3.66 ms); BRUTE NEAREST keeps per-lane loads (measured faster there: C2 3.39 vs 3.48,
   // P6 26.9 vs 27.5 ms with the bulk copy)
-  constexpr bool TMA_TILE = PRUNE == 0 && MODE == 1 && SPIN_BRUTE_TMA;
+  constexpr bool TMA_TILE = PRUNE == 0 && (MODE == 1 || SPIN_TMA_NEAREST) && SPIN_BRUTE_TMA;
   __shared__ __align__(8) uint64_t s_tile_bar[NWARP];   // BRUTE: tile bulk-copy barrier per warp
   unsigned tile_phase = 0;
   if (TMA_TILE) {
@@ -732,7 +738,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             bulk_load(sT, p.tpos + (size_t)(j[0] >> 7) * 256, 4096u, &s_tile_bar[warp]);
           }
-          mbar_wait(&s_tile_bar[warp], tile_phase);
+          if (SPIN_TMA_WAIT_ALL || lane == 0) mbar_wait(&s_tile_bar[warp], tile_phase);
+          if (!SPIN_TMA_WAIT_ALL) __syncwarp();   // lane 0 acquired the phase; the warp barrier orders the rest
           tile_phase ^= 1u;
         }
 #pragma unroll
