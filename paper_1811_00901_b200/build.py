@@ -50,6 +50,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     global OUT
     if out:
         OUT = os.path.abspath(out)
+        os.makedirs(os.path.dirname(OUT), exist_ok=True)
     build_dir = BUILD if not defs else BUILD + "_" + "_".join(d.strip("-D").replace("=", "") for d in defs)
     os.makedirs(build_dir, exist_ok=True)
     objs = [os.path.join(build_dir, u[2] + ".o") for u in UNITS]

@@ -670,8 +670,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
               }
               qtail = (unsigned)total;
               // every entry of the tile sits at slots 0 .. total-1: plain passes of 32 x APL
-              // (BRUTE BILINEAR keeps the ring passes below: measured 1.3% faster there)
-              if (!(MODE == 1 && PRUNE == 0)) {
+              {
                 __syncwarp();
                 if (skip_accept) return;
                 constexpr int PASS = 32 * APL;
