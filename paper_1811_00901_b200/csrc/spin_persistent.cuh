@@ -47,6 +47,9 @@
 #ifndef SPIN_TMA_NEAREST
 #define SPIN_TMA_NEAREST 0    // bulk-copy staging for BRUTE NEAREST too
 #endif
+#ifndef SPIN_APL_CELLS
+#define SPIN_APL_CELLS 2      // CELLS candidates per lane per accept pass
+#endif
 #ifndef SPIN_APL_BRUTE512
 #define SPIN_APL_BRUTE512 1   // the same for the 512-thread (W = 32) variant
 #endif
@@ -585,7 +588,9 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       };
       // CELLS (dense, latency-bound) takes two candidates per lane per pass so that the
       // two independent decisions interleave; BRUTE keeps one (fewer live registers).
-      constexpr int APL = PRUNE == 1 ? 2 : (NT == 512 ? SPIN_APL_BRUTE512 : SPIN_APL_BRUTE);
+      // (CELLS: two per lane for BILINEAR, one for NEAREST, as measured: C3 47.3 vs 48.0 ms,
+      // C5 188 vs 191 ms)
+      constexpr int APL = PRUNE == 1 ? (MODE == 1 ? SPIN_APL_CELLS : 1) : (NT == 512 ? SPIN_APL_BRUTE512 : SPIN_APL_BRUTE);
       auto process_pair = [&](unsigned e0, bool v0, unsigned e1, bool v1) {
         float4 P0, N0, X0, NX0, P1, N1, X1, NX1;
         load_entry(e0, P0, N0, X0, NX0);
