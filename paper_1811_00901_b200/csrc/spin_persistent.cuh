@@ -953,24 +953,21 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             for (int g = 0; g < G; ++g) live += sM[g] >= 0;
             visited += (unsigned long long)T * live;
           }
+          int lo = 0;   // row of this thread's previous point (its f is smaller)
           for (int f0 = 0; f0 < T; f0 += NT * KP) {
             int j[KP];
-            int lo = 0;   // row of the previous point of this thread (its f is smaller)
 #pragma unroll
             for (int k = 0; k < KP; ++k) {
               const int f = f0 + tid + k * NT;
               if (f < T) {
                 // largest r with sRowO[r] <= f: gallop from the previous point's row, then
-                // bisect (k = 0 bisects the whole batch)
-                int hi = nb - 1;
-                if (k > 0) {
-                  int step = 1;
-                  while (lo + step < nb && sRowO[lo + step] <= f) {
-                    lo += step;
-                    step <<= 1;
-                  }
-                  hi = min(lo + step, nb) - 1;
+                // bisect
+                int step = 1;
+                while (lo + step < nb && sRowO[lo + step] <= f) {
+                  lo += step;
+                  step <<= 1;
                 }
+                int hi = min(lo + step, nb) - 1;
                 while (lo < hi) {
                   const int mid = (lo + hi + 1) >> 1;
                   if (sRowO[mid] <= f) lo = mid; else hi = mid - 1;
