@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         // common case: the whole tile fits the ring and one scan places every entry;
         // dense tiles go CHB bits of a mask word (<= 32 * CHB entries) at a time, each
         // appended after the ring was drained to < 64 pending entries.
-        constexpr int CHB = QCAP >= 64 + 256 ? 8 : 4;
+        constexpr int CHB = QCAP >= 64 + 512 ? 16 : QCAP >= 64 + 256 ? 8 : 4;
         static_assert(QCAP >= 64 + 32 * CHB, "ring too small for the dense path");
         const bool dense = total > QCAP - 64;
         const int nchunks = dense ? (32 / CHB) * NWD : 1;
