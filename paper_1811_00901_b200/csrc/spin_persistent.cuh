@@ -691,6 +691,32 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             } else {
               constexpr int CPW = 32 / CHB;               // chunks per mask word
               const int sub = ci % CPW;
+              if (PRUNE == 1 && CPW > 1 && sub == 0) {
+                // a whole mask word that fits the ring goes in one scan
+                unsigned mw = sMask[(ci / CPW) * 32 + lane];
+                const int cw = __popc(mw);
+                int xw = cw;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                  const int y = __shfl_up_sync(0xffffffffu, xw, o);
+                  if (lane >= o) xw += y;
+                }
+                const int tw = __shfl_sync(0xffffffffu, xw, 31);
+                if (tw <= QCAP - 64) {
+                  unsigned pos = qtail + (unsigned)(xw - cw);
+                  const unsigned eb = ((unsigned)(ci / CPW) << 10) | ((unsigned)lane << 5);
+                  while (mw) {
+                    const unsigned bit = msb(mw);
+                    mw ^= 1u << bit;
+                    sQ[pos & (QCAP - 1)] = (uint16_t)(eb | bit);
+                    ++pos;
+                  }
+                  qtail += (unsigned)tw;
+                  ci += CPW;
+                  goto appended;
+                }
+              }
+              {
               unsigned m = (sMask[(ci / CPW) * 32 + lane] >> (CHB * sub)) & ((1u << CHB) - 1u);
               const int c2 = __popc(m);
               int x2 = c2;
@@ -710,8 +736,10 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
                 ++pos;
               }
               qtail += (unsigned)t2;
+              }
+              ++ci;
             }
-            ++ci;
+          appended:;
           }
           const bool more = ci < nchunks;
           __syncwarp();
