@@ -619,6 +619,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
     p.self_a = (float)(p.A - i0);
   }
   if (!(Eu_a < 0.25 && Ew_a < 0.25)) p.no_fast_cert = 1;  // fp32 cannot resolve bins: skip it
+  if (p.no_fast_cert) p.D2g = -1.0f;   // the fp32 stage certifies nothing (decide: dd <= D2g fails)
 
   // ---- cloud, centres, dealing, outputs
   p.cpos = h->pos;

@@ -294,7 +294,8 @@ __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const f
   const float uval = fmaf(-be, p.inv_b, p.Au);
   const float wval = q * p.inv_b2;                                   // (alpha/b)^2
   // fp32 verdicts need the certified domain (|d| <= D) and |u| < 2^21 (magic rounding)
-  const bool unc0 = (p.no_fast_cert != 0) | !(ds > p.Es_a) | !(dd <= p.D2g) |
+  // (SPIN_F_NO_FAST_CERT arrives as D2g = -1: every candidate is uncertain)
+  const bool unc0 = !(ds > p.Es_a) | !(dd <= p.D2g) |
                     !(fabsf(uval) < 2097152.0f);
   Dec r;
   r.a = 0.f;
