@@ -50,6 +50,9 @@
 #ifndef SPIN_APL_CELLS
 #define SPIN_APL_CELLS 2      // CELLS candidates per lane per accept pass
 #endif
+#ifndef SPIN_HOT_UNROLL
+#define SPIN_HOT_UNROLL 2     // unroll of the sphere-only centre-batch loop
+#endif
 #ifndef SPIN_APL_BRUTE512
 #define SPIN_APL_BRUTE512 1   // the same for the 512-thread (W = 32) variant
 #endif
@@ -57,6 +60,7 @@
 
 namespace spin {
 
+constexpr int HOT_UNROLL = SPIN_HOT_UNROLL;   // sphere-only batch loop unroll
 constexpr int NT_DEFAULT = SPIN_NT;   // threads per CTA (one CTA per SM); 512 for G = 32 at W > 24
 constexpr int KP = SPIN_KP;       // points per thread (register blocking)
 constexpr int LOGKP = KP == 4 ? 2 : 1;
@@ -805,7 +809,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         // mask bit (k << 3) | c: point k of this lane, centre cb + c; one loop per variant
         // so the variant branch is taken once per tile, not once per batch
         if (PRUNE == 0 && !sup_hot) {
-#pragma unroll 2
+#pragma unroll HOT_UNROLL
           for (int cb = 0; cb < cb_end; cb += CB) {
             unsigned rej = 0u;
 #pragma unroll
