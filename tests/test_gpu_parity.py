@@ -121,9 +121,10 @@ def test_bumpy_ragged(spin, torch, mode, N, M):
     check(gpu, ora, st, mode, f"bumpy N={N} M={M} {mode}")
 
 
-@pytest.mark.parametrize("W", [1, 2, 5, 24, 32, 64])
+@pytest.mark.parametrize("W", [1, 2, 5, 17, 24, 28, 32, 33, 41, 64])
 def test_widths(spin, torch, W):
-    """W = 1 .. 64 (G = 32/16/8 kernel variants), odd W (real W/2, #3)."""
+    """W = 1 .. 64 across every BRUTE launch shape the planner picks (768 threads with
+    G = 64 / 32 / 24 / 16 / 8 / 4, 512 threads with G = 32 at W = 33), odd W (real W/2, #3)."""
     P, Nn = clouds.bumpy_sphere(3000, 7)
     cen = np.arange(0, 3000, 41, dtype=np.int32)
     b = 0.4 / W
@@ -295,6 +296,20 @@ def test_cells_vs_oracle_and_brute(spin, torch, mode):
         np.testing.assert_array_equal(got, cells)
     got = run_gpu(spin, torch, P, Nn, cen, W, b, c, mode, prune="cells", flags=spin.F_NO_SORT)
     np.testing.assert_array_equal(got, cells)
+
+
+@pytest.mark.parametrize("W", [3, 24, 33, 64])
+def test_cells_widths(spin, torch, W):
+    """CELLS at widths that select G = 32 / 16 / 8 / 4: equal to BRUTE, and to the oracle."""
+    P, Nn = clouds.clustered(12000, 21)
+    cen = clouds.sample_centres(12000, 200, 22)
+    b = 0.16 / W
+    for mode in ("nearest", "bilinear"):
+        cells = run_gpu(spin, torch, P, Nn, cen, W, b, 0.5, mode, prune="cells")
+        brute = run_gpu(spin, torch, P, Nn, cen, W, b, 0.5, mode)
+        np.testing.assert_array_equal(cells, brute, err_msg=f"W={W} {mode}")
+        ora, st = oracle(P, Nn, cen[:25], W, b, 0.5, mode, cells=True)
+        check(cells[:25], ora, st, mode, f"cells W={W} {mode}")
 
 
 def test_cells_floor_and_literal(spin, torch):
