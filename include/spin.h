@@ -41,7 +41,7 @@ typedef enum {
   SPIN_OK = 0,
   SPIN_E_INVAL = 1,    /* a synchronous argument check failed                        */
   SPIN_E_RANGE = 2,    /* a centre index outside [0, N) (detected on the device)     */
-  SPIN_E_INPUT = 3,    /* non-finite coordinate, or |normal| outside [0.999, 1.001] */
+  SPIN_E_INPUT = 3,    /* non-finite coordinate, |coordinate| > 2^40, or |normal| outside [0.999, 1.001] */
   SPIN_E_NOMEM = 4,    /* device or host allocation failed                           */
   SPIN_E_CUDA = 5,     /* a CUDA runtime error (message carries cudaGetErrorString) */
   SPIN_E_OVERFLOW = 6  /* an accumulator could not hold a bin (see spin_generate)   */
@@ -132,7 +132,7 @@ typedef struct {
  *   N: number of oriented points, 1 <= N < 2^31.
  * Copies and re-lays the cloud out as SoA float4 {x,y,z,|x|^2} + {nx,ny,nz,0} in
  * HBM (the input "replicated to every worker", P:256 / P:333, is resident once).
- * Validates: every coordinate finite, every |normal| in [0.999, 1.001]
+ * Validates: every coordinate finite with |coordinate| <= 2^40, every |normal| in [0.999, 1.001]
  * (SPIN_E_INPUT names the first bad index).  Normals are NOT renormalised (#7).
  * Synchronises `stream`.  The caller may free its arrays when it returns.
  */

@@ -262,7 +262,7 @@ spin_status load_cloud(spin_ctx* h, const float* points, const float* normals, i
   std::memcpy(red, h->h_red, sizeof red);
   const int32_t bad = red[0];
   if (bad != big)
-    return fail(SPIN_E_INPUT, "point %d: non-finite coordinate or |normal| outside [0.999, 1.001]", bad);
+    return fail(SPIN_E_INPUT, "point %d: non-finite coordinate, |coordinate| > 2^40, or |normal| outside [0.999, 1.001]", bad);
   auto unflip = [](int32_t i) { int32_t v = i >= 0 ? i : i ^ 0x7fffffff; float f; std::memcpy(&f, &v, 4); return f; };
   std::memcpy(&h->absmax, &red[1], 4);
   for (int a = 0; a < 6; ++a) h->aabb[a] = unflip(red[2 + a]);
@@ -543,9 +543,37 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   // centre c~ = fl(2(p + mid n))/2 that contains the region cylinder (|beta - mid| <= h,
   // alpha^2 <= Qmax), margin m = B.x - |x|^2 + K with B = 2c~, K = rho^2 - |c~|^2 + 2E
   // (DESIGN.md 7.1).  |c~ - c'| <= u (X + |mid|) widens the radius.
-  const double rho = std::sqrt(rg.h * rg.h + rg.Qmax) + 1.01 * u * (X + amid);
-  const double Ms = rho * rho + (2.0 * X + amid) * (2.0 * X + amid) * 1.01;
-  const double E_sph = 6.0 * u * Ms * 1.05;
+  // Two BRUTE filters share the margin: packed fp32 (FFMA2) and the tensor cores (tf32
+  // mma.sync), whose operands B and K are rounded to tf32: |c~ - c'| <= 2^-11 |c'|.
+  // fp32 error: 5u per term magnitude.  Tensor cores (x, y, z split into tf32 hi + lo,
+  // w = -|x|^2 and K rounded to tf32, exact products, fp32 accumulation): 2^-21 |B||x| +
+  // 2^-12 (|x|^2 + |K|) plus an accumulation allowance of 2^-19 of the summed magnitudes
+  // (and 2^-100 absolute for flushed subnormals).  E bounds the filter in use, so every
+  // region pair keeps m > 0.  The tensor cores are used unless their
+  // looser bound grows the candidate sphere by more than 6% (clouds far from the origin
+  // relative to the region size).
+  auto sphere = [&](bool mma, double& rho_o, double& E_o) {
+    const double shift = 1.01 * (mma ? std::ldexp(1.0, -11) : u) * (X + amid);
+    rho_o = std::sqrt(rg.h * rg.h + rg.Qmax) + shift;
+    const double Ms = rho_o * rho_o + (2.0 * X + amid) * (2.0 * X + amid) * 1.01;
+    E_o = 6.0 * u * Ms * 1.05;
+    if (mma) {
+      const double Kmax = 1.05 * (rho_o * rho_o + (X + amid) * (X + amid)) + 4.0 * E_o;
+      const double BX = 2.02 * (X + amid) * X;
+      E_o += 1.01 * (std::ldexp(1.0, -21) * BX + std::ldexp(1.0, -12) * (X * X + Kmax) +
+                     std::ldexp(1.0, -19) * (BX + X * X + Kmax)) + std::ldexp(1.0, -100);
+    }
+  };
+  double rho, E_sph, rho_f, E_f;
+  sphere(true, rho, E_sph);
+  sphere(false, rho_f, E_f);
+  const bool use_mma = prune == SPIN_BRUTE && std::getenv("SPIN_NO_MMA") == nullptr &&
+                       rho * rho + 3.0 * E_sph <= 1.06 * (rho_f * rho_f + 3.0 * E_f);
+  if (!use_mma) {
+    rho = rho_f;
+    E_sph = E_f;
+  }
+  const double shift = 1.01 * (use_mma ? std::ldexp(1.0, -11) : u) * (X + amid);
   const double Es_h = 4.0 * u * 1.01;
   // CELLS hot loop: the region cylinder in expanded forms (bounds hold inside the region)
   const double Eb_h = 8.0 * u * (X + amid) * 1.01;
@@ -559,6 +587,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   p.Qmax = rg.Qmax;
   p.rho2 = rho * rho;
   p.E_sph = E_sph;
+  p.mma = use_mma ? 1 : 0;
   p.Eq_hot = Eq_h;
   p.h_test = f32_up(rg.h + Eb_h);
   p.c_test = has_support ? f32_down(cos_As - Es_h) : -INFINITY;
@@ -572,7 +601,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
                      : (prune == SPIN_BRUTE ? 2 : 1);
   // candidates satisfy |d| <= D.  BRUTE: |x - c~|^2 <= rho^2 + 4E, so
   // |d| <= |c~ - p| + sqrt(rho^2 + 4E).  CELLS: q <= Qmax + 2Eq, |beta| <= |mid| + h_test + Eb.
-  const double Dh = (amid + 1.01 * u * (X + amid) + std::sqrt(rho * rho + 4.0 * E_sph)) * 1.001;
+  const double Dh = (amid + shift + std::sqrt(rho * rho + 4.0 * E_sph)) * 1.001;
   const double Cmax = (X + amid) * (X + amid) * 1.01;
   const double bmax = amid + (double)p.h_test + Eb_h;
   const double D2c = (rg.Qmax + 2.0 * Eq_h + 4.0 * u * (rg.Qmax + Cmax) + bmax * bmax) * 1.001;

@@ -40,7 +40,8 @@ struct KParams {
   double mid, Qmax;          // beta window centre, alpha^2 bound: region is |beta-mid|<=h, q<=Qmax
   double rho2;               // hot loop: squared radius of the sphere about the (rounded)
                              // window centre that contains the region
-  double E_sph;              // hot-loop bound on the fp32 error of the sphere margin
+  double E_sph;              // hot-loop bound on the error of the sphere margin
+  int32_t mma;               // BRUTE: sphere filter on the tensor cores (tf32 B and K)
   double Eq_hot;             // CELLS hot loop: bound on |q''_fp32 - q''| (added to Qmax - C)
   float c_test, h_test;      // hot loop: s >= c_test (support), CELLS |beta''| <= h_test
   int32_t has_support;
@@ -95,6 +96,10 @@ struct LaunchCfg {
 // ---- launchers implemented in spin_kernels.cu
 LaunchCfg choose_launch(int W, int mode, int prune);
 int tile_points();   // cloud padding: a multiple of every CTA tile (threads x KP points)
+// padding sentinel |x|^2 (finite: the tensor-core filter splits it into tf32 hi/lo parts)
+constexpr float SENTINEL_R2 = 0x1p100f;
+// largest accepted |coordinate| (SPIN_E_INPUT above): |x|^2 and the filter products stay finite
+constexpr float COORD_MAX = 0x1p40f;
 constexpr int KP_POINTS = 4;   // points per thread (register blocking; SPIN_KP)
 int occupancy_blocks(const LaunchCfg& lc, int W, int mode, int prune);
 cudaError_t launch_spin(const LaunchCfg& lc, int mode, int prune, int grid, const KParams& p,

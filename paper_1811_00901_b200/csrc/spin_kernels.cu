@@ -89,14 +89,18 @@ __global__ void k_relayout(const float* __restrict__ pts, const float* __restric
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= Npad) return;
   if (j >= N) {
-    pos[j] = make_float4(0.f, 0.f, 0.f, INFINITY);   // sentinel: |x|^2 = +inf never passes
+    // sentinel: |x|^2 = 2^100 (finite, so the tf32 hi/lo split of the tensor-core filter
+    // stays NaN-free) makes every margin hugely negative: it never passes
+    pos[j] = make_float4(0.f, 0.f, 0.f, SENTINEL_R2);
     nrm4[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     return;
   }
   const float x = pts[3 * j], y = pts[3 * j + 1], z = pts[3 * j + 2];
   const float a = nrm[3 * j], b = nrm[3 * j + 1], c = nrm[3 * j + 2];
   const double n2 = (double)a * a + (double)b * b + (double)c * c;
-  const bool ok = isfinite(x) && isfinite(y) && isfinite(z) && isfinite(a) && isfinite(b) &&
+  // |coordinate| <= 2^40 keeps |x|^2 and every filter product far from fp32 overflow
+  const bool ok = fabsf(x) <= COORD_MAX && fabsf(y) <= COORD_MAX && fabsf(z) <= COORD_MAX &&
+                  isfinite(a) && isfinite(b) &&
                   isfinite(c) && n2 >= 0.999 * 0.999 && n2 <= 1.001 * 1.001;
   if (!ok) atomicMin(bad, (int32_t)min(j, (int64_t)0x7fffffff));
   const double xx = (double)x * x + (double)y * y + (double)z * z;
@@ -252,7 +256,7 @@ __global__ void k_cell_scatter(const float4* __restrict__ pos, const float4* __r
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= Npad) return;
   if (j >= N) {
-    spos[j] = make_float4(0.f, 0.f, 0.f, INFINITY);
+    spos[j] = make_float4(0.f, 0.f, 0.f, SENTINEL_R2);
     snrm[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     return;
   }

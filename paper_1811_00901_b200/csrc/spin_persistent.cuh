@@ -53,6 +53,9 @@
 #ifndef SPIN_HOT_UNROLL
 #define SPIN_HOT_UNROLL 2     // unroll of the sphere-only centre-batch loop
 #endif
+#ifndef SPIN_BRUTE_MMA
+#define SPIN_BRUTE_MMA 1      // BRUTE sphere filter on the tensor cores (0: packed fp32 FFMA2)
+#endif
 #ifndef SPIN_APL_BRUTE512
 #define SPIN_APL_BRUTE512 1   // the same for the 512-thread (W = 32) variant
 #endif
@@ -149,6 +152,22 @@ __device__ __forceinline__ f2 add2(f2 a, f2 b) {
   f2 d;
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
+}
+// ---- tensor-core sphere filter (BRUTE): tf32 operands, legacy mma.sync (HMMA)
+// round to the nearest tf32 (10-bit mantissa, ties away), low 13 bits zero
+__device__ __forceinline__ unsigned tf32u(float x) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float tf32f(float x) { return __uint_as_float(tf32u(x)); }
+// D[16x8] = A[16x8] B[8x8] + C, tf32 in, fp32 accumulate (one HMMA.1688.F32.TF32)
+__device__ __forceinline__ void mma_tf32(float& d0, float& d1, float& d2, float& d3, unsigned a0,
+                                         unsigned a1, unsigned a2, unsigned a3, unsigned b0,
+                                         unsigned b1, float c0, float c1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%11,%10,%11};"
+               : "=f"(d0), "=f"(d1), "=f"(d2), "=f"(d3)
+               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "f"(c0), "f"(c1));
 }
 __device__ __forceinline__ void up2u(f2 v, unsigned& lo, unsigned& hi) {
   asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
@@ -437,6 +456,11 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   // r2 {nx,nx',ny,ny'}, r3 {nz,nz',0,0}
   float4* sT = reinterpret_cast<float4*>(smem + L.oTP) + warp * 32 * KP * 2;
   constexpr int CB = cb_of(G);
+  // BRUTE sphere filter on the tensor cores (mma.sync tf32, hi/lo split of the points):
+  // NCB column blocks of 8 centres, 8 row blocks of 16 points per warp tile
+  constexpr bool MMA_FILTER = PRUNE == 0 && SPIN_BRUTE_MMA;
+  constexpr int NCB = (G + 7) / 8;
+  static_assert(!MMA_FILTER || (NCB == G / CB && KP == 4), "mma mask layout: NCB words per lane");
   unsigned* sMask = reinterpret_cast<unsigned*>(smem + L.oMask) + warp * 32 * (G / CB);
   const int hiWords = (WW + 1) / 2;
   uint32_t* gHi = p.hi_scratch + (size_t)blockIdx.x * G * hiWords;   // zero outside groups
@@ -498,13 +522,18 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
               // BRUTE: sphere of radius rho about c~ = B/2, B = fl(2(p + mid n)) (DESIGN.md
               // 7.1): K = rho^2 - |c~|^2 + 2E rounded up, so the fp32 margin
               // B.x - |x|^2 + K is positive for every pair of the region
-              const float Bx = __double2float_rn(2.0 * ((double)P4.x + mid * N4.x));
-              const float By = __double2float_rn(2.0 * ((double)P4.y + mid * N4.y));
-              const float Bz = __double2float_rn(2.0 * ((double)P4.z + mid * N4.z));
+              // with the tensor-core filter B is rounded to tf32 (an exact operand;
+              // |B - 2c'| <= 2^-11 |2c'|, the planner's rho covers the shift of c~)
+              float Bx = __double2float_rn(2.0 * ((double)P4.x + mid * N4.x));
+              float By = __double2float_rn(2.0 * ((double)P4.y + mid * N4.y));
+              float Bz = __double2float_rn(2.0 * ((double)P4.z + mid * N4.z));
+              if (MMA_FILTER && p.mma) { Bx = tf32f(Bx); By = tf32f(By); Bz = tf32f(Bz); }
               const double cx = 0.5 * Bx, cy = 0.5 * By, cz = 0.5 * Bz;
               const double K = p.rho2 - (cx * cx + cy * cy + cz * cz) + 2.0 * p.E_sph;
+              float Kf = __double2float_ru(K);
+              if (MMA_FILTER && p.mma) Kf = tf32f(Kf);   // a tensor-core operand too (in E)
               A4 = make_float4(N4.x, N4.y, N4.z, 0.f);
-              B4 = make_float4(Bx, By, Bz, __double2float_ru(K));
+              B4 = make_float4(Bx, By, Bz, Kf);
             } else {
               // CELLS: the region cylinder itself, beta'' = n.x - n.p - mid and
               // -q'' = beta''^2 + 2(p + mid n).x - |x|^2 - C >= -Qt
@@ -581,11 +610,33 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       constexpr int NWD = G / CB;                      // mask words per lane per tile
       // candidate operands: centre slot gs, point (source lane, k) from the staged tile
       // entry = (mask word w << 10) | (source lane << 5) | mask bit (k << 3 | c)
-      auto load_entry = [&](unsigned e, float4& P4, float4& N4, float4& X4, float4& NX4) {
-        const int gs = (int)(e >> 10) * CB + (int)(e & 7u);
+      // Tiles filtered on the tensor cores (BRUTE, support test not in the hot loop) use
+      // the mma layout: mask word w of lane L holds bit (j << 3) | (s & 7) for output j
+      // of HMMA s = 8w + (s & 7) = rb * NCB + cb: centre slot (2(L&3) + (j&1)) * NCB + cb
+      // and row r = (L>>2) + 8(j>>1) of row block rb, staged at lane (rb&3)*8 + ((r+rb)&7),
+      // point (rb>>2)*2 + (r>>3).  (Slots and rows are spread so that one lane's
+      // candidates read different shared-memory banks in the accept passes.)
+      bool tile_mma = false;
+      auto decode_entry = [&](unsigned e, int& gs, int& sl, int& kk) {
+        if (MMA_FILTER && tile_mma) {
+          const int bit = (int)(e & 31u), ln = (int)(e >> 5) & 31;
+          const int sidx = (int)(e >> 10) * 8 + (bit & 7), jv = bit >> 3;
+          const int rb = sidx / NCB, cbk = sidx - rb * NCB;
+          gs = (2 * (ln & 3) + (jv & 1)) * NCB + cbk;
+          const int r = (ln >> 2) + 8 * (jv >> 1);
+          sl = (rb & 3) * 8 + ((r + rb) & 7);
+          kk = (rb >> 2) * 2 + (r >> 3);
+        } else {
+          gs = (int)(e >> 10) * CB + (int)(e & 7u);
+          sl = (int)(e >> 5) & 31;    // source lane
+          kk = (int)(e >> 3) & 3;     // point k of that lane
+        }
+      };
+      auto load_entry = [&](unsigned e, int& gs, float4& P4, float4& N4, float4& X4, float4& NX4) {
+        int sl, kk;
+        decode_entry(e, gs, sl, kk);
         P4 = sP[gs];
         N4 = sN[gs];
-        const int sl = (int)(e >> 5) & 31, kk = (int)(e >> 3) & 3;   // source lane, point k
         const float* rec = reinterpret_cast<const float*>(sT + (kk >> 1) * 32 + sl) + (kk & 1);
         constexpr int RS = (KP / 2) * 32 * 4;                       // floats between records
         X4 = make_float4(rec[0], rec[2], rec[RS], 0.f);
@@ -598,12 +649,13 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       constexpr int APL = PRUNE == 1 ? (MODE == 1 ? SPIN_APL_CELLS : 1) : (NT == 512 ? SPIN_APL_BRUTE512 : SPIN_APL_BRUTE);
       auto process_pair = [&](unsigned e0, bool v0, unsigned e1, bool v1) {
         float4 P0, N0, X0, NX0, P1, N1, X1, NX1;
-        load_entry(e0, P0, N0, X0, NX0);
+        int g0, g1 = 0;
+        load_entry(e0, g0, P0, N0, X0, NX0);
         Dec d0 = decide<MODE>(p, P0, N0, X0, NX0);
         Dec d1;
         d1.status = 0;
         if (APL == 2) {
-          load_entry(e1, P1, N1, X1, NX1);
+          load_entry(e1, g1, P1, N1, X1, NX1);
           d1 = decide<MODE>(p, P1, N1, X1, NX1);
           if (!v1) d1.status = 0;
         }
@@ -612,7 +664,6 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         if (SUP == 2) ct.srej += (unsigned)(v0 & (d0.sup_out != 0));
         if (d0.status == 2) resolve<MODE>(p, d0, P0, N0, X0, NX0, ct);
         if (APL == 2 && d1.status == 2) resolve<MODE>(p, d1, P1, N1, X1, NX1, ct);
-        const int g0 = (int)(e0 >> 10) * CB + (int)(e0 & 7u), g1 = (int)(e1 >> 10) * CB + (int)(e1 & 7u);
         if (d0.status) { ++ct.acc; apply<MODE, G>(p, d0, sImg + g0 * WW, g0, &s_carry); }
         if (APL == 2 && d1.status) {
           ++ct.acc;
@@ -790,6 +841,71 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           sT[(3 * (KP / 2) + pr) * 32 + lane] = make_float4(b0.z, b1.z, 0.f, 0.f);
         }
         __syncwarp();
+        const bool sup_hot = SUP == 1 || (SUP == 2 && sup_on);
+        tile_mma = MMA_FILTER && p.mma && !sup_hot;
+        if (MMA_FILTER && p.mma && !sup_hot) {
+          // sphere margins m = B.x - |x|^2 + K of 16 points x 8 centres per HMMA:
+          // A = the points as (x, y, z, -|x|^2) split into tf32 hi and lo parts (columns
+          // 0-3 and 4-7; x = hi + lo + O(2^-22 |x|)), B = (Bx, By, Bz, 1) twice (B is tf32
+          // exactly), C = K.  The planner's E bounds the tf32 / accumulation error, so
+          // every pair of the region still has m > 0.
+          const int gid = lane >> 2, tig = lane & 3;
+          // A = 16 points x 8: (x_hi, y_hi, z_hi, w_hi, x_lo, y_lo, z_lo, 1), w = -|x|^2;
+          // B = 8 centres x 8: (Bx, By, Bz, 1, Bx, By, Bz, K) (B and K tf32 exactly), so
+          // D = B.(x_hi + x_lo) + w_hi + K with no accumulator input.  Thread (gid, tig)
+          // supplies component tig of rows gid and gid + 8 (records r0 {x,x',y,y'},
+          // r1 {z,z',-|x|^2,-|x'|^2} of the staged pair layout; see decode_entry).
+          // hi = round to nearest tf32 (half an ulp of the 10-bit mantissa added, low 13
+          // bits cleared; every |value| here is below 2^101), lo = x - hi (exact) cut to
+          // tf32: |x - hi - lo| <= 2^-21 |x|, |w - w_hi| <= 2^-12 |w| (planner's E_mma)
+          const float* sTf = reinterpret_cast<const float*>(sT);
+          // B fragments of the group's centres (column gid = centre slot gid*NCB + cb,
+          // rows tig and tig + 4)
+          unsigned bu0[NCB], bu1[NCB];
+          const float* sBf = reinterpret_cast<const float*>(sB);
+#pragma unroll
+          for (int cb = 0; cb < NCB; ++cb) {
+            const int sb = gid * NCB + cb;
+            float b1 = sBf[(G >= 8 || sb < G ? sb : 0) * 4 + tig];
+            float b0 = tig == 3 ? 1.0f : b1;
+            if (G < 8 && sb >= G) {   // no such centre: margin -inf
+              b0 = 0.0f;
+              b1 = tig == 3 ? -INFINITY : 0.0f;
+            }
+            bu0[cb] = __float_as_uint(b0);
+            bu1[cb] = __float_as_uint(b1);
+          }
+          unsigned rej[NCB];
+#pragma unroll
+          for (int w = 0; w < NCB; ++w) rej[w] = 0u;
+#pragma unroll
+          for (int rb = 0; rb < 8; ++rb) {
+            // rows gid and gid + 8: staged lane (rb&3)*8 + ((gid+rb)&7), points
+            // (rb>>2)*2 + 0 / 1 = the two halves of one pair record (adjacent floats)
+            const int sl = (rb & 3) * 8 + ((gid + rb) & 7);
+            const float2 v01 = *reinterpret_cast<const float2*>(
+                sTf + (((tig >> 1) * (KP / 2) + (rb >> 2)) * 32 + sl) * 4 + 2 * (tig & 1));
+            const float v0 = v01.x, v1 = v01.y;
+            const unsigned h0 = (__float_as_uint(v0) + 0x1000u) & 0xffffe000u;
+            const unsigned h1 = (__float_as_uint(v1) + 0x1000u) & 0xffffe000u;
+            const unsigned l0 = tig == 3 ? 0x3f800000u : __float_as_uint(v0 - __uint_as_float(h0)) & 0xffffe000u;
+            const unsigned l1 = tig == 3 ? 0x3f800000u : __float_as_uint(v1 - __uint_as_float(h1)) & 0xffffe000u;
+            // all NCB products of the row block in flight before their sign gather
+            float d[NCB][4];
+#pragma unroll
+            for (int cb = 0; cb < NCB; ++cb)
+              mma_tf32(d[cb][0], d[cb][1], d[cb][2], d[cb][3], h0, h1, l0, l1, bu0[cb], bu1[cb], 0.0f, 0.0f);
+#pragma unroll
+            for (int cb = 0; cb < NCB; ++cb) {
+              const int sidx = rb * NCB + cb;
+              rej[sidx >> 3] = reject_bits4(rej[sidx >> 3], __float_as_uint(d[cb][0]), __float_as_uint(d[cb][1]),
+                                            __float_as_uint(d[cb][2]), __float_as_uint(d[cb][3]),
+                                            0x01010101u << (sidx & 7));
+            }
+          }
+#pragma unroll
+          for (int w = 0; w < NCB; ++w) sMask[w * 32 + lane] = ~rej[w];
+        } else {
 #pragma unroll
         for (int pr = 0; pr < KP / 2; ++pr) {
           f2 r[8];
@@ -802,7 +918,6 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           NX2[pr] = r[4]; NY2[pr] = r[5]; NZ2[pr] = r[6];
         }
         const float c_test = p.c_test, h_test = p.h_test;
-        const bool sup_hot = SUP == 1 || (SUP == 2 && sup_on);
         // a partial group skips its empty batches (their mask words are zero)
         const int cb_end = ((gcount + CB - 1) / CB) * CB;
         for (int cb = cb_end; cb < G; cb += CB) sMask[(cb / CB) * 32 + lane] = 0u;
@@ -884,6 +999,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             }
             sMask[(cb / CB) * 32 + lane] = mask;
           }
+        }
         }
         __syncwarp();
         if (p.debug_skip < 2) compact_and_accept();
