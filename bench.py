@@ -207,12 +207,47 @@ def oracle_sample(cfg, P, Nn, cen, mode, seconds):
     return done, pairs, dt
 
 
+THREAD_VARS = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")
+
+
+def _oracle_worker(job):
+    """One host core: the oracle on an interleaved slice of the images, time-bounded."""
+    cfg, P, Nn, cen, mode, seconds = job
+    return oracle_sample(cfg, P, Nn, cen, mode, seconds)
+
+
+def oracle_parallel(cfg, P, Nn, cen, mode, seconds, cores=None):
+    """The oracle as it stands, one process per host core (spawned: no CUDA state is
+    inherited), each on every cores-th image; throughput = all pairs / the slowest
+    worker's own time (process start-up excluded)."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+    cores = cores or len(os.sched_getaffinity(0))
+    jobs = [(cfg, P, Nn, cen[i::cores], mode, seconds) for i in range(cores)]
+    saved = {k: os.environ.get(k) for k in THREAD_VARS}
+    os.environ.update({k: "1" for k in THREAD_VARS})   # one thread per worker process
+    try:
+        with cf.ProcessPoolExecutor(cores, mp_context=mp.get_context("spawn")) as ex:
+            res = list(ex.map(_oracle_worker, jobs))
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    done = sum(r[0] for r in res)
+    pairs = sum(r[1] for r in res)
+    dt = max(r[2] for r in res)
+    return done, pairs, dt, cores
+
+
 def cpu_baseline_dict(cfg, P, Nn, cen, mode, seconds):
-    done, pairs, dt = oracle_sample(cfg, P, Nn, cen, mode, seconds)
+    done, pairs, dt, cores = oracle_parallel(cfg, P, Nn, cen, mode, seconds)
     kind = "visited" if cfg["prune"] == "cells" else "all"
-    return {"value": pairs / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"first {done} of {len(cen)} images of {cfg['name']} ({kind} pairs, "
-                      f"numpy float64 + exact fallback, single thread, {dt:.1f} s)",
+    return {"value": pairs / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{done} of {len(cen)} images of {cfg['name']} ({kind} pairs, numpy float64 "
+                      f"+ exact fallback; {cores} processes, one per host core, each on every "
+                      f"{cores}-th image for {seconds:.0f} s; {dt:.1f} s slowest worker)",
             "images_per_s": done / dt}
 
 
@@ -231,8 +266,9 @@ def run_reference(args):
     for _ in range(args.warmup):
         oracle_sample(cfg, P, Nn, cen, mode, min(per, 2.0))
     tot_pairs, tot_t, tot_img = 0, 0.0, 0
+    cores = 1
     for _ in range(args.steps):
-        d, p, t = oracle_sample(cfg, P, Nn, cen, mode, per)
+        d, p, t, cores = oracle_parallel(cfg, P, Nn, cen, mode, per)
         tot_pairs += p
         tot_t += t
         tot_img += d
@@ -244,9 +280,10 @@ def run_reference(args):
             "config": {"workload": cfg["name"], "N": cfg["N"], "M": cfg["M"], "W": cfg["W"],
                        "b": cfg["b"], "cos_As": cfg["cos_As"], "mode": mode, "prune": cfg["prune"],
                        "sample": "each step: images of the workload in order for a bounded time"},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{tot_img} images of {cfg['name']} over {args.steps} steps "
-                                       f"(numpy float64 + exact fallback, single thread)"},
+                                       f"(numpy float64 + exact fallback, {cores} processes, "
+                                       f"one per host core)"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "images_per_s": tot_img / tot_t}
     print(json.dumps(line), flush=True)
@@ -443,6 +480,12 @@ def run_spin(args):
                      "unit": "TFLOP/s", "frac": achieved_tflops / FP32_PEAK_TFLOPS,
                      "traffic": load_traffic(cfg["name"], mode),
                      "kernel": "spin_persistent", "kernel_ms": kern,
+                     "filter": ("sphere margin on the tensor cores (mma.sync m16n8k8 tf32, "
+                                "hi/lo split)" if st0.get("filter_mma") else
+                                "packed fp32 (FFMA2)"),
+                     "note": "frac = pair throughput in the paper formulation's flops "
+                             "(20 per pair) over the FP32 peak (north-star metric); the "
+                             "kernel itself is issue/ALU-pipe bound (DESIGN.md 7.2)",
                      "flop_per_pair": FLOP_PER_PAIR,
                      "peak_source": "derived 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md); "
                                     "FFMA microbenchmark measured 72.5 TFLOP/s",

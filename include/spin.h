@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SPIN_ABI_VERSION 4
+#define SPIN_ABI_VERSION 5
 
 typedef struct spin_ctx* spin_handle;
 typedef struct CUstream_st* spin_stream; /* identical to cudaStream_t */
@@ -123,6 +123,9 @@ typedef struct {
   int32_t cta_capacity;     /* length of the three arrays above                            */
   int64_t tiles_support_hot; /* BRUTE: warp tiles (32 x 4 points x G centres) whose hot
                                  loop ran the support test (adaptive placement)             */
+  int32_t filter_mma;       /* BRUTE: 1 if the sphere filter ran on the tensor cores (tf32
+                               mma.sync), 0 if on packed fp32 (far-from-origin clouds,
+                               SPIN_NO_MMA, or CELLS)                                         */
 } spin_stats;
 
 /*

@@ -779,6 +779,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
     stats->fp64_fallbacks = (int64_t)sv[ST_F64];
     stats->exact_fallbacks = (int64_t)sv[ST_EXACT];
     stats->tiles_support_hot = (int64_t)sv[ST_SUPHOT];
+    stats->filter_mma = p.mma;
     stats->P = grid;
     stats->G = lc.G;
     stats->n_units = (int32_t)n_units;

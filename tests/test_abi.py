@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), f"libspin.so does not export {n}"
     assert set(names) == set(spin.EXPORTS)
-    assert spin.abi_version() == 4
+    assert spin.abi_version() == 5
 
 
 def test_binding_has_no_cpu_fallback():
