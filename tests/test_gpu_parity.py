@@ -584,3 +584,30 @@ def test_count_in_sphere_matches_numpy(spin, torch):
         d = X - X[c]
         want += int(np.count_nonzero((d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2] <= R * R))
     assert got == want
+
+
+def test_tensor_core_filter_selection_and_parity(spin, torch):
+    """The BRUTE sphere filter runs on the tensor cores (tf32 mma.sync)
+    for clouds near the origin and falls back to packed fp32 where the tf32 bound would
+    loosen the sphere (far from the origin); both give oracle-exact NEAREST images, and
+    the fp32 arm forced by SPIN_NO_MMA gives the identical images."""
+    P, Nn = clouds.bumpy_sphere(4000, 21)
+    cen = np.arange(0, 4000, 13, dtype=np.int32)
+    gpu, st = run_gpu(spin, torch, P, Nn, cen, 16, 0.02, 0.5, "nearest", stats=True)
+    assert st["filter_mma"] == 1
+    ora, ost = oracle(P, Nn, cen, 16, 0.02, 0.5, "nearest")
+    check(gpu, ora, ost, "nearest", "tensor-core filter")
+    os.environ["SPIN_NO_MMA"] = "1"
+    try:
+        g2, st2 = run_gpu(spin, torch, P, Nn, cen, 16, 0.02, 0.5, "nearest", stats=True)
+    finally:
+        del os.environ["SPIN_NO_MMA"]
+    assert st2["filter_mma"] == 0
+    assert np.array_equal(gpu, g2)
+    # candidates: the tf32 sphere may only be slightly looser than the fp32 one
+    assert 0.99 * st2["pairs_candidate"] <= st["pairs_candidate"] <= 1.06 * st2["pairs_candidate"]
+    Pf = (P.astype(np.float64) + np.asarray([1e4, 0.0, 0.0])).astype(np.float32)
+    g3, st3 = run_gpu(spin, torch, Pf, Nn, cen[:40], 16, 0.02, 0.5, "nearest", stats=True)
+    assert st3["filter_mma"] == 0
+    ora3, ost3 = oracle(Pf, Nn, cen[:40], 16, 0.02, 0.5, "nearest")
+    check(g3, ora3, ost3, "nearest", "far cloud, fp32 filter")
