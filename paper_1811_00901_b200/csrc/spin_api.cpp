@@ -622,6 +622,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   p.inv_b = (float)(1.0 / b);
   p.inv_b2 = (float)(1.0 / (b * b));
   p.Af = (float)p.A;
+  p.Wf = (float)W;
   p.Au = (flags & SPIN_F_LITERAL_HALF_WIDTH) ? (float)(p.A / b) : (float)p.A;
   p.floor_f = (flags & SPIN_F_FLOOR_BINS) ? 1.0f : 0.0f;
   p.Es_a = f32_up(Es_a);

@@ -53,6 +53,7 @@ struct KParams {
   // accept path, fp32 stage
   float c_f;                 // (float)cos_As, its rounding is inside Es_a
   float inv_b, inv_b2, Af;
+  float Wf;                  // (float)W
   float Au;                  // u = fma(-beta, inv_b, Au): W/2 (scaled) or fl32(W/(2b)) (literal)
   float floor_f;             // 1.0 for SPIN_F_FLOOR_BINS, else 0.0
   float self_kf;             // (float)self_k

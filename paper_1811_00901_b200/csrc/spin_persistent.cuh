@@ -242,9 +242,8 @@ __host__ __device__ inline Layout make_layout(int G, int W, int mode, int prune,
   L.oP = o; o += 16 * (size_t)G;
   L.oN = o; o += 16 * (size_t)G;
   L.oM = o; o = align16(o + 4 * (size_t)G);
-  const size_t WW = (size_t)W * W;
-  L.oImg = o; o = align16(o + 4 * (size_t)img_stride(W, mode, prune) * G);
-  L.oHi = o;
+  // everything but the images has a compile-time offset (G, NT, mode, prune are template
+  // constants); the images, whose size depends on the runtime W, go last
   L.oQ = o; o += 2 * (size_t)qcap_of(prune, G) * NWARP;
   o = align16(o);
   L.oTP = o; o += 32 * (size_t)32 * KP * NWARP;    // per-warp staged tile, pair layout (32 B/point)
@@ -258,6 +257,8 @@ __host__ __device__ inline Layout make_layout(int G, int W, int mode, int prune,
     o += 4 * (ROWCAP + 1);
     o = align16(o);
   }
+  L.oImg = o; o = align16(o + 4 * (size_t)img_stride(W, mode, prune) * G);
+  L.oHi = o;
   L.total = o;
   return L;
 }
@@ -313,7 +314,7 @@ struct Dec {
 template <int MODE>
 __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const float4 N4,
                                       const float4 X4, const float4 NX4) {
-  const float Wf = (float)p.W, Wm1 = Wf - 1.0f;
+  const float Wf = p.Wf, Wm1 = Wf - 1.0f;
   const float d0 = __fsub_rn(X4.x, P4.x), d1 = __fsub_rn(X4.y, P4.y), d2 = __fsub_rn(X4.z, P4.z);
   // support test, inclusive, cosine form (#5); c_f = -inf disables it (ds = +inf)
   const float s = fmaf(N4.x, NX4.x, fmaf(N4.y, NX4.y, N4.z * NX4.z));
