@@ -289,6 +289,13 @@ __device__ __forceinline__ float rint_magic(float x) {
   return __fsub_rn(__fadd_rn(x, 12582912.0f), 12582912.0f);
 }
 
+// k*W + l for integral floats k, l in [0, W) (< 2^12) on the FMA pipe: the float sum is
+// exact, +2^23 puts the integer in the low mantissa bits (no F2I on the XU pipe).  Used
+// only for certified verdicts; other lanes may carry garbage, masked in range.
+__device__ __forceinline__ int bin_index(float k, float l, float Wf) {
+  return (int)(__float_as_uint(__fadd_rn(__fmaf_rn(k, Wf, l), 8388608.0f)) & 0x7fffffu);
+}
+
 // The slow stages, out of line; operands by value so the fast path keeps no stack.
 static __device__ __noinline__ SlowOut slow_pair(float4 P4, float4 N4, float4 X4, float4 NX4, int W,
                                           double A, double b, double cos_As, int has_support,
@@ -356,7 +363,7 @@ __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const f
     if (self) { kf = p.self_kf; lf = 0.0f; ku = false; lu = false; }
     const bool out = (!ku & ((kf < 0.0f) | (kf >= Wf))) | (!lu & (lf >= Wf));
     r.status = (sup_out | (!unc0 & out)) ? 0 : ((unc0 | ku | lu) ? 2 : 1);
-    r.bin = (int)kf * p.W + (int)lf;
+    r.bin = bin_index(kf, lf, Wf);
   } else {
     // BILINEAR region 0 <= u < W-1, w < (W-1)^2  (#12); the self pair (u = W/2, w = 0)
     // is interior for W >= 3 and needs no special case
@@ -374,7 +381,7 @@ __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const f
     const float fj = fminf(fmaxf(rint_magic(v - 0.5f), 0.0f), Wm1 - 1.0f);
     r.a = fminf(fmaxf(uval - fi, 0.0f), 1.0f);
     r.c = fminf(fmaxf(v - fj, 0.0f), 1.0f);
-    r.bin = (int)fi * p.W + (int)fj;
+    r.bin = bin_index(fi, fj, Wf);
   }
   return r;
 }
