@@ -238,7 +238,18 @@ def oracle_parallel(cfg, P, Nn, cen, mode, seconds, cores=None):
     done = sum(r[0] for r in res)
     pairs = sum(r[1] for r in res)
     dt = max(r[2] for r in res)
+    oracle_parallel.per_core = statistics.mean(r[1] / r[2] for r in res if r[2] > 0)
     return done, pairs, dt, cores
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def cpu_baseline_dict(cfg, P, Nn, cen, mode, seconds):
@@ -248,7 +259,8 @@ def cpu_baseline_dict(cfg, P, Nn, cen, mode, seconds):
             "sample": f"{done} of {len(cen)} images of {cfg['name']} ({kind} pairs, numpy float64 "
                       f"+ exact fallback; {cores} processes, one per host core, each on every "
                       f"{cores}-th image for {seconds:.0f} s; {dt:.1f} s slowest worker)",
-            "images_per_s": done / dt}
+            "images_per_s": done / dt, "per_core_value": oracle_parallel.per_core,
+            "cpu_model": cpu_model()}
 
 
 def run_reference(args):

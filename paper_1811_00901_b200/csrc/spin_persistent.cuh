@@ -59,6 +59,9 @@
 #ifndef SPIN_IMG_PAD
 #define SPIN_IMG_PAD 1        // 1: odd image stride in shared memory for CELLS BILINEAR (0: W^2)
 #endif
+#ifndef SPIN_IMG_PAD_BRUTE
+#define SPIN_IMG_PAD_BRUTE 1  // the odd stride for BRUTE BILINEAR too (C4 401 -> 398 ms)
+#endif
 #ifndef SPIN_APL_BRUTE512
 #define SPIN_APL_BRUTE512 1   // the same for the 512-thread (W = 32) variant
 #endif
@@ -223,11 +226,11 @@ __device__ __forceinline__ unsigned reject_bits4(unsigned rej, unsigned m0, unsi
 }
 
 // ------------------------------------------------------------------ smem layout
-// Shared-memory image stride in words.  CELLS BILINEAR: odd (W^2 or W^2 + 1), so the same
-// bin of neighbouring images falls in different banks (measured: C3 43.8 -> 41.8 ms; for
-// BRUTE and NEAREST the padding measured 1-3% slower)
+// Shared-memory image stride in words.  BILINEAR: odd (W^2 or W^2 + 1), so the same bin
+// of neighbouring images falls in different banks (measured: C3 43.8 -> 41.8 ms, C4 401 ->
+// 398 ms; for NEAREST the padding measured 1-3% slower)
 __host__ __device__ constexpr int img_stride(int W, int mode, int prune) {
-  return (mode == 1 && prune == 1) ? ((W * W) | SPIN_IMG_PAD) : W * W;
+  return (mode == 1 && (prune == 1 || SPIN_IMG_PAD_BRUTE)) ? ((W * W) | SPIN_IMG_PAD) : W * W;
 }
 struct Layout {
   size_t oA, oB, oP, oN, oM, oImg, oHi, oQ, oTP, oTN, oMask, oRowS, oRowO, total;
