@@ -225,6 +225,17 @@ __device__ __forceinline__ unsigned reject_bits4(unsigned rej, unsigned m0, unsi
   return d;
 }
 
+// the same gather for "accepted" bits: acc | (K & ~sign bytes) in the final LOP3
+__device__ __forceinline__ unsigned accept_bits4(unsigned acc, unsigned m0, unsigned m1,
+                                                 unsigned m2, unsigned m3, unsigned K) {
+  unsigned a, b, c, d;
+  asm("prmt.b32 %0, %1, %2, 0xfbfb;" : "=r"(a) : "r"(m0), "r"(m1));
+  asm("prmt.b32 %0, %1, %2, 0xfbfb;" : "=r"(b) : "r"(m2), "r"(m3));
+  asm("prmt.b32 %0, %1, %2, 0x7610;" : "=r"(c) : "r"(a), "r"(b));
+  asm("lop3.b32 %0, %1, %2, %3, 0xae;" : "=r"(d) : "r"(c), "r"(K), "r"(acc));
+  return d;
+}
+
 // ------------------------------------------------------------------ smem layout
 // Shared-memory image stride in words.  BILINEAR: odd (W^2 or W^2 + 1), so the same bin
 // of neighbouring images falls in different banks (measured: C3 43.8 -> 41.8 ms, C4 401 ->
@@ -896,9 +907,9 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             bu0[cb] = __float_as_uint(b0);
             bu1[cb] = __float_as_uint(b1);
           }
-          unsigned rej[NCB];
+          unsigned accm[NCB];
 #pragma unroll
-          for (int w = 0; w < NCB; ++w) rej[w] = 0u;
+          for (int w = 0; w < NCB; ++w) accm[w] = 0u;
 #pragma unroll
           for (int rb = 0; rb < 8; ++rb) {
             // rows gid and gid + 8: staged lane (rb&3)*8 + ((gid+rb)&7), points
@@ -919,13 +930,13 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
 #pragma unroll
             for (int cb = 0; cb < NCB; ++cb) {
               const int sidx = rb * NCB + cb;
-              rej[sidx >> 3] = reject_bits4(rej[sidx >> 3], __float_as_uint(d[cb][0]), __float_as_uint(d[cb][1]),
-                                            __float_as_uint(d[cb][2]), __float_as_uint(d[cb][3]),
-                                            0x01010101u << (sidx & 7));
+              accm[sidx >> 3] = accept_bits4(accm[sidx >> 3], __float_as_uint(d[cb][0]), __float_as_uint(d[cb][1]),
+                                             __float_as_uint(d[cb][2]), __float_as_uint(d[cb][3]),
+                                             0x01010101u << (sidx & 7));
             }
           }
 #pragma unroll
-          for (int w = 0; w < NCB; ++w) sMask[w * 32 + lane] = ~rej[w];
+          for (int w = 0; w < NCB; ++w) sMask[w * 32 + lane] = accm[w];
         } else {
 #pragma unroll
         for (int pr = 0; pr < KP / 2; ++pr) {
