@@ -1,6 +1,6 @@
 // spin_persistent.cuh — the persistent spin kernel of the hot path (sm_100a).
 // Instantiated in spin_inst_*.cu (one translation unit per (mode, support) pair so the
-// 40 variants compile in parallel); dispatched from spin_kernels.cu.
+// 56 variants compile in parallel); dispatched from spin_kernels.cu.
 //
 // Persistent spin kernel: P resident CTAs; each CTA
 // asks the device "master" (one u32 in global memory) for the next chunk of the
@@ -11,8 +11,10 @@
 //   a8  streams the cloud through registers (BRUTE: all N points, Alg. 1's inner
 //       loop P:161; CELLS: the grid rows around the group), each thread holding K
 //       points that are reused against all G centres (n-body blocking),
-//   a9  runs the conservative fp32 pair test — support n.nx >= cos_As,
-//       beta window and alpha^2 bound — packing pass bits into a mask,
+//   a9  runs the conservative pair test — BRUTE: the region's bounding sphere as a tf32
+//       tensor-core GEMM (mma.sync, points split hi/lo), or on packed fp32 with the
+//       support n.nx >= cos_As; CELLS: beta window and alpha^2 bound
+//        plus support on packed fp32 — packing pass bits into a mask,
 //   a10 compacts candidates into a per-warp shared-memory queue and processes them
 //       32 at a time: exact-certified bin decision, shared-memory u32 atomics
 //       (NEAREST ++) or 2^-23 fixed point (BILINEAR),
@@ -20,7 +22,7 @@
 //       (spin_exact.cuh),
 //   a12 writes the G images to out[m] in the caller's order (add(spinImages)),
 //   a13 records %globaltimer start/finish and units per CTA (fig:loadim).
-// No tensor cores: the pair test is not a contraction.
+// Tensor cores only for the BRUTE sphere margin, a genuine bilinear form.
 #pragma once
 #include <cstdint>
 #include <cfloat>
