@@ -50,8 +50,20 @@ typedef enum {
 /* Loop schedules of PAPER.md §2.2.  STATIC = PSIA's fixed blocks
  * (P:476-477); SS = one unit per request; GSS = ceil(R/P) per request
  * (P:224-228); FAC = batches of P equal chunks, size ceil(R_batch/(2P))
- * (the FAC2 reading). */
-typedef enum { SPIN_STATIC = 0, SPIN_SS = 1, SPIN_GSS = 2, SPIN_FAC = 3 } spin_schedule;
+ * (the FAC2 reading).
+ * Beyond the paper (its "more complex DLS techniques" future work; SURVEY §8(f)
+ * NEXT-4): WF = weighted factoring — FAC2 batches of P chunks, but the chunk a worker
+ * receives is weighted by its relative speed w_i (mean 1):
+ * ceil(R_batch * wq_i / (fac_divisor * P * 1024)) with wq_i = round(1024 w_i); the
+ * speeds are known a priori — here those of the heterogeneous-worker emulation below
+ * (slow CTAs 1/slowdown, the rest 1, normalised to mean 1).  AWF = adaptive weighted
+ * factoring — the same rule with w_i = the worker's measured rate (units per busy time
+ * over its chunks so far) over the mean rate of the workers that have reported (1 before
+ * a worker's first chunk).  WF/AWF chunks depend on who requests, so they are claimed on
+ * the device by a compare-and-swap on the packed batch state; they need n_units < 2^24,
+ * P < 2^16 and no shared multi-device dealer. */
+typedef enum { SPIN_STATIC = 0, SPIN_SS = 1, SPIN_GSS = 2, SPIN_FAC = 3, SPIN_WF = 4,
+               SPIN_AWF = 5 } spin_schedule;
 
 /* NEAREST: the paper's integer count tempSpinImage[k,l]++ (P:173-174).
  * BILINEAR: weight 1 split over the 4 bins around (u, v) (north star; not in the
@@ -203,6 +215,9 @@ spin_status spin_generate_host(spin_handle h, const int32_t* h_centre_idx, int64
  * writes the chunk boundaries b_0 = 0 < b_1 < ... < b_n = n_units into h_bounds
  * (capacity `cap` entries, n_chunks + 1 needed) and the chunk count into *n_chunks.
  * SPIN_E_RANGE if cap is too small (*n_chunks still set).  P >= 1, n_units >= 0.
+ * SPIN_WF: the sequence for requests in round-robin worker order 0, 1, ..., P-1, 0, ...
+ * with the weights cp implies; SPIN_AWF (measured weights) has no static trace:
+ * SPIN_E_INVAL.
  */
 spin_status spin_chunk_sequence(spin_schedule sched, int64_t n_units, int32_t P,
                                 const spin_chunk_params* cp, int64_t* h_bounds, int64_t cap,

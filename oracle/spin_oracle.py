@@ -391,10 +391,21 @@ def generate_cells(points, normals, centre_idx, W: int, b: float, cos_As: float,
 
 # ============================================================================ scheduling
 
-STATIC, SS, GSS, FAC = 0, 1, 2, 3
+STATIC, SS, GSS, FAC, WF, AWF = 0, 1, 2, 3, 4, 5
 
 
-def chunk_sizes(kind: int, n: int, P: int, gss_min_chunk: int = 1, fac_divisor: int = 2):
+def wf_integer_weights(P: int, slow: int, slowdown: float):
+    """Weighted factoring's relative speeds for the heterogeneous-worker emulation
+    (spin.h SPIN_WF): slow workers 1/slowdown, the rest 1, normalised to mean 1, as
+    integers round(1024 w) (at least 1)."""
+    S = min(max(slow, 0), P)
+    ws = 1.0 / slowdown if slowdown > 1.0 else 1.0
+    mean = (S * ws + (P - S)) / P
+    return [max(1, math.floor(1024.0 * (ws if i < S else 1.0) / mean + 0.5)) for i in range(P)]
+
+
+def chunk_sizes(kind: int, n: int, P: int, gss_min_chunk: int = 1, fac_divisor: int = 2,
+                slow: int = 0, slowdown: float = 1.0):
     """Chunk sizes of the paper's loop schedules (§2.2).
 
     STATIC: P near-equal blocks, the first n mod P of size ceil(n/P) (#17)
@@ -402,7 +413,10 @@ def chunk_sizes(kind: int, n: int, P: int, gss_min_chunk: int = 1, fac_divisor: 
     GSS   : ceil(remaining / P) per request, at least gss_min_chunk (#16)
     FAC   : batches of P equal chunks, ceil(R_batch / (fac_divisor * P)) (P:229-230,
             FAC2 reading #15)
-    Every chunk is capped at the remaining count.
+    WF    : weighted factoring (beyond the paper, its future work P:238): batches of P
+            chunks, worker i's chunk ceil(R_batch * wq_i / (fac_divisor * P * 1024)),
+            requests in round-robin worker order; with equal weights it is FAC
+    Every chunk is capped at the remaining count and is at least 1.
     """
     if P < 1 or n < 0:
         raise ValueError("need P >= 1 and n >= 0")
@@ -430,6 +444,20 @@ def chunk_sizes(kind: int, n: int, P: int, gss_min_chunk: int = 1, fac_divisor: 
                 t = min(c, R)
                 sizes.append(t)
                 R -= t
+        return sizes
+    if kind == WF:
+        wq = wf_integer_weights(P, slow, slowdown)
+        worker = 0
+        while R > 0:
+            R_batch = R
+            for _ in range(P):
+                if R == 0:
+                    break
+                want = -(-(R_batch * wq[worker]) // (fac_divisor * P * 1024))
+                t = min(max(1, want), R)
+                sizes.append(t)
+                R -= t
+                worker = (worker + 1) % P
         return sizes
     raise ValueError("unknown schedule")
 

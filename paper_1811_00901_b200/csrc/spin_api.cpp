@@ -121,8 +121,26 @@ Region region_of(int W, double b, int mode, uint32_t flags) {
   return r;
 }
 
+// WF integer weights (mean 1024): slow workers 1/slowdown, the rest 1, normalised to mean 1
+void wf_weights(int32_t P, int32_t slow, float slowdown, uint32_t* wq_slow, uint32_t* wq_fast) {
+  const int S = std::min(std::max(slow, 0), P);
+  const double ws = slowdown > 1.0f ? 1.0 / slowdown : 1.0;
+  const double mean = (S * ws + (P - S)) / P;
+  *wq_slow = (uint32_t)std::max(1.0, std::floor(1024.0 * ws / mean + 0.5));
+  *wq_fast = (uint32_t)std::max(1.0, std::floor(1024.0 / mean + 0.5));
+}
+
+// one WF claim: the chunk of a worker with integer weight wq given the batch state
+// (next unit, batch remaining Rb, chunks dealt in this batch cnt); the device dealer
+// (spin_persistent) applies the same integer rule
+inline int64_t wf_chunk(int64_t n, int64_t next, int64_t Rb, uint32_t wq, int32_t fac_div, int32_t P) {
+  const int64_t den = (int64_t)fac_div * P * 1024;
+  const int64_t c = (Rb * (int64_t)wq + den - 1) / den;
+  return std::min(std::max<int64_t>(c, 1), n - next);
+}
+
 void build_bounds(spin_schedule sched, int64_t n, int32_t P, int32_t gss_min, int32_t fac_div,
-                  std::vector<int64_t>& out) {
+                  std::vector<int64_t>& out, int32_t slow = 0, float slowdown = 1.0f) {
   out.clear();
   out.push_back(0);
   if (n <= 0) return;
@@ -153,6 +171,23 @@ void build_bounds(spin_schedule sched, int64_t n, int32_t P, int32_t gss_min, in
           R -= t;
         }
       }
+      break;
+    case SPIN_WF: {      // weighted factoring, requests in round-robin worker order
+      uint32_t wqs, wqf;
+      wf_weights(P, slow, slowdown, &wqs, &wqf);
+      int64_t next = 0, Rb = 0;
+      int32_t cnt = 0, who = 0;
+      while (next < n) {
+        if (cnt == 0) Rb = n - next;
+        const int64_t c = wf_chunk(n, next, Rb, who < slow ? wqs : wqf, fac_div, P);
+        next += c;
+        out.push_back(next);
+        cnt = cnt + 1 == P ? 0 : cnt + 1;
+        who = who + 1 == P ? 0 : who + 1;
+      }
+      break;
+    }
+    default:
       break;
   }
 }
@@ -202,6 +237,8 @@ struct spin_ctx {
   uint32_t* hi_scratch = nullptr; int64_t hi_cap = 0;   // kept zero between launches
   // e2e pipelining of spin_generate_host: per-segment completion counters + copy stream
   unsigned* seg_done = nullptr; int64_t seg_cap = 0;
+  // WF/AWF dealer: [0] packed batch state, [1] unused, [2..] per-CTA measured rates (float)
+  unsigned long long* wf_state = nullptr; int64_t wf_cap = 0;
   int32_t pipe_seg_images = 0;                         // armed for the next launch only
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_seg0 = nullptr;
@@ -371,13 +408,15 @@ spin_status spin_chunk_sequence(spin_schedule sched, int64_t n_units, int32_t P,
                                 int64_t* n_chunks) {
   if (P < 1) return fail(SPIN_E_INVAL, "P=%d must be >= 1", P);
   if (n_units < 0) return fail(SPIN_E_INVAL, "n_units must be >= 0");
-  if (sched < SPIN_STATIC || sched > SPIN_FAC) return fail(SPIN_E_INVAL, "bad schedule %d", (int)sched);
+  if (sched < SPIN_STATIC || sched > SPIN_WF)
+    return fail(SPIN_E_INVAL, sched == SPIN_AWF ? "AWF weights are measured at run time: no static trace"
+                                                : "bad schedule %d", (int)sched);
   spin_chunk_params d{};
   if (cp) d = *cp;
   if (d.gss_min_chunk < 0 || d.fac_divisor < 0) return fail(SPIN_E_INVAL, "negative chunk parameter");
   std::vector<int64_t> b;
   build_bounds(sched, n_units, P, d.gss_min_chunk ? d.gss_min_chunk : 1,
-               d.fac_divisor ? d.fac_divisor : 2, b);
+               d.fac_divisor ? d.fac_divisor : 2, b, d.slow_ctas, d.slowdown);
   if (n_chunks) *n_chunks = (int64_t)b.size() - 1;
   if ((int64_t)b.size() > cap || !h_bounds)
     return fail(SPIN_E_RANGE, "need %lld bound entries, cap is %lld", (long long)b.size(), (long long)cap);
@@ -438,7 +477,8 @@ void spin_destroy(spin_handle h) {
   void* ptrs[] = {h->pos, h->nrm, h->tpos, h->cell_start, h->spos, h->snrm, h->keys, h->counts,
                   h->cursor, h->scan_tmp, h->ckeys, h->cstarts, h->order, h->bounds,
                   h->counter, h->stats, h->err, h->cta_t0, h->cta_t1, h->cta_units, h->cidx,
-                  h->outbuf, h->stage_p, h->stage_n, h->red, h->hi_scratch, h->seg_done};
+                  h->outbuf, h->stage_p, h->stage_n, h->red, h->hi_scratch, h->seg_done,
+                  h->wf_state};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->h_err) cudaFreeHost(h->h_err);
@@ -469,7 +509,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   if (mode != SPIN_NEAREST && mode != SPIN_BILINEAR) return fail(SPIN_E_INVAL, "bad mode %d", (int)mode);
   if (mode == SPIN_BILINEAR && W < 2) return fail(SPIN_E_INVAL, "BILINEAR needs W >= 2");
   if (prune != SPIN_BRUTE && prune != SPIN_CELLS) return fail(SPIN_E_INVAL, "bad prune %d", (int)prune);
-  if (sched < SPIN_STATIC || sched > SPIN_FAC) return fail(SPIN_E_INVAL, "bad schedule %d", (int)sched);
+  if (sched < SPIN_STATIC || sched > SPIN_AWF) return fail(SPIN_E_INVAL, "bad schedule %d", (int)sched);
   if (!std::isfinite(b) || b < 1e-30 || b > 1e30) return fail(SPIN_E_INVAL, "b=%g must be finite in [1e-30, 1e30]", b);
   const bool has_support = !(std::isinf(cos_As) && cos_As < 0);
   if (has_support && !(cos_As >= -1.0 && cos_As <= 1.0))
@@ -506,8 +546,12 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   const int64_t n_units = (M + unit - 1) / unit;
   const int gmin = cpar.gss_min_chunk ? cpar.gss_min_chunk : 1;
   const int fdiv = cpar.fac_divisor ? cpar.fac_divisor : 2;
+  const bool wf = sched == SPIN_WF || sched == SPIN_AWF;   // dealt on the device by CAS
+  if (wf && (n_units >= (1 << 24) || P >= (1 << 16) || cpar.d_counter))
+    return fail(SPIN_E_INVAL, "WF/AWF need n_units < 2^24 (have %lld), P < 2^16 (have %d) and no shared dealer",
+                (long long)n_units, P);
   const long long key[6] = {(long long)sched, (long long)n_units, P, gmin, fdiv, 1};
-  if (!std::equal(key, key + 6, h->bounds_key)) {
+  if (!wf && !std::equal(key, key + 6, h->bounds_key)) {
     build_bounds(sched, n_units, P, gmin, fdiv, h->bounds_h);
     std::vector<int32_t> b32(h->bounds_h.begin(), h->bounds_h.end());
     spin_status st = ensure(h->bounds, h->bounds_cap, (int64_t)b32.size(), "chunk table");
@@ -516,7 +560,12 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
     CK(cudaStreamSynchronize(s), "chunk table");  // b32 is a temporary
     std::copy(key, key + 6, h->bounds_key);
   }
-  const int n_chunks = (int)h->bounds_h.size() - 1;
+  const int n_chunks = wf ? 0 : (int)h->bounds_h.size() - 1;
+  if (wf) {   // packed batch state (u64) + per-CTA measured rates (AWF)
+    spin_status st = ensure(h->wf_state, h->wf_cap, 2 + grid, "WF dealer state");
+    if (st != SPIN_OK) return st;
+    CK(cudaMemsetAsync(h->wf_state, 0, (2 + grid) * sizeof(unsigned long long), s), "memset");
+  }
   if (h->cta_cap < grid) {
     if (h->cta_t0) cudaFree(h->cta_t0);
     if (h->cta_t1) cudaFree(h->cta_t1);
@@ -664,6 +713,15 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   p.n_chunks = n_chunks;
   p.unit_images = unit;
   p.is_static = sched == SPIN_STATIC ? 1 : 0;
+  p.wf = sched == SPIN_WF ? 1 : sched == SPIN_AWF ? 2 : 0;
+  if (wf) {
+    p.wf_state = h->wf_state;
+    p.awf_rate = reinterpret_cast<float*>(h->wf_state + 2);
+    p.n_units = (int32_t)n_units;
+    p.fac_div = fdiv;
+    p.P = P;
+    wf_weights(P, cpar.slowdown > 1.0f ? cpar.slow_ctas : 0, cpar.slowdown, &p.wq_slow, &p.wq_fast);
+  }
   p.cta_offset = cpar.cta_offset;
   p.slow_ctas = cpar.slowdown > 1.0f ? std::min(cpar.slow_ctas, grid) : 0;
   p.slowdown = cpar.slowdown > 1.0f ? cpar.slowdown : 1.0f;
@@ -785,6 +843,11 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
     stats->G = lc.G;
     stats->n_units = (int32_t)n_units;
     stats->n_chunks = n_chunks;
+    if (wf) {   // requests counted on the device; every CTA's last request finds no work
+      unsigned requests = 0;
+      CK(cudaMemcpy(&requests, h->counter, sizeof requests, cudaMemcpyDeviceToHost), "requests");
+      stats->n_chunks = (int32_t)requests - grid;
+    }
     const int nc = std::min(grid, stats->cta_capacity);
     if (nc > 0) {
       if (stats->h_cta_start_ns) CK(cudaMemcpy(stats->h_cta_start_ns, h->cta_t0, nc * 8, cudaMemcpyDeviceToHost), "cta");

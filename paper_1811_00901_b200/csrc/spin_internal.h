@@ -32,6 +32,12 @@ struct KParams {
   int32_t unit_images;                     // images per unit
   int32_t is_static;                       // chunk = blockIdx.x, no atomics
   unsigned int* counter;                   // the "master": one u32 in global memory
+  // WF / AWF (weighted factoring, dealt by CAS; wf = 1 WF, 2 AWF, 0 table dealer)
+  int32_t wf;
+  unsigned long long* wf_state;            // (next unit : 24 | batch R : 24 | count : 16)
+  float* awf_rate;                         // [grid] measured units per microsecond (AWF)
+  int32_t n_units, fac_div, P;
+  uint32_t wq_slow, wq_fast;               // WF integer weights (mean 1024)
 
   // ---- region constants (a2).  Doubles are exact host values; floats are the
   // conservative fp32 thresholds of the hot loop.

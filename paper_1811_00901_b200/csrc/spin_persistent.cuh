@@ -516,21 +516,81 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   unsigned long long visited = 0;
   bool first = true;
 
+  __shared__ int s_wu[2];              // WF/AWF: the claimed unit range
+  unsigned long long t_claim = 0, awf_ns = 0;
+  long long awf_units = 0;
   for (;;) {
     // ---- a6: request a chunk (PAPER.md:336-342 / 372-377)
-    if (tid == 0) {
-      if (first && p.slow_first && (int)blockIdx.x >= p.slow_ctas) {
+    if (warp == 0) {
+      if (lane == 0 && first && p.slow_first && (int)blockIdx.x >= p.slow_ctas) {
         // heterogeneity emulation: the slow workers request first
         while (*reinterpret_cast<volatile unsigned*>(p.counter) < (unsigned)p.slow_ctas) __nanosleep(256);
       }
-      s_chunk = p.is_static ? (first ? p.cta_offset + (int)blockIdx.x : p.n_chunks)
-                            : (int)atomicAdd(p.counter, 1u);
+      __syncwarp();
+      if (p.wf) {
+        // weighted factoring (beyond the paper; spin.h): this worker's integer
+        // weight (mean 1024) — a priori (WF) or from the measured rates (AWF: mine over
+        // the mean of the workers that have reported; 1024 before my first chunk)
+        unsigned wq = (int)blockIdx.x < p.slow_ctas ? p.wq_slow : p.wq_fast;
+        if (p.wf == 2) {
+          const volatile float* rates = p.awf_rate;
+          float sum = 0.f;
+          int cnt = 0;
+          for (int i = lane; i < (int)gridDim.x; i += 32) {
+            const float r = rates[i];
+            if (r > 0.f) { sum += r; ++cnt; }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+          cnt = __reduce_add_sync(0xffffffffu, cnt);
+          const float mine = rates[blockIdx.x];
+          wq = 1024u;
+          if (mine > 0.f && cnt > 0)
+            wq = (unsigned)fminf(fmaxf(rintf(1024.f * mine * (float)cnt / sum), 16.f), 65536.f);
+        }
+        if (lane == 0) {
+          // claim: compare-and-swap on (next : 24 | batch R : 24 | count : 16); a batch of
+          // P claims shares R = the units left at its first claim (FAC2 batches);
+          // the same integer rule as the host trace (spin_api.cpp wf_chunk)
+          const unsigned U = (unsigned)p.n_units;
+          const unsigned long long den = (unsigned long long)p.fac_div * (unsigned)p.P * 1024ull;
+          unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(p.wf_state);
+          for (;;) {
+            const unsigned next = (unsigned)(old & 0xffffffull);
+            if (next >= U) { s_wu[0] = s_wu[1] = (int)U; break; }
+            const unsigned cnt = (unsigned)(old >> 48);
+            const unsigned Rb = cnt == 0 ? U - next : (unsigned)((old >> 24) & 0xffffffull);
+            unsigned long long c = ((unsigned long long)Rb * wq + den - 1ull) / den;
+            c = min(max(c, 1ull), (unsigned long long)(U - next));
+            const unsigned nn = next + (unsigned)c;
+            const unsigned nc = cnt + 1u >= (unsigned)p.P ? 0u : cnt + 1u;
+            const unsigned long long nw = (unsigned long long)nn | ((unsigned long long)Rb << 24) |
+                                          ((unsigned long long)nc << 48);
+            const unsigned long long prev = atomicCAS(p.wf_state, old, nw);
+            if (prev == old) { s_wu[0] = (int)next; s_wu[1] = (int)nn; break; }
+            old = prev;
+          }
+          atomicAdd(p.counter, 1u);   // requests (stats n_chunks; the slow-first wait)
+          t_claim = gtimer();
+        }
+      } else if (lane == 0) {
+        s_chunk = p.is_static ? (first ? p.cta_offset + (int)blockIdx.x : p.n_chunks)
+                              : (int)atomicAdd(p.counter, 1u);
+      }
     }
     __syncthreads();
-    const int u = s_chunk;
     first = false;
-    if (u >= p.n_chunks) break;
-    const int u0 = p.bounds[u], u1 = p.bounds[u + 1];
+    int u0, u1;
+    if (p.wf) {
+      u0 = s_wu[0];
+      u1 = s_wu[1];
+      if (u0 >= u1) break;
+    } else {
+      const int u = s_chunk;
+      if (u >= p.n_chunks) break;
+      u0 = p.bounds[u];
+      u1 = p.bounds[u + 1];
+    }
     const long long i0 = (long long)u0 * p.unit_images;
     const long long i1 = min((long long)u1 * p.unit_images, (long long)p.M);
 
@@ -1220,6 +1280,13 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       __syncthreads();
     }
     units_done += u1 - u0;
+    if (p.wf == 2 && tid == 0) {
+      // AWF: my rate so far, units per microsecond of chunk time (incl. any emulated idling)
+      awf_units += u1 - u0;
+      awf_ns += gtimer() - t_claim;
+      reinterpret_cast<volatile float*>(p.awf_rate)[blockIdx.x] =
+          (float)((double)awf_units * 1e3 / (double)max(awf_ns, 1ull));
+    }
   }
 
   // ---- a13: instrumentation

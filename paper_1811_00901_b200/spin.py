@@ -18,12 +18,12 @@ if not os.path.exists(LIB_PATH):
     raise ImportError(f"libspin.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'`")
 _lib = C.CDLL(LIB_PATH)
 
-STATIC, SS, GSS, FAC = 0, 1, 2, 3
+STATIC, SS, GSS, FAC, WF, AWF = 0, 1, 2, 3, 4, 5
 NEAREST, BILINEAR = 0, 1
 BRUTE, CELLS = 0, 1
 F_LITERAL_HALF_WIDTH, F_FLOOR_BINS, F_NO_SORT, F_NO_FAST_CERT, F_SUPPORT_LAST = 0x1, 0x2, 0x4, 0x8, 0x10
 F_SUPPORT_FIRST = 0x20
-SCHEDULES = {"STATIC": STATIC, "SS": SS, "GSS": GSS, "FAC": FAC}
+SCHEDULES = {"STATIC": STATIC, "SS": SS, "GSS": GSS, "FAC": FAC, "WF": WF, "AWF": AWF}
 MODES = {"nearest": NEAREST, "bilinear": BILINEAR}
 PRUNES = {"brute": BRUTE, "cells": CELLS}
 STATUS = {0: "SPIN_OK", 1: "SPIN_E_INVAL", 2: "SPIN_E_RANGE", 3: "SPIN_E_INPUT",
@@ -214,9 +214,13 @@ def default_P(W: int, mode="nearest", prune="brute") -> int:
     return _lib.spin_default_P(int(W), _enum(mode, MODES), _enum(prune, PRUNES))
 
 
-def chunk_sequence(schedule, n_units: int, P: int, gss_min_chunk: int = 0, fac_divisor: int = 0):
-    """Chunk boundaries [0, b1, ..., n_units] of a schedule (host-only; spin_chunk_sequence)."""
+def chunk_sequence(schedule, n_units: int, P: int, gss_min_chunk: int = 0, fac_divisor: int = 0,
+                   slow_ctas: int = 0, slowdown: float = 0.0):
+    """Chunk boundaries [0, b1, ..., n_units] of a schedule (host-only; spin_chunk_sequence;
+    WF with requests in round-robin worker order and the emulation's weights)."""
     cp = ChunkParams(0, 0, gss_min_chunk, fac_divisor, 0)
+    cp.slow_ctas = slow_ctas
+    cp.slowdown = slowdown
     n = C.c_int64(0)
     st = _lib.spin_chunk_sequence(_enum(schedule, SCHEDULES), n_units, P, C.byref(cp), None, 0, C.byref(n))
     if st not in (0, 2):

@@ -58,6 +58,21 @@ def test_chunk_sequence_matches_oracle(kind):
             O.chunk_bounds(kind, n, P, gss_min_chunk=g, fac_divisor=f)
 
 
+def test_weighted_factoring_matches_oracle():
+    from paper_1811_00901_b200 import spin
+    rng = np.random.default_rng(11)
+    for _ in range(200):
+        n = int(rng.integers(0, 30000))
+        P = int(rng.integers(1, 600))
+        f = int(rng.integers(1, 4))
+        S = int(rng.integers(0, P + 1))
+        sd = float(np.float32(rng.uniform(1.0, 8.0)))
+        assert spin.chunk_sequence("WF", n, P, fac_divisor=f, slow_ctas=S, slowdown=sd) == \
+            O.chunk_bounds(O.WF, n, P, fac_divisor=f, slow=S, slowdown=sd)
+    with pytest.raises(spin.SpinError):
+        spin.chunk_sequence("AWF", 100, 4)   # measured weights: no static trace
+
+
 def test_chunk_goldens_through_abi():
     from paper_1811_00901_b200 import spin
     g = json.load(open(os.path.join(ROOT, "tests", "golden", "chunks.json")))

@@ -254,7 +254,7 @@ def test_schedule_invariance(spin, torch):
     cen = np.arange(0, 6000, 3, dtype=np.int32)
     for mode in ("nearest", "bilinear"):
         ref = run_gpu(spin, torch, P, Nn, cen, 16, 0.02, 0.5, mode)
-        for sched in ("STATIC", "SS", "GSS", "FAC"):
+        for sched in ("STATIC", "SS", "GSS", "FAC", "WF", "AWF"):
             for Pn in (1, 7, 148, 0):
                 for unit in (0, 1, 5):
                     got = run_gpu(spin, torch, P, Nn, cen, 16, 0.02, 0.5, mode, schedule=sched,
@@ -275,6 +275,14 @@ def test_dealer_stats_and_cta_times(spin, torch):
         assert np.all(st["cta_end_ns"] >= st["cta_start_ns"])
         exp = len(spin.chunk_sequence(sched, st["n_units"], 64)) - 1
         assert st["n_chunks"] == exp
+    # WF / AWF claim their chunks by compare-and-swap: every unit exactly once, the claim
+    # count between the FAC count (equal weights) and SS's
+    fac = len(spin.chunk_sequence("FAC", -(-8000 // 64), 64)) - 1
+    for sched in ("WF", "AWF"):
+        img, st = run_gpu(spin, torch, P, Nn, cen, 16, 0.02, 0.5, "nearest", stats=True,
+                          schedule=sched, P=64, cta_capacity=64, slow_ctas=8, slowdown=3.0)
+        assert int(st["cta_units"].sum()) == st["n_units"]
+        assert fac // 2 <= st["n_chunks"] <= st["n_units"], (sched, st["n_chunks"], fac)
 
 
 # ------------------------------------------------------------------ cell list
@@ -547,7 +555,7 @@ def test_heterogeneous_workers_same_images_and_trend(spin, torch):
         d_cen = _dev(torch, cen)
         ref = eng.generate(d_cen, 16, 0.02, 0.5, schedule="STATIC").clone()
         times = {}
-        for sched in ("STATIC", "SS", "GSS", "FAC"):
+        for sched in ("STATIC", "SS", "GSS", "FAC", "WF", "AWF"):
             for slow_first in (False, True):
                 kw = dict(schedule=sched, P=148, slow_ctas=37, slowdown=4.0, slow_first=slow_first)
                 out, st = eng.generate(d_cen, 16, 0.02, 0.5, stats=True, cta_capacity=148, **kw)
@@ -563,6 +571,14 @@ def test_heterogeneous_workers_same_images_and_trend(spin, torch):
         assert t_static / t_ss >= 1.5, times
         u = st_ss["cta_units"]
         assert u[:37].mean() < 0.6 * u[37:].mean(), u
+        # weighted factoring knows the slow workers a priori (WF): well ahead of FAC's equal
+        # chunks, the slow CTAs get fewer units; AWF measures them, but only after its first
+        # (equal-weight) batch, which already overloads the slow CTAs: it must still beat STATIC
+        t_wf, st_w = times[("WF", False)]
+        assert t_wf <= 0.9 * times[("FAC", False)][0], times
+        uw = st_w["cta_units"]
+        assert uw[:37].mean() < 0.6 * uw[37:].mean(), uw
+        assert t_static / times[("AWF", False)][0] >= 1.5, times
     finally:
         eng.close()
 

@@ -355,3 +355,34 @@ def test_region_radius_bounds_contributors():
             d = np.linalg.norm(P.astype(np.float64) - P[ci], axis=1)
             for j in np.nonzero(d > R)[0][:200]:
                 assert O.exact_pair(P[ci], Nn[ci], P[j], Nn[j], W, b, -math.inf, mode, flags) is None
+
+
+def test_weighted_factoring_pins():
+    """WF (beyond the paper, spin.h SPIN_WF): equal weights reproduce FAC2 (P:229-230,
+    reading #15) exactly; a hand-derived heterogeneous golden; every batch of P chunks
+    covers at least half of the units left at its start and the sizes tile n."""
+    g = json.load(open(os.path.join(GOLD, "chunks.json")))
+    assert O.chunk_sizes(O.WF, 100, 4, slow=1, slowdown=2.0) == g["WF_100_4_slow1_x2"]["sizes"]
+    rng = np.random.default_rng(7)
+    for _ in range(300):
+        n = int(rng.integers(0, 20000))
+        P = int(rng.integers(1, 300))
+        f = int(rng.integers(1, 4))
+        assert O.chunk_sizes(O.WF, n, P, fac_divisor=f) == O.chunk_sizes(O.FAC, n, P, fac_divisor=f)
+        S = int(rng.integers(0, P + 1))
+        sd = float(rng.uniform(1.0, 8.0))
+        s = O.chunk_sizes(O.WF, n, P, fac_divisor=f, slow=S, slowdown=sd)
+        assert sum(s) == n and all(c >= 1 for c in s)
+        wq = O.wf_integer_weights(P, S, sd)
+        R = n
+        for b in range(0, len(s), P):
+            batch = s[b:b + P]
+            left = R - sum(batch)
+            if left > 0:
+                # a complete batch hands out at least R_batch * sum(wq) / (f P 1024) units
+                assert len(batch) == P
+                assert sum(batch) * f * P * 1024 >= R * sum(wq)
+                # and a slow worker never gets more than a fast one
+                if 0 < S < P:
+                    assert max(batch[:S]) <= min(batch[S:])
+            R = left

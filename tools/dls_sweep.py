@@ -38,7 +38,7 @@ def main(argv=None):
     ap.add_argument("--P", default="0")
     ap.add_argument("--units", default="0,1")
     ap.add_argument("--policies", default="STATIC,SS,GSS,FAC",
-                    help="STATIC,SS,GSS,FAC and HW (one CTA per unit, the hardware block "
+                    help="STATIC,SS,GSS,FAC,WF,AWF and HW (one CTA per unit, the hardware block "
                          "scheduler as the dealer: the non-persistent control of SURVEY 8(d))")
     ap.add_argument("--no-sort", action="store_true")
     # heterogeneous-worker emulation: CTAs 0..slow-1 run `slowdown` x slower
