@@ -50,7 +50,7 @@ def parse(argv=None):
                     help="weak: every GPU runs the full workload (default); strong: the "
                          "configured centres are split across GPUs")
     ap.add_argument("--mode", default=None, choices=[None, "nearest", "bilinear"])
-    ap.add_argument("--schedule", default="SS", choices=["STATIC", "SS", "GSS", "FAC"])
+    ap.add_argument("--schedule", default="SS", choices=["STATIC", "SS", "GSS", "FAC", "WF", "AWF"])
     ap.add_argument("--W", type=int, default=None)
     ap.add_argument("--P", type=int, default=0)
     ap.add_argument("--unit", type=int, default=0)
