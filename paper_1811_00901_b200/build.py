@@ -18,12 +18,12 @@ BUILD = os.path.join(HERE, "..", "build", "spin")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr"]
-# (source, extra defines, object name): the persistent kernel's 50 instantiations are
-# split over six translation units (one per (mode, support placement) pair)
+# (source, extra defines, object name): the persistent kernel's 112 instantiations are
+# split over twelve translation units (one per (mode, support placement, dealer) triple)
 UNITS = [("spin_kernels.cu", (), "spin_kernels"), ("spin_api.cpp", (), "spin_api"),
          ("spin_io.cpp", (), "spin_io")] + [
-    ("spin_inst.cu", (f"-DINST_MODE={m}", f"-DINST_SUP={u}"), f"spin_inst_{m}_{u}")
-    for m in (0, 1) for u in (0, 1, 2)]
+    ("spin_inst.cu", (f"-DINST_MODE={m}", f"-DINST_SUP={u}", f"-DINST_DEAL={d}"), f"spin_inst_{m}_{u}_{d}")
+    for m in (0, 1) for u in (0, 1, 2) for d in (0, 1)]
 SOURCES = [u[0] for u in UNITS]
 
 

@@ -6,17 +6,19 @@
 namespace spin {
 
 // ------------------------------------------------------------------ dispatch
-const void* kernel_ptr_0_0(int prune, int G, int nt);
-const void* kernel_ptr_0_1(int prune, int G, int nt);
-const void* kernel_ptr_1_0(int prune, int G, int nt);
-const void* kernel_ptr_1_1(int prune, int G, int nt);
-const void* kernel_ptr_0_2(int prune, int G, int nt);
-const void* kernel_ptr_1_2(int prune, int G, int nt);
-static const void* kernel_for(int mode, int prune, int G, int sup, int nt) {
+// kernel_ptr_M_S_D: MODE M, support placement S, dealer D (0 chunk table, 1 WF / AWF
+// compare-and-swap; a separate instantiation, so the table dealer's code is unchanged)
+#define SPIN_DECL(m, s, d) const void* kernel_ptr_##m##_##s##_##d(int prune, int G, int nt);
+SPIN_DECL(0, 0, 0) SPIN_DECL(0, 1, 0) SPIN_DECL(0, 2, 0) SPIN_DECL(1, 0, 0) SPIN_DECL(1, 1, 0) SPIN_DECL(1, 2, 0)
+SPIN_DECL(0, 0, 1) SPIN_DECL(0, 1, 1) SPIN_DECL(0, 2, 1) SPIN_DECL(1, 0, 1) SPIN_DECL(1, 1, 1) SPIN_DECL(1, 2, 1)
+#undef SPIN_DECL
+static const void* kernel_for(int mode, int prune, int G, int sup, int nt, int deal) {
   if (prune == 1 && sup == 2) sup = 1;   // adaptive placement is BRUTE-only
-  if (mode == 0)
-    return sup == 2 ? kernel_ptr_0_2(prune, G, nt) : sup ? kernel_ptr_0_1(prune, G, nt) : kernel_ptr_0_0(prune, G, nt);
-  return sup == 2 ? kernel_ptr_1_2(prune, G, nt) : sup ? kernel_ptr_1_1(prune, G, nt) : kernel_ptr_1_0(prune, G, nt);
+  typedef const void* (*Fn)(int, int, int);
+  static const Fn tab[2][2][3] = {
+      {{kernel_ptr_0_0_0, kernel_ptr_0_1_0, kernel_ptr_0_2_0}, {kernel_ptr_1_0_0, kernel_ptr_1_1_0, kernel_ptr_1_2_0}},
+      {{kernel_ptr_0_0_1, kernel_ptr_0_1_1, kernel_ptr_0_2_1}, {kernel_ptr_1_0_1, kernel_ptr_1_1_1, kernel_ptr_1_2_1}}};
+  return tab[deal ? 1 : 0][mode ? 1 : 0][sup](prune, G, nt);
 }
 
 LaunchCfg choose_launch(int W, int mode, int prune) {
@@ -59,7 +61,7 @@ LaunchCfg choose_launch(int W, int mode, int prune) {
 int tile_points() { return 6144; }
 
 int occupancy_blocks(const LaunchCfg& lc, int W, int mode, int prune) {
-  const void* f = kernel_for(mode, prune, lc.G, 1, lc.threads);
+  const void* f = kernel_for(mode, prune, lc.G, 1, lc.threads, 0);
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.smem);
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, lc.threads, lc.smem) != cudaSuccess)
@@ -70,7 +72,7 @@ int occupancy_blocks(const LaunchCfg& lc, int W, int mode, int prune) {
 
 cudaError_t launch_spin(const LaunchCfg& lc, int mode, int prune, int grid, const KParams& p,
                         cudaStream_t s) {
-  const void* f = kernel_for(mode, prune, lc.G, p.support_in_hot, lc.threads);
+  const void* f = kernel_for(mode, prune, lc.G, p.support_in_hot, lc.threads, p.wf ? 1 : 0);
   cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.smem);
   if (e != cudaSuccess) return e;
   void* args[] = {(void*)&p};

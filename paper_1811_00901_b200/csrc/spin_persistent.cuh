@@ -1,6 +1,6 @@
 // spin_persistent.cuh — the persistent spin kernel of the hot path (sm_100a).
-// Instantiated in spin_inst_*.cu (one translation unit per (mode, support) pair so the
-// 56 variants compile in parallel); dispatched from spin_kernels.cu.
+// Instantiated in spin_inst.cu (one translation unit per (mode, support, dealer) triple
+// so the 112 variants compile in parallel); dispatched from spin_kernels.cu.
 //
 // Persistent spin kernel: P resident CTAs; each CTA
 // asks the device "master" (one u32 in global memory) for the next chunk of the
@@ -388,11 +388,22 @@ __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const f
     const bool wu = !(fabsf(wval - lim) > p.Ew_a);
     const bool out = (!uu & !((uval > 0.f) & (uval < Wm1))) | (!wu & !(wval < lim));
     r.status = (sup_out | (!unc0 & out)) ? 0 : ((unc0 | uu | wu) ? 2 : 1);
-    // v only places the splat (continuous in v across bin edges), so the approximate
-    // square root (MUFU, ~2 ulp) is within the BILINEAR tolerance; the region edge was
-    // decided on w above
+    // v only places the splat (continuous in v across bin edges); the region edge was
+    // decided on w above.  alpha^2 = |d|^2 - beta^2 cancels when X - P is nearly parallel
+    // to n (its error ~3u|d|^2 becomes 3u|d|^2 / (2 b alpha) in v), so within 1/8 rad of
+    // the normal axis (alpha^2 < |d|^2 / 64) the splat takes alpha^2 from Lagrange's
+    // identity, |d x n|^2 - (|n|^2 - 1)|d|^2, whose fp32 error is O(u |d| alpha); outside
+    // it the direct form's v error is below 12u|d|/b.  The approximate square root (MUFU,
+    // ~2 ulp) is within the tolerance.
+    float qs = q;
+    if (q < dd * 0.015625f) {
+      const float cx = fmaf(d1, N4.z, -(d2 * N4.y));
+      const float cy = fmaf(d2, N4.x, -(d0 * N4.z));
+      const float cz = fmaf(d0, N4.y, -(d1 * N4.x));
+      qs = fmaf(cx, cx, fmaf(cy, cy, fmaf(cz, cz, -N4.w * dd)));
+    }
     float v;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(v) : "f"(fmaxf(wval, 0.0f)));
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(v) : "f"(fmaxf(qs * p.inv_b2, 0.0f)));
     const float fi = fminf(fmaxf(rint_magic(uval - 0.5f), 0.0f), Wm1 - 1.0f);
     const float fj = fminf(fmaxf(rint_magic(v - 0.5f), 0.0f), Wm1 - 1.0f);
     r.a = fminf(fmaxf(uval - fi, 0.0f), 1.0f);
@@ -442,11 +453,62 @@ __device__ __forceinline__ void apply(const KParams& p, const Dec& d, uint32_t* 
   }
 }
 
+// ------------------------------------------------------------------ WF / AWF dealer
+// Weighted factoring (beyond the paper, its future work P:238; spin.h SPIN_WF / SPIN_AWF),
+// called by warp 0: this worker's integer weight (mean 1024) — a priori (WF) or from the
+// measured rates (AWF: mine over the mean of the workers that have reported; 1024 before
+// my first chunk) — then lane 0 claims [wu[0], wu[1]) by compare-and-swap on the packed
+// state (next : 24 | batch R : 24 | count : 16): a batch of P claims shares R = the units
+// left at its first claim (FAC2 batches), the same integer rule as the host
+// trace (spin_api.cpp wf_chunk).  Out of line: one call per chunk.
+static __device__ __noinline__ void wf_claim(const KParams& p, int lane, int* wu,
+                                             unsigned long long& t_claim) {
+  unsigned wq = (int)blockIdx.x < p.slow_ctas ? p.wq_slow : p.wq_fast;
+  if (p.wf == 2) {
+    const volatile float* rates = p.awf_rate;
+    float sum = 0.f;
+    int cnt = 0;
+    for (int i = lane; i < (int)gridDim.x; i += 32) {
+      const float r = rates[i];
+      if (r > 0.f) { sum += r; ++cnt; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    const float mine = rates[blockIdx.x];
+    wq = 1024u;
+    if (mine > 0.f && cnt > 0)
+      wq = (unsigned)fminf(fmaxf(rintf(1024.f * mine * (float)cnt / sum), 16.f), 65536.f);
+  }
+  if (lane == 0) {
+    const unsigned U = (unsigned)p.n_units;
+    const unsigned long long den = (unsigned long long)p.fac_div * (unsigned)p.P * 1024ull;
+    unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(p.wf_state);
+    for (;;) {
+      const unsigned next = (unsigned)(old & 0xffffffull);
+      if (next >= U) { wu[0] = wu[1] = (int)U; break; }
+      const unsigned cnt = (unsigned)(old >> 48);
+      const unsigned Rb = cnt == 0 ? U - next : (unsigned)((old >> 24) & 0xffffffull);
+      unsigned long long c = ((unsigned long long)Rb * wq + den - 1ull) / den;
+      c = min(max(c, 1ull), (unsigned long long)(U - next));
+      const unsigned nn = next + (unsigned)c;
+      const unsigned nc = cnt + 1u >= (unsigned)p.P ? 0u : cnt + 1u;
+      const unsigned long long nw = (unsigned long long)nn | ((unsigned long long)Rb << 24) |
+                                    ((unsigned long long)nc << 48);
+      const unsigned long long prev = atomicCAS(p.wf_state, old, nw);
+      if (prev == old) { wu[0] = (int)next; wu[1] = (int)nn; break; }
+      old = prev;
+    }
+    atomicAdd(p.counter, 1u);   // requests (stats n_chunks; the slow-first wait)
+    t_claim = gtimer();
+  }
+}
+
 // ------------------------------------------------------------------ the kernel
 // SUP = 1: the hot loop evaluates the support test for every pair (the paper's order,
 // P:166 before P:169-171); SUP = 0: the hot loop tests the region only and the support
 // test is decided in the accept path (SPIN_F_SUPPORT_LAST, or no support test at all).
-template <int MODE, int PRUNE, int G, int SUP, int NT>
+template <int MODE, int PRUNE, int G, int SUP, int NT, int DEAL>
 __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__ KParams p) {
   constexpr int NWARP = NT / 32;
   constexpr int ROWCAP = NT;        // CELLS: grid rows staged per batch
@@ -517,63 +579,21 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   bool first = true;
 
   __shared__ int s_wu[2];              // WF/AWF: the claimed unit range
-  unsigned long long t_claim = 0, awf_ns = 0;
-  long long awf_units = 0;
+  // AWF bookkeeping of tid 0 (in shared memory: no registers live across the loop):
+  // [0] claim time, [1] chunk time so far, [2] units so far
+  __shared__ unsigned long long s_awf[3];
+  if (DEAL && tid == 0) s_awf[0] = s_awf[1] = s_awf[2] = 0ull;
   for (;;) {
     // ---- a6: request a chunk (PAPER.md:336-342 / 372-377)
-    if (warp == 0) {
+    if (DEAL ? warp == 0 : tid == 0) {
       if (lane == 0 && first && p.slow_first && (int)blockIdx.x >= p.slow_ctas) {
         // heterogeneity emulation: the slow workers request first
         while (*reinterpret_cast<volatile unsigned*>(p.counter) < (unsigned)p.slow_ctas) __nanosleep(256);
       }
-      __syncwarp();
-      if (p.wf) {
-        // weighted factoring (beyond the paper; spin.h): this worker's integer
-        // weight (mean 1024) — a priori (WF) or from the measured rates (AWF: mine over
-        // the mean of the workers that have reported; 1024 before my first chunk)
-        unsigned wq = (int)blockIdx.x < p.slow_ctas ? p.wq_slow : p.wq_fast;
-        if (p.wf == 2) {
-          const volatile float* rates = p.awf_rate;
-          float sum = 0.f;
-          int cnt = 0;
-          for (int i = lane; i < (int)gridDim.x; i += 32) {
-            const float r = rates[i];
-            if (r > 0.f) { sum += r; ++cnt; }
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-          cnt = __reduce_add_sync(0xffffffffu, cnt);
-          const float mine = rates[blockIdx.x];
-          wq = 1024u;
-          if (mine > 0.f && cnt > 0)
-            wq = (unsigned)fminf(fmaxf(rintf(1024.f * mine * (float)cnt / sum), 16.f), 65536.f);
-        }
-        if (lane == 0) {
-          // claim: compare-and-swap on (next : 24 | batch R : 24 | count : 16); a batch of
-          // P claims shares R = the units left at its first claim (FAC2 batches);
-          // the same integer rule as the host trace (spin_api.cpp wf_chunk)
-          const unsigned U = (unsigned)p.n_units;
-          const unsigned long long den = (unsigned long long)p.fac_div * (unsigned)p.P * 1024ull;
-          unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(p.wf_state);
-          for (;;) {
-            const unsigned next = (unsigned)(old & 0xffffffull);
-            if (next >= U) { s_wu[0] = s_wu[1] = (int)U; break; }
-            const unsigned cnt = (unsigned)(old >> 48);
-            const unsigned Rb = cnt == 0 ? U - next : (unsigned)((old >> 24) & 0xffffffull);
-            unsigned long long c = ((unsigned long long)Rb * wq + den - 1ull) / den;
-            c = min(max(c, 1ull), (unsigned long long)(U - next));
-            const unsigned nn = next + (unsigned)c;
-            const unsigned nc = cnt + 1u >= (unsigned)p.P ? 0u : cnt + 1u;
-            const unsigned long long nw = (unsigned long long)nn | ((unsigned long long)Rb << 24) |
-                                          ((unsigned long long)nc << 48);
-            const unsigned long long prev = atomicCAS(p.wf_state, old, nw);
-            if (prev == old) { s_wu[0] = (int)next; s_wu[1] = (int)nn; break; }
-            old = prev;
-          }
-          atomicAdd(p.counter, 1u);   // requests (stats n_chunks; the slow-first wait)
-          t_claim = gtimer();
-        }
-      } else if (lane == 0) {
+      if (DEAL) {
+        __syncwarp();
+        wf_claim(p, lane, s_wu, s_awf[0]);   // warp 0 (AWF reads the rates), lane 0 claims
+      } else {
         s_chunk = p.is_static ? (first ? p.cta_offset + (int)blockIdx.x : p.n_chunks)
                               : (int)atomicAdd(p.counter, 1u);
       }
@@ -581,7 +601,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
     __syncthreads();
     first = false;
     int u0, u1;
-    if (p.wf) {
+    if (DEAL) {
       u0 = s_wu[0];
       u1 = s_wu[1];
       if (u0 >= u1) break;
@@ -611,6 +631,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           if (c >= 0 && c < p.N) {
             P4 = __ldg(&p.cpos[c]);
             N4 = __ldg(&p.cnrm[c]);
+            // |n|^2 - 1 for the BILINEAR splat position (Lagrange's identity, decide)
+            N4.w = (float)((double)N4.x * N4.x + (double)N4.y * N4.y + (double)N4.z * N4.z - 1.0);
             const double mid = p.mid;
             if (PRUNE == 0) {
               // BRUTE: sphere of radius rho about c~ = B/2, B = fl(2(p + mid n)) (DESIGN.md
@@ -1280,12 +1302,12 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       __syncthreads();
     }
     units_done += u1 - u0;
-    if (p.wf == 2 && tid == 0) {
+    if (DEAL && p.wf == 2 && tid == 0) {
       // AWF: my rate so far, units per microsecond of chunk time (incl. any emulated idling)
-      awf_units += u1 - u0;
-      awf_ns += gtimer() - t_claim;
+      s_awf[2] += (unsigned long long)(u1 - u0);
+      s_awf[1] += gtimer() - s_awf[0];
       reinterpret_cast<volatile float*>(p.awf_rate)[blockIdx.x] =
-          (float)((double)awf_units * 1e3 / (double)max(awf_ns, 1ull));
+          (float)((double)s_awf[2] * 1e3 / (double)max(s_awf[1], 1ull));
     }
   }
 

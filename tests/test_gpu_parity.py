@@ -627,3 +627,61 @@ def test_tensor_core_filter_selection_and_parity(spin, torch):
     assert st3["filter_mma"] == 0
     ora3, ost3 = oracle(Pf, Nn, cen[:40], 16, 0.02, 0.5, "nearest")
     check(g3, ora3, ost3, "nearest", "far cloud, fp32 filter")
+
+
+def _fuzz_cloud(rng, kind, n):
+    """Small seeded clouds with the structures that stress the filters and the decisions:
+    surfaces, volumes, exact duplicates, coplanar / collinear sets, dyadic grids (exact
+    ties), far offsets and tiny scales."""
+    if kind == "bumpy":
+        P, Nn = clouds.bumpy_sphere(n, int(rng.integers(1 << 30)))
+    elif kind == "clustered":
+        P, Nn = clouds.clustered(n, int(rng.integers(1 << 30)))
+    else:
+        if kind == "dyadic":
+            P = rng.integers(-16, 17, size=(n, 3)).astype(np.float64) / 16.0
+        elif kind == "planar":
+            P = np.c_[rng.uniform(-1, 1, (n, 2)), np.zeros(n)]
+        else:  # collinear
+            P = np.c_[rng.uniform(-1, 1, n), np.zeros(n), np.zeros(n)]
+        g = rng.normal(size=(n, 3))
+        Nn = g / np.linalg.norm(g, axis=1, keepdims=True)
+        if kind != "collinear":
+            Nn[: n // 2] = [0.0, 0.0, 1.0]
+    P = np.asarray(P, np.float64)
+    dup = rng.integers(0, n, size=max(1, n // 20))
+    P[dup[: len(dup) // 2]] = P[dup[len(dup) // 2: 2 * (len(dup) // 2)]]   # exact duplicates
+    scale = float(rng.choice([1.0, 1.0, 1e-2, 64.0]))
+    off = rng.uniform(-1, 1, 3) * float(rng.choice([0.0, 0.0, 2.0, 50.0]))
+    return (P * scale + off).astype(np.float32), np.asarray(Nn, np.float32), scale
+
+
+def test_fuzz_against_oracle(spin, torch):
+    """Seeded random configurations (widths, bin sizes, support angles, modes, flags,
+    pruning, every schedule incl. WF/AWF, P, unit) on small structured clouds: NEAREST
+    bit-exact and BILINEAR within tolerance against the oracle, CELLS = BRUTE."""
+    rng = np.random.default_rng(20261020)
+    kinds = ["bumpy", "clustered", "dyadic", "planar", "collinear"]
+    scheds = ["STATIC", "SS", "GSS", "FAC", "WF", "AWF"]
+    for case in range(40):
+        kind = kinds[case % len(kinds)]
+        n = int(rng.integers(50, 1500))
+        P, Nn, scale = _fuzz_cloud(rng, kind, n)
+        M = int(rng.integers(1, 80))
+        cen = rng.integers(0, n, size=M).astype(np.int32)
+        W = int(rng.choice([2, 3, 4, 5, 8, 13, 16, 24, 32]))
+        b = float(rng.choice([0.02, 0.05, 0.1, 0.25])) * scale
+        c = float(rng.choice([0.5, 0.0, -0.5, -math.inf, math.cos(math.radians(37.0))]))
+        mode = "nearest" if case % 2 == 0 else "bilinear"
+        flags = int(rng.choice([0, 0, 0, 1, 2])) if mode == "nearest" else 0
+        kw = dict(schedule=scheds[case % len(scheds)], P=int(rng.choice([0, 1, 5, 148])),
+                  unit=int(rng.choice([0, 1, 3])), flags=flags)
+        what = f"case {case} {kind} n={n} M={M} W={W} b={b:g} c={c:g} {mode} {kw}"
+        brute = run_gpu(spin, torch, P, Nn, cen, W, b, c, mode, **kw)
+        ora, st = oracle(P, Nn, cen, W, b, c, mode, flags=flags)
+        check(brute, ora, st, mode, what + " brute")
+        cells = run_gpu(spin, torch, P, Nn, cen, W, b, c, mode, prune="cells", **kw)
+        if mode == "nearest":
+            np.testing.assert_array_equal(cells, brute, err_msg=what + " cells != brute")
+        else:
+            check(cells, ora, st, mode, what + " cells")
