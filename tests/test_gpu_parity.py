@@ -660,10 +660,11 @@ def test_fuzz_against_oracle(spin, torch):
     """Seeded random configurations (widths, bin sizes, support angles, modes, flags,
     pruning, every schedule incl. WF/AWF, P, unit) on small structured clouds: NEAREST
     bit-exact and BILINEAR within tolerance against the oracle, CELLS = BRUTE."""
-    rng = np.random.default_rng(20261020)
+    # (SPIN_FUZZ_CASES / SPIN_FUZZ_SEED widen the campaign for one-off runs)
+    rng = np.random.default_rng(int(os.environ.get("SPIN_FUZZ_SEED", "20261020")))
     kinds = ["bumpy", "clustered", "dyadic", "planar", "collinear"]
     scheds = ["STATIC", "SS", "GSS", "FAC", "WF", "AWF"]
-    for case in range(40):
+    for case in range(int(os.environ.get("SPIN_FUZZ_CASES", "40"))):
         kind = kinds[case % len(kinds)]
         n = int(rng.integers(50, 1500))
         P, Nn, scale = _fuzz_cloud(rng, kind, n)
@@ -674,8 +675,10 @@ def test_fuzz_against_oracle(spin, torch):
         c = float(rng.choice([0.5, 0.0, -0.5, -math.inf, math.cos(math.radians(37.0))]))
         mode = "nearest" if case % 2 == 0 else "bilinear"
         flags = int(rng.choice([0, 0, 0, 1, 2])) if mode == "nearest" else 0
+        # knobs that must not change images: NO_SORT, NO_FAST_CERT, SUPPORT_LAST / FIRST
+        knobs = int(rng.choice([0, 0, 0x4, 0x8, 0x10, 0x20]))
         kw = dict(schedule=scheds[case % len(scheds)], P=int(rng.choice([0, 1, 5, 148])),
-                  unit=int(rng.choice([0, 1, 3])), flags=flags)
+                  unit=int(rng.choice([0, 1, 3])), flags=flags | knobs)
         what = f"case {case} {kind} n={n} M={M} W={W} b={b:g} c={c:g} {mode} {kw}"
         brute = run_gpu(spin, torch, P, Nn, cen, W, b, c, mode, **kw)
         ora, st = oracle(P, Nn, cen, W, b, c, mode, flags=flags)
