@@ -396,7 +396,7 @@ __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const f
     // it the direct form's v error is below 12u|d|/b.  The approximate square root (MUFU,
     // ~2 ulp) is within the tolerance.
     float qs = q;
-    if (q < dd * 0.015625f) {
+    if (q < dd * 0.015625f) {   // (a warp-vote variant measured 1-2% slower)
       const float cx = fmaf(d1, N4.z, -(d2 * N4.y));
       const float cy = fmaf(d2, N4.x, -(d0 * N4.z));
       const float cz = fmaf(d0, N4.y, -(d1 * N4.x));
