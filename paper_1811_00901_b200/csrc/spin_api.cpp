@@ -762,11 +762,20 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
     p.h_cell = h->h_cell;
     p.R_up = R;
     if (!(flags & SPIN_F_NO_SORT)) {
-      int shift = 0;
+      // centre keys: Morton codes of a grid of up to 2^ob cells per axis — coarser than
+      // the cell grid (shift) or finer (sub-cell refinement sub), so that G consecutive
+      // centres of a dense region form a compact group (C5: 2^8 per axis cuts the visited
+      // pairs by 16% and the time by 6% against 2^6); ob grows with M so the 2^(3 ob)
+      // counting-sort buckets stay within 64 M
+      int ob = 6;
+      while (ob < 8 && ((int64_t)1 << (3 * (ob + 1))) <= 64 * M) ++ob;
+      if (const char* e = std::getenv("SPIN_ORDER_BITS")) ob = std::min(std::max(std::atoi(e), 1), 8);
+      int shift = 0, sub = 0;
       const int dmax = std::max(h->dx, std::max(h->dy, h->dz));
-      while ((dmax >> shift) > 64) ++shift;
+      while ((dmax >> shift) > (1 << ob)) ++shift;
+      while (shift == 0 && (dmax << (sub + 1)) <= (1 << ob)) ++sub;
       int bits = 0;
-      while ((1 << bits) < ((dmax - 1) >> shift) + 1) ++bits;
+      while ((1 << bits) < (((dmax << sub) - 1) >> shift) + 1) ++bits;
       bits = std::max(bits, 1);
       const int64_t nb = (int64_t)1 << (3 * bits);
       if ((st = ensure(h->ckeys, h->ckeys_cap, M, "centre keys")) != SPIN_OK) return st;
@@ -776,7 +785,8 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
       if ((st = ensure(h->cursor, h->cursor_cap, nb, "cursor")) != SPIN_OK) return st;
       if ((st = ensure(h->scan_tmp, h->scan_tmp_cap, (int64_t)scan_tmp_elems(nb) + 1, "scan_tmp")) != SPIN_OK) return st;
       CK(launch_centre_order(d_centre_idx, M, h->pos, (int32_t)h->N, h->ox, h->oy, h->oz,
-                             h->inv_h, h->dx, h->dy, h->dz, shift, bits, h->ckeys, h->counts,
+                             h->inv_h * (float)(1 << sub), h->dx << sub, h->dy << sub, h->dz << sub,
+                             shift, bits, h->ckeys, h->counts,
                              h->cstarts, h->cursor, h->scan_tmp, h->order, s),
          "centre order");
       if (cpar.d_counter) {

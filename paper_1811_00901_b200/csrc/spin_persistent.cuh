@@ -64,6 +64,9 @@
 #ifndef SPIN_IMG_PAD_BRUTE
 #define SPIN_IMG_PAD_BRUTE 1  // the odd stride for BRUTE BILINEAR too (C4 401 -> 398 ms)
 #endif
+#ifndef SPIN_QCAP_CELLS
+#define SPIN_QCAP_CELLS 1024  // CELLS per-warp candidate ring (entries)
+#endif
 #ifndef SPIN_APL_BRUTE512
 #define SPIN_APL_BRUTE512 1   // the same for the 512-thread (W = 32) variant
 #endif
@@ -82,7 +85,7 @@ __host__ __device__ constexpr int cb_of(int G) { return G < CB_MAX ? G : CB_MAX;
 // (G <= 32 BRUTE groups hold ~100 candidates per warp tile: a 256-entry ring frees the
 // shared memory that lets W = 32 run 768-thread CTAs with G = 24)
 __host__ __device__ constexpr int qcap_of(int prune, int G = 64) {
-  return prune ? 1024 : (G <= 32 ? 256 : 512);
+  return prune ? SPIN_QCAP_CELLS : (G <= 32 ? 256 : 512);
 }
 
 static_assert(CB_MAX * KP == 32 && KP == 4 && KP == KP_POINTS, "mask is one u32: bit (k << 3) | c");
