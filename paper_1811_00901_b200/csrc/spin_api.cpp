@@ -311,9 +311,10 @@ spin_status load_cloud(spin_ctx* h, const float* points, const float* normals, i
 }
 
 spin_status ensure_grid(spin_ctx* h, float R, cudaStream_t s, double* build_ms) {
-  // cell edge R/4 (measured against R/2, R/3, R/6, R/8 with the per-row chord
-  // hulls: C3 47.2 / C5 189 ms at R/4); grow it if the grid would exceed 2^24 cells
-  double hh = 0.25 * R;
+  // cell edge R/8 (with the per-row chord hulls and the fine centre order,
+  // measured against R/3 .. R/16: C3 41.9, C5 152.4, C5 W=24 561.7 ms at R/8, 42.4 /
+  // 159.0 / 570.2 at R/4); grow it if the grid would exceed 2^24 cells
+  double hh = 0.125 * R;
   if (const char* c = std::getenv("SPIN_DEBUG_CELLS_PER_R")) hh = R / std::atof(c);   // measurement knob
   const double ex = std::max(1e-30, (double)h->aabb[3] - h->aabb[0]);
   const double ey = std::max(1e-30, (double)h->aabb[4] - h->aabb[1]);
