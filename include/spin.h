@@ -144,7 +144,7 @@ typedef struct {
  * spin_create — make a handle that owns a device copy of the oriented point cloud.
  *   points, normals: fp32 [N][3] (x,y,z) — the set OP of PAPER.md:115 with normals
  *                    np_i.  Host or device pointers (cudaMemcpyDefault).
- *   N: number of oriented points, 1 <= N < 2^31.
+ *   N: number of oriented points, 1 <= N < 2^31 - 12288 (room for the tile padding).
  * Copies and re-lays the cloud out as SoA float4 {x,y,z,|x|^2} + {nx,ny,nz,0} in
  * HBM (the input "replicated to every worker", P:256 / P:333, is resident once).
  * Validates: every coordinate finite with |coordinate| <= 2^40, every |normal| in [0.999, 1.001]

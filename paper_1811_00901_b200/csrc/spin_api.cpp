@@ -261,7 +261,7 @@ spin_status load_cloud(spin_ctx* h, const float* points, const float* normals, i
   if (!points || !normals) return fail(SPIN_E_INVAL, "points/normals must be non-null");
   const int64_t TILE_POINTS = tile_points();
   if (N < 1 || N >= ((int64_t)1 << 31) - 2 * TILE_POINTS)
-    return fail(SPIN_E_INVAL, "N=%lld outside [1, 2^31)", (long long)N);
+    return fail(SPIN_E_INVAL, "N=%lld outside [1, 2^31 - 12288)", (long long)N);
   const int64_t Npad = ((N + 1 + TILE_POINTS - 1) / TILE_POINTS) * TILE_POINTS;  // >= 1 sentinel
   if (Npad > h->cap) {
     if (h->pos) cudaFree(h->pos);
