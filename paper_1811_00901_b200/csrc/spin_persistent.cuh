@@ -52,6 +52,9 @@
 #ifndef SPIN_APL_CELLS
 #define SPIN_APL_CELLS 2      // CELLS candidates per lane per accept pass
 #endif
+#ifndef SPIN_APL_CELLS_NEAREST
+#define SPIN_APL_CELLS_NEAREST 1  // CELLS NEAREST candidates per lane per accept pass
+#endif
 #ifndef SPIN_HOT_UNROLL
 #define SPIN_HOT_UNROLL 2     // unroll of the sphere-only centre-batch loop
 #endif
@@ -765,7 +768,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       // two independent decisions interleave; BRUTE keeps one (fewer live registers).
       // (CELLS: two per lane for BILINEAR, one for NEAREST, as measured: C3 47.3 vs 48.0 ms,
       // C5 188 vs 191 ms)
-      constexpr int APL = PRUNE == 1 ? (MODE == 1 ? SPIN_APL_CELLS : 1) : (NT == 512 ? SPIN_APL_BRUTE512 : SPIN_APL_BRUTE);
+      constexpr int APL = PRUNE == 1 ? (MODE == 1 ? SPIN_APL_CELLS : SPIN_APL_CELLS_NEAREST)
+                                     : (NT == 512 ? SPIN_APL_BRUTE512 : SPIN_APL_BRUTE);
       auto process_pair = [&](unsigned e0, bool v0, unsigned e1, bool v1) {
         float4 P0, N0, X0, NX0, P1, N1, X1, NX1;
         int g0, g1 = 0;
