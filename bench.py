@@ -238,8 +238,8 @@ def oracle_parallel(cfg, P, Nn, cen, mode, seconds, cores=None):
     done = sum(r[0] for r in res)
     pairs = sum(r[1] for r in res)
     dt = max(r[2] for r in res)
-    oracle_parallel.per_core = statistics.mean(r[1] / r[2] for r in res if r[2] > 0)
-    return done, pairs, dt, cores
+    per_core = statistics.mean([r[1] / r[2] for r in res if r[2] > 0] or [0.0])
+    return done, pairs, dt, cores, per_core
 
 
 def cpu_model():
@@ -253,13 +253,13 @@ def cpu_model():
 
 
 def cpu_baseline_dict(cfg, P, Nn, cen, mode, seconds):
-    done, pairs, dt, cores = oracle_parallel(cfg, P, Nn, cen, mode, seconds)
+    done, pairs, dt, cores, per_core = oracle_parallel(cfg, P, Nn, cen, mode, seconds)
     kind = "visited" if cfg["prune"] == "cells" else "all"
     return {"value": pairs / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{done} of {len(cen)} images of {cfg['name']} ({kind} pairs, numpy float64 "
                       f"+ exact fallback; {cores} processes, one per host core, each on every "
                       f"{cores}-th image for {seconds:.0f} s; {dt:.1f} s slowest worker)",
-            "images_per_s": done / dt, "per_core_value": oracle_parallel.per_core,
+            "images_per_s": done / dt, "per_core_value": per_core,
             "cpu_model": cpu_model()}
 
 
@@ -280,7 +280,7 @@ def run_reference(args):
     tot_pairs, tot_t, tot_img = 0, 0.0, 0
     cores = 1
     for _ in range(args.steps):
-        d, p, t, cores = oracle_parallel(cfg, P, Nn, cen, mode, per)
+        d, p, t, cores, _ = oracle_parallel(cfg, P, Nn, cen, mode, per)
         tot_pairs += p
         tot_t += t
         tot_img += d
