@@ -688,3 +688,29 @@ def test_fuzz_against_oracle(spin, torch):
             np.testing.assert_array_equal(cells, brute, err_msg=what + " cells != brute")
         else:
             check(cells, ora, st, mode, what + " cells")
+
+
+def test_bilinear_near_normal_axis(spin, torch):
+    """BILINEAR splat positions of points on or near a centre's normal axis (alpha << |d|):
+    |d|^2 - beta^2 cancels there, so the GPU takes alpha^2 from Lagrange's identity
+    (reading 25).  Oblique normals, off-origin centres, points at 0 to 1e-3
+    rad off the axis across the whole beta window; both prunings."""
+    rng = np.random.default_rng(5)
+    for W, b in ((16, 0.02), (32, 0.01), (8, 0.05)):
+        n0 = rng.normal(size=3)
+        n0 /= np.linalg.norm(n0)
+        t1 = np.cross(n0, [0.3, 0.5, 0.8])
+        t1 /= np.linalg.norm(t1)
+        P0 = np.array([0.4, -0.3, 0.6])
+        xs = [P0]
+        for u in np.linspace(0.05, W - 1.05, 23):
+            beta = (W / 2 - u) * b
+            for off in (0.0, 1e-6, 1e-5, 1e-4, 1e-3):
+                xs.append(P0 + beta * n0 + off * abs(beta) * t1)
+        X = np.asarray(xs, np.float32)
+        Nn = np.tile(n0.astype(np.float32), (len(X), 1))
+        cen = [0, 7, 40]
+        ora, st = oracle(X, Nn, cen, W, b, 0.5, "bilinear")
+        for prune in ("brute", "cells"):
+            gpu = run_gpu(spin, torch, X, Nn, cen, W, b, 0.5, "bilinear", prune=prune)
+            check(gpu, ora, st, "bilinear", f"near-axis W={W} {prune}")
