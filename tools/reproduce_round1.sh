@@ -30,7 +30,18 @@ python tools/dls_sweep.py --config 5 --W 24 --reps 5 --units 0 > ${out}_dls_c5w2
 python tools/dls_sweep.py --config 2 --reps 5 --units 0 --slow 37 --slowdown 4 > ${out}_het_c2.jsonl 2>&1
 python tools/dls_sweep.py --config 2 --reps 5 --P 8 --units 0 --slow 2 --slowdown 4 > ${out}_het_c2_p8.jsonl 2>&1
 python tools/dls_sweep.py --config 2 --reps 5 --P 8 --units 0 --slow 2 --slowdown 4 --slow-first > ${out}_het_c2_p8_sf.jsonl 2>&1
+# 7.3: weighted factoring (WF) and adaptive weighted factoring (AWF)
+python tools/dls_sweep.py --config 2 --reps 5 --units 0 --slow 37 --slowdown 4 --policies STATIC,SS,GSS,FAC,WF,AWF > ${out}_het_c2_wf.jsonl 2>&1
+python tools/dls_sweep.py --config 2 --reps 5 --P 8 --units 0 --slow 2 --slowdown 4 --policies STATIC,SS,GSS,FAC,WF,AWF > ${out}_het_c2_p8_wf.jsonl 2>&1
+python tools/dls_sweep.py --config 3 --reps 5 --units 0 --policies STATIC,SS,FAC,WF,AWF > ${out}_dls_c3_wf.jsonl 2>&1
+python tools/dls_sweep.py --config 5 --reps 5 --units 0 --policies STATIC,SS,FAC,WF,AWF > ${out}_dls_c5_wf.jsonl 2>&1
+# 7.1/7.2: tensor-core vs packed-fp32 sphere filter, with stages switched off
+bash tools/ab_mma.sh > ${out}_ab_mma.txt 2>&1
+# §5: seeded fuzz campaigns against the oracle
+for seed in 1 2 3 4 5 6 7; do SPIN_FUZZ_SEED=$seed SPIN_FUZZ_CASES=150 python -m pytest tests/test_gpu_parity.py -q -k fuzz > ${out}_fuzz_$seed.log 2>&1; done
 # 7.1: isolated pair-test loop variants
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench/hotloop_mma tools/microbench/hotloop_mma.cu && \
+  tools/microbench/hotloop_mma > ${out}_hotloop_mma.jsonl 2>&1
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench/hotloop2 tools/microbench/hotloop2.cu && \
   tools/microbench/hotloop2 > ${out}_hotloop2.jsonl 2>&1
 echo done
