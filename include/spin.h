@@ -58,8 +58,8 @@ typedef enum {
  * speeds are known a priori — here those of the heterogeneous-worker emulation below
  * (slow CTAs 1/slowdown, the rest 1, normalised to mean 1).  AWF = adaptive weighted
  * factoring — the same rule with w_i = the worker's measured rate (units per busy time
- * over its chunks so far) over the mean rate of the workers that have reported (1 before
- * a worker's first chunk).  WF/AWF chunks depend on who requests, so they are claimed on
+ * over its chunks so far) over the mean rate of the workers that have reported; a worker
+ * without a measurement yet probes with a one-unit chunk.  WF/AWF chunks depend on who requests, so they are claimed on
  * the device by a compare-and-swap on the packed batch state; they need n_units < 2^24,
  * P < 2^16 and no shared multi-device dealer. */
 typedef enum { SPIN_STATIC = 0, SPIN_SS = 1, SPIN_GSS = 2, SPIN_FAC = 3, SPIN_WF = 4,

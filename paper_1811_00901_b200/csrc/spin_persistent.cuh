@@ -462,9 +462,10 @@ __device__ __forceinline__ void apply(const KParams& p, const Dec& d, uint32_t* 
 // ------------------------------------------------------------------ WF / AWF dealer
 // Weighted factoring (beyond the paper, its future work P:238; spin.h SPIN_WF / SPIN_AWF),
 // called by warp 0: this worker's integer weight (mean 1024) — a priori (WF) or from the
-// measured rates (AWF: mine over the mean of the workers that have reported; 1024 before
-// my first chunk) — then lane 0 claims [wu[0], wu[1]) by compare-and-swap on the packed
-// state (next : 24 | batch R : 24 | count : 16): a batch of P claims shares R = the units
+// measured rates (AWF: mine over the mean of the workers that have reported; a one-unit
+// probing chunk before my first measurement) — then lane 0 claims [wu[0], wu[1]) by
+// compare-and-swap on the packed state (next : 24 | batch R : 24 | count : 16): a batch
+// of P claims shares R = the units
 // left at its first claim (FAC2 batches), the same integer rule as the host
 // trace (spin_api.cpp wf_chunk).  Out of line: one call per chunk.
 static __device__ __noinline__ void wf_claim(const KParams& p, int lane, int* wu,
@@ -482,7 +483,9 @@ static __device__ __noinline__ void wf_claim(const KParams& p, int lane, int* wu
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     const float mine = rates[blockIdx.x];
-    wq = 1024u;
+    // before its first measurement a worker probes with a one-unit chunk (weight 0 -> the
+    // minimum chunk), so the weights are known before the large early chunks
+    wq = 0u;
     if (mine > 0.f && cnt > 0)
       wq = (unsigned)fminf(fmaxf(rintf(1024.f * mine * (float)cnt / sum), 16.f), 65536.f);
   }
