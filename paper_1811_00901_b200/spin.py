@@ -279,6 +279,8 @@ class SpinEngine:
                  cta_capacity=0, stream=None, slow_ctas=0, slowdown=0.0, slow_first=False,
                  grid=0, cta_offset=0, shared_counter=None):
         """Images for device int32 centre_idx [M] into a device fp32 [M, W, W] tensor.
+        schedule: STATIC / SS / GSS / FAC (the paper's), WF / AWF (weighted factoring; the
+        WF weights come from the slow-worker emulation below).
         slow_ctas / slowdown / slow_first: heterogeneous-worker emulation (timing only).
         grid / cta_offset / shared_counter (device address of a zeroed u32): one schedule
         dealt across devices; only this device's chunks are written to `out`."""
