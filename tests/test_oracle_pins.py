@@ -386,3 +386,24 @@ def test_weighted_factoring_pins():
                 if 0 < S < P:
                     assert max(batch[:S]) <= min(batch[S:])
             R = left
+
+
+def test_bilinear_on_the_normal_axis():
+    """Points on the centre's normal axis have alpha = 0 exactly: all their BILINEAR weight
+    lies in column 0, split between rows i0 = floor(u) and i0 + 1 by a = u - i0 with
+    u = W/2 - beta/b (reading 12; the GPU's near-axis splat, reading 25, is
+    checked against this).  Dyadic inputs: every step is exact."""
+    W, b = 8, 0.25
+    zs = [-0.75, -0.5, -0.3125, 0.0625, 0.5, 0.8125]
+    X = np.array([[0.0, 0.0, 0.0]] + [[0.0, 0.0, z] for z in zs], np.float32)
+    Nn = np.tile(np.array([0.0, 0.0, 1.0], np.float32), (len(X), 1))
+    img = O.generate(X, Nn, [0], W, b, -math.inf, O.BILINEAR)[0]
+    exp = np.zeros((W, W))
+    for z in [0.0] + zs:
+        u = W / 2 - z / b
+        i0 = math.floor(u)
+        if 0 <= i0 <= W - 2:
+            exp[i0, 0] += 1 - (u - i0)
+            exp[i0 + 1, 0] += u - i0
+    assert np.array_equal(img, exp)
+    assert np.all(img[:, 1:] == 0)
