@@ -188,6 +188,10 @@ spin_status spin_load_cloud(spin_handle h, const float* points, const float* nor
  * this call returns if stats != NULL, else the next call on the handle returns.
  * d_centre_idx and d_out must not alias each other or handle memory.  A handle is
  * not safe for concurrent spin_generate calls (shared scratch): serialise per handle.
+ * CUDA graphs: a call may be captured (stream capture) once an uncaptured call with
+ * the same (W, mode, prune, sched, cp, M) has set up the handle's tables and grid; a
+ * captured call records only memsets and kernels, skips the deferred error report
+ * and refuses stats (SPIN_E_INVAL).  Replays reuse the captured pointers and sizes.
  */
 spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M, int32_t W,
                           double b, double cos_As, spin_schedule sched,

@@ -497,8 +497,14 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
                           float* d_out, spin_stats* stats, spin_stream stream) {
   if (!h) return fail(SPIN_E_INVAL, "null handle");
   cudaStream_t s = (cudaStream_t)stream;
+  // inside a stream capture (CUDA graphs) nothing may synchronise or query events: the
+  // deferred error report is skipped and stats are refused
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) cap = cudaStreamCaptureStatusNone;
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  if (capturing && stats) return fail(SPIN_E_INVAL, "stats synchronise the stream: not inside a stream capture");
   // ---- a deferred SPIN_E_RANGE / overflow from an earlier asynchronous call
-  if (h->err_pending && cudaEventQuery(h->ev_err) == cudaSuccess) {
+  if (!capturing && h->err_pending && cudaEventQuery(h->ev_err) == cudaSuccess) {
     h->err_pending = false;
     if (h->h_err[0]) { h->h_err[0] = 0; return fail(SPIN_E_RANGE, "an earlier call saw a centre index outside [0, N)"); }
     if (h->h_err[1]) { h->h_err[1] = 0; return fail(SPIN_E_OVERFLOW, "an earlier call overflowed a bin accumulator"); }
@@ -823,13 +829,17 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   // ---- a6-a13: the persistent launch
   if (!cpar.d_counter) CK(cudaMemsetAsync(h->counter, 0, sizeof(unsigned), s), "memset");
   CK(cudaMemsetAsync(h->stats, 0, ST_NSLOTS * sizeof(unsigned long long), s), "memset");
-  CK(cudaEventRecord(h->ev0, s), "event");
+  if (!capturing) CK(cudaEventRecord(h->ev0, s), "event");
   CK(launch_spin(lc, (int)mode, (int)prune, grid, p, s), "spin kernel launch");
-  CK(cudaEventRecord(h->ev1, s), "event");
-  CK(cudaMemcpyAsync(h->h_err, h->err, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "err readback");
-  CK(cudaMemsetAsync(h->err, 0, 2 * sizeof(int32_t), s), "memset");
-  CK(cudaEventRecord(h->ev_err, s), "event");
-  h->err_pending = true;
+  if (!capturing) {
+    CK(cudaEventRecord(h->ev1, s), "event");
+    CK(cudaMemcpyAsync(h->h_err, h->err, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "err readback");
+    CK(cudaMemsetAsync(h->err, 0, 2 * sizeof(int32_t), s), "memset");
+    CK(cudaEventRecord(h->ev_err, s), "event");
+    h->err_pending = true;
+  } else {
+    CK(cudaMemsetAsync(h->err, 0, 2 * sizeof(int32_t), s), "memset");
+  }
 
   if (stats) {
     CK(cudaStreamSynchronize(s), "stats sync");

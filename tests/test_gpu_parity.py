@@ -714,3 +714,36 @@ def test_bilinear_near_normal_axis(spin, torch):
         for prune in ("brute", "cells"):
             gpu = run_gpu(spin, torch, X, Nn, cen, W, b, 0.5, "bilinear", prune=prune)
             check(gpu, ora, st, "bilinear", f"near-axis W={W} {prune}")
+
+
+def test_cuda_graph_capture(spin, torch):
+    """spin_generate can be captured in a CUDA graph after one uncaptured call (spin.h):
+    replays reproduce the images (BRUTE and CELLS, whose centre-ordering kernels are part
+    of the graph); stats inside a capture are refused."""
+    P, Nn = clouds.bumpy_sphere(5000, 17)
+    cen = _dev(torch, np.arange(0, 5000, 7, dtype=np.int32))
+    eng = spin.SpinEngine(_dev(torch, P), _dev(torch, Nn))
+    try:
+        s = torch.cuda.Stream()
+        for prune, mode in (("brute", "bilinear"), ("cells", "nearest")):
+            out = torch.empty((cen.shape[0], 16, 16), dtype=torch.float32, device="cuda")
+            with torch.cuda.stream(s):
+                eng.generate(cen, 16, 0.02, 0.5, out=out, schedule="SS", prune=prune, mode=mode)
+                torch.cuda.synchronize()
+                ref = out.clone()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    eng.generate(cen, 16, 0.02, 0.5, out=out, schedule="SS", prune=prune, mode=mode)
+                for _ in range(3):
+                    out.zero_()
+                    g.replay()
+                    torch.cuda.synchronize()
+                    assert torch.equal(out, ref), (prune, mode)
+        with torch.cuda.stream(s):
+            g2 = torch.cuda.CUDAGraph()
+            with pytest.raises(spin.SpinError):
+                with torch.cuda.graph(g2, stream=s):
+                    eng.generate(cen, 16, 0.02, 0.5, schedule="SS", stats=True)
+        torch.cuda.synchronize()
+    finally:
+        eng.close()
