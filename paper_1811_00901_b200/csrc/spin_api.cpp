@@ -603,7 +603,8 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   // mma.sync), whose operands B and K are rounded to tf32: |c~ - c'| <= 2^-11 |c'|.
   // fp32 error: 5u per term magnitude.  Tensor cores (x, y, z split into tf32 hi + lo,
   // w = -|x|^2 and K rounded to tf32, exact products, fp32 accumulation): 2^-21 |B||x| +
-  // 2^-12 (|x|^2 + |K|) plus an accumulation allowance of 2^-19 of the summed magnitudes
+  // 2^-11 (|x|^2 + |K|) (round to nearest at 11 significant bits) plus an accumulation
+  // allowance of 2^-19 of the summed magnitudes
   // (and 2^-100 absolute for flushed subnormals).  E bounds the filter in use, so every
   // region pair keeps m > 0.  The tensor cores are used unless their
   // looser bound grows the candidate sphere by more than 6% (clouds far from the origin
@@ -616,7 +617,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
     if (mma) {
       const double Kmax = 1.05 * (rho_o * rho_o + (X + amid) * (X + amid)) + 4.0 * E_o;
       const double BX = 2.02 * (X + amid) * X;
-      E_o += 1.01 * (std::ldexp(1.0, -21) * BX + std::ldexp(1.0, -12) * (X * X + Kmax) +
+      E_o += 1.01 * (std::ldexp(1.0, -21) * BX + std::ldexp(1.0, -11) * (X * X + Kmax) +
                      std::ldexp(1.0, -19) * (BX + X * X + Kmax)) + std::ldexp(1.0, -100);
     }
   };

@@ -983,7 +983,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           // r1 {z,z',-|x|^2,-|x'|^2} of the staged pair layout; see decode_entry).
           // hi = round to nearest tf32 (half an ulp of the 10-bit mantissa added, low 13
           // bits cleared; every |value| here is below 2^101), lo = x - hi (exact) cut to
-          // tf32: |x - hi - lo| <= 2^-21 |x|, |w - w_hi| <= 2^-12 |w| (planner's E_mma)
+          // tf32: |x - hi - lo| <= 2^-21 |x|, |w - w_hi| <= 2^-11 |w| (planner's E_mma)
           const float* sTf = reinterpret_cast<const float*>(sT);
           // B fragments of the group's centres (column gid = centre slot gid*NCB + cb,
           // rows tig and tig + 4)
