@@ -716,6 +716,7 @@ def test_bilinear_near_normal_axis(spin, torch):
             check(gpu, ora, st, "bilinear", f"near-axis W={W} {prune}")
 
 
+@pytest.mark.filterwarnings("ignore:The CUDA Graph is empty")  # the refused stats capture
 def test_cuda_graph_capture(spin, torch):
     """spin_generate can be captured in a CUDA graph after one uncaptured call (spin.h):
     replays reproduce the images (BRUTE and CELLS, whose centre-ordering kernels are part
