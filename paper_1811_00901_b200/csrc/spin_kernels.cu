@@ -23,10 +23,8 @@ static const void* kernel_for(int mode, int prune, int G, int sup, int nt, int d
 
 LaunchCfg choose_launch(int W, int mode, int prune) {
   // One CTA per SM.  Images live in shared memory (NEAREST 4 B/bin, BILINEAR 6 B/bin);
-  // take the largest G in {64, 32, 16, 8, 4} whose 768-thread layout fits.  When that
-  // G is below 32 (BRUTE, W > 24), a 512-thread CTA with G = 32 is taken instead: its
-  // smaller staged tile frees the room, and tile reuse by 32 centres beats the extra
-  // warps (C4: 524 -> 469 ms).
+  // CELLS take the largest G <= 32 whose 768-thread layout fits; BRUTE the first entry
+  // of the measured preference list below that fits.
   constexpr int LIMIT = 220 * 1024;
   LaunchCfg lc;
   lc.threads = NT_DEFAULT;
