@@ -2,11 +2,15 @@
 """bench.py — throughput of the spin-image hot path on B200 (one JSON line on rank 0).
 
 A "step" is one spin_generate call over the whole configured workload (every §8(a)
-row: dealing, pair test, accept path, write-back).  Default workload = BASELINE.json
-configs[1] (C2: N = M = 100,000 bumpy sphere, W = 16, b = 0.02, 60 deg, brute force).
+row: dealing, pair test, accept path, write-back).  Default workload = the largest
+single-GPU configuration, BASELINE.json configs[3] (C4: N = M = 1,000,000 bumpy sphere,
+W = 32, b = 0.01, 90 deg, BILINEAR, brute force, 1e12 pairs, 4.1 GB of images); --config 2
+is C2.  The line also carries a "dls" record: the paper's experiment (STATIC vs SS / GSS /
+FAC) on the density-imbalanced cell-list workload C5 (W = 8),
+medians and quartiles over 5 repetitions, with its own clock record.
 
-  python bench.py [--gpus N --steps K --warmup W] [--config 2] [--mode bilinear]
-                  [--schedule GSS] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config 4] [--mode bilinear]
+                  [--schedule GSS] [--impl reference] [--no-dls]
 
 Timing: CUDA events on the launching stream around each step, L2 flushed (256 MB
 write) before every step, max over ranks.  `value` = pair evaluations/s over all
@@ -41,7 +45,7 @@ def parse(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="spin", choices=["spin", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--dealer", choices=("local", "shared"), default="local",
                     help="shared: ONE schedule of the configured centres dealt to every GPU's "
                          "CTAs from one counter on GPU 0 (CUDA IPC / NVLink peer atomics; the "
@@ -61,6 +65,13 @@ def parse(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dls", action="store_true", help="skip the C5 DLS record")
+    ap.add_argument("--dls-reps", type=int, default=5)
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
+                    help="process-group backend for the barrier / max-over-ranks timing "
+                         "(gloo: CPU tensors, for the 2-rank test with both ranks on one GPU)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="every rank on cuda:0 (test of the shared-dealer plumbing on one GPU)")
     return ap.parse_args(argv)
 
 
@@ -185,61 +196,30 @@ class ClockSampler:
 
 # ----------------------------------------------------------------- oracle legs
 
-def oracle_sample(cfg, P, Nn, cen, mode, seconds):
-    """Time the oracle as it stands on a bounded sample of the workload's images."""
-    from oracle import spin_oracle as O
-    m = O.NEAREST if mode == "nearest" else O.BILINEAR
-    brute = cfg["prune"] == "brute"
-    gen = O.generate if brute else O.generate_cells
-    grid = None
-    done, pairs = 0, 0
-    t0 = time.perf_counter()
-    idx = 0
-    if not brute:
-        grid = O.CellGrid(P, O.region_radius(cfg["W"], cfg["b"], m))
-    while time.perf_counter() - t0 < seconds and idx < len(cen):
-        c = cen[idx:idx + 1]
-        gen(P, Nn, c, cfg["W"], cfg["b"], cfg["cos_As"], m)
-        pairs += len(P) if brute else len(grid.neighbours(P[int(c[0])]))
-        done += 1
-        idx += 1
-    dt = time.perf_counter() - t0
-    return done, pairs, dt
-
-
-THREAD_VARS = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")
-
-
-def _oracle_worker(job):
-    """One host core: the oracle on an interleaved slice of the images, time-bounded."""
-    cfg, P, Nn, cen, mode, seconds = job
-    return oracle_sample(cfg, P, Nn, cen, mode, seconds)
-
-
-def oracle_parallel(cfg, P, Nn, cen, mode, seconds, cores=None):
-    """The oracle as it stands, one process per host core (spawned: no CUDA state is
-    inherited), each on every cores-th image; throughput = all pairs / the slowest
-    worker's own time (process start-up excluded)."""
-    import concurrent.futures as cf
-    import multiprocessing as mp
-    cores = cores or len(os.sched_getaffinity(0))
-    jobs = [(cfg, P, Nn, cen[i::cores], mode, seconds) for i in range(cores)]
-    saved = {k: os.environ.get(k) for k in THREAD_VARS}
-    os.environ.update({k: "1" for k in THREAD_VARS})   # one thread per worker process
-    try:
-        with cf.ProcessPoolExecutor(cores, mp_context=mp.get_context("spawn")) as ex:
-            res = list(ex.map(_oracle_worker, jobs))
-    finally:
-        for k, v in saved.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
-    done = sum(r[0] for r in res)
-    pairs = sum(r[1] for r in res)
-    dt = max(r[2] for r in res)
-    per_core = statistics.mean([r[1] / r[2] for r in res if r[2] > 0] or [0.0])
-    return done, pairs, dt, cores, per_core
+def oracle_rate(cfg, P, Nn, cen, mode, seconds, threads=0, max_images=None):
+    """The C++ oracle (oracle/spin_oracle.cpp: double with certified bounds, std::thread over
+    images) as it stands, on a BOUNDED sample of the workload: images in workload order from
+    image 0, in growing batches until `seconds` of wall clock (CELLS: every batch builds
+    the oracle's own grid, which is part of its work).  Returns (images, pairs, seconds)."""
+    from oracle import spin_oracle_cpp as OC
+    m = OC.NEAREST if mode == "nearest" else OC.BILINEAR
+    gen = OC.generate if cfg["prune"] == "brute" else OC.generate_cells
+    limit = len(cen) if max_images is None else min(len(cen), max_images)
+    done = pairs = 0
+    t_tot = 0.0
+    batch = 8
+    while t_tot < seconds and done < limit:
+        c = cen[done:min(limit, done + batch)]
+        st = {}
+        t0 = time.perf_counter()
+        gen(P, Nn, c, cfg["W"], cfg["b"], cfg["cos_As"], m, stats=st, threads=threads)
+        dt = time.perf_counter() - t0
+        t_tot += dt
+        pairs += st["visited"]
+        done += len(c)
+        left = seconds - t_tot
+        batch = int(max(1, min(4 * len(c), len(c) * left / max(dt, 1e-9))))
+    return done, pairs, t_tot
 
 
 def cpu_model():
@@ -252,18 +232,33 @@ def cpu_model():
     return None
 
 
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def cpu_baseline_dict(cfg, P, Nn, cen, mode, seconds):
-    done, pairs, dt, cores, per_core = oracle_parallel(cfg, P, Nn, cen, mode, seconds)
+    """BASELINE.md's CPU row: the oracle on every host core after the GPU timing (a
+    reported baseline, not the target), plus one thread on a <= 200-image subsample."""
+    T = host_threads()
+    done, pairs, dt = oracle_rate(cfg, P, Nn, cen, mode, seconds, threads=T)
+    d1, p1, t1 = oracle_rate(cfg, P, Nn, cen, mode, min(5.0, seconds / 2), threads=1, max_images=200)
     kind = "visited" if cfg["prune"] == "cells" else "all"
-    return {"value": pairs / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{done} of {len(cen)} images of {cfg['name']} ({kind} pairs, numpy float64 "
-                      f"+ exact fallback; {cores} processes, one per host core, each on every "
-                      f"{cores}-th image for {seconds:.0f} s; {dt:.1f} s slowest worker)",
-            "images_per_s": done / dt, "per_core_value": per_core,
+    return {"value": pairs / dt, "unit": UNIT, "cores": T, "kind": "oracle",
+            "sample": f"{done} of {len(cen)} images of {cfg['name']} in workload order ({kind} pairs; "
+                      f"C++ oracle: double with certified bounds, escalation to threshold form in "
+                      f"double / __float128 / exact; std::thread x {T}; {dt:.1f} s)",
+            "images_per_s": done / dt,
+            "single_thread": {"value": p1 / t1, "images": d1, "seconds": t1},
             "cpu_model": cpu_model()}
 
 
 def run_reference(args):
+    """--impl reference: there is no reference implementation, so the
+    reference arm is the oracle as it stands (C++, every host core), each step a bounded
+    sample of the same workload; rank 0 only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
@@ -275,12 +270,12 @@ def run_reference(args):
     P, Nn = clouds.make_cloud(args.config)
     cen = rank_centres(args.config, cfg["N"], 0)
     per = max(1.0, args.cpu_seconds / max(1, args.steps + args.warmup))
+    T = host_threads()
     for _ in range(args.warmup):
-        oracle_sample(cfg, P, Nn, cen, mode, min(per, 2.0))
+        oracle_rate(cfg, P, Nn, cen, mode, min(per, 2.0), threads=T)
     tot_pairs, tot_t, tot_img = 0, 0.0, 0
-    cores = 1
     for _ in range(args.steps):
-        d, p, t, cores, _ = oracle_parallel(cfg, P, Nn, cen, mode, per)
+        d, p, t = oracle_rate(cfg, P, Nn, cen, mode, per, threads=T)
         tot_pairs += p
         tot_t += t
         tot_img += d
@@ -292,10 +287,10 @@ def run_reference(args):
             "config": {"workload": cfg["name"], "N": cfg["N"], "M": cfg["M"], "W": cfg["W"],
                        "b": cfg["b"], "cos_As": cfg["cos_As"], "mode": mode, "prune": cfg["prune"],
                        "sample": "each step: images of the workload in order for a bounded time"},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": T, "kind": "oracle",
                              "sample": f"{tot_img} images of {cfg['name']} over {args.steps} steps "
-                                       f"(numpy float64 + exact fallback, {cores} processes, "
-                                       f"one per host core)"},
+                                       f"(C++ oracle, std::thread x {T})",
+                             "cpu_model": cpu_model()},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "images_per_s": tot_img / tot_t}
     print(json.dumps(line), flush=True)
@@ -303,6 +298,73 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------- the GPU arm
+
+def quartiles(x):
+    """min / Q1 / median / Q3 / max / mean, inclusive linear interpolation."""
+    x = np.sort(np.asarray(x, np.float64))
+    q = np.quantile(x, [0.0, 0.25, 0.5, 0.75, 1.0])
+    return dict(min=float(q[0]), q1=float(q[1]), median=float(q[2]), q3=float(q[3]),
+                max=float(q[4]), mean=float(x.mean()))
+
+
+def dls_record(spin, torch, dev, reps: int):
+    """The paper's experiment (STATIC vs SS / GSS / FAC) on one
+    B200: workers = the persistent CTAs, master = the device chunk counter, workload = the
+    density-imbalanced cell-list config C5 at W = 8 (NEAREST, bit-exact).  Repetitions are
+    interleaved over the policies; times are the spin kernel's CUDA-event durations;
+    "beats STATIC" = median below STATIC's median and Q3 below STATIC's Q1.
+    Clocks are sampled during these repetitions."""
+    from synth import clouds
+    cfg = dict(clouds.CONFIGS[5])
+    W, b, c = 8, cfg["b"], cfg["cos_As"]
+    P, Nn = clouds.make_cloud(5)
+    cen = clouds.make_centres(5, cfg["N"])
+    eng = spin.SpinEngine(torch.from_numpy(P).to(dev), torch.from_numpy(Nn).to(dev))
+    try:
+        d_cen = torch.from_numpy(cen).to(dev)
+        out = torch.empty((len(cen), W, W), dtype=torch.float32, device=dev)
+        pols = ("STATIC", "SS", "GSS", "FAC")
+        kw = dict(mode="nearest", prune="cells", out=out)
+        eng.generate(d_cen, W, b, c, schedule="STATIC", **kw)     # builds and caches the grid
+        torch.cuda.synchronize()
+        ref = out.clone()
+        identical = True
+        for pol in pols:                                          # warm-up, and same images
+            eng.generate(d_cen, W, b, c, schedule=pol, **kw)
+            torch.cuda.synchronize()
+            identical &= bool(torch.equal(out, ref))
+        times = {p: [] for p in pols}
+        busy = {p: [] for p in pols}
+        meta = {}
+        clock = ClockSampler(dev.index or 0)
+        clock.start()
+        for _ in range(reps):
+            for pol in pols:
+                _, st = eng.generate(d_cen, W, b, c, schedule=pol, stats=True, cta_capacity=4096, **kw)
+                times[pol].append(st["elapsed_ms"])
+                npc = min(st["P"], 4096)
+                bt = (st["cta_end_ns"][:npc] - st["cta_start_ns"][:npc]).astype(np.float64)
+                busy[pol].append(float(bt.max() / bt.mean()))
+                meta[pol] = (st["P"], st["G"], st["n_chunks"])
+        clocks = clock.stop()
+        torch.cuda.synchronize()
+        identical &= bool(torch.equal(out, ref))
+        q = {p: quartiles(times[p]) for p in pols}
+        s = q["STATIC"]
+        return {"workload": f"{cfg['name']} W={W} (cells, NEAREST, {len(cen)} random centres)",
+                "reps": reps, "P": meta["STATIC"][0], "unit_images": meta["STATIC"][1],
+                "n_chunks": {p: meta[p][2] for p in pols},
+                "kernel_ms": q,
+                "speedup_vs_static": {p: s["median"] / q[p]["median"] for p in pols if p != "STATIC"},
+                "beats_static": {p: bool(q[p]["median"] < s["median"] and q[p]["q3"] < s["q1"])
+                                 for p in pols if p != "STATIC"},
+                "cta_busy_max_over_mean": {p: float(np.median(busy[p])) for p in pols},
+                "images_identical_across_policies": identical,
+                "rule": "beats STATIC = median below STATIC's median and Q3 below STATIC's Q1",
+                "clocks": clocks}
+    finally:
+        eng.close()
+
 
 def load_traffic(cfg_name, mode):
     path = os.path.join(ROOT, "profiles", "traffic.json")
@@ -316,9 +378,11 @@ def load_traffic(cfg_name, mode):
 def run_spin(args):
     import torch
     rank, world, local = dist_env()
-    dist_init("nccl")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dist_init(args.dist_backend)
+    gpu = 0 if args.same_device else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    cdev = dev if args.dist_backend == "nccl" else None     # device of the timing collectives
     from paper_1811_00901_b200 import spin
     from synth import clouds
 
@@ -371,7 +435,7 @@ def run_spin(args):
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, L2 flushed before each, events on the launching stream
-    clock = ClockSampler(local)
+    clock = ClockSampler(gpu)
     clock.start()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
@@ -387,7 +451,7 @@ def run_spin(args):
     barrier()
     clocks = clock.stop()
     step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
-    total_ms = allreduce_max(sum(step_ms), dev)
+    total_ms = allreduce_max(sum(step_ms), cdev)
     ms_per_step = total_ms / args.steps
 
     # ---- dominant kernel: its own CUDA-event duration (library stats, same stream)
@@ -403,7 +467,7 @@ def run_spin(args):
     # secondary (same run): the support test on every pair in the hot loop, the paper's
     # order (P:166 before P:169-171) -- identical images; reported beside the main line
     alt = None
-    pairs_all_est = allreduce_sum(pairs_step, dev) if dealer is None else pairs_step
+    pairs_all_est = allreduce_sum(pairs_step, cdev) if dealer is None else pairs_step
     if args.support == "auto" and cfg["cos_As"] > -math.inf:
         akw = dict(kw, flags=spin.F_SUPPORT_FIRST)
         for _ in range(2):
@@ -418,7 +482,7 @@ def run_spin(args):
             gen(d_cen, W, b, c, pre=False, **akw)
             e1.record(stream)
         torch.cuda.synchronize()
-        a_ms = allreduce_max(sum(e0.elapsed_time(e1) for e0, e1 in aev), dev) / args.steps
+        a_ms = allreduce_max(sum(e0.elapsed_time(e1) for e0, e1 in aev), cdev) / args.steps
         _, ast = gen(d_cen, W, b, c, stats=True, **akw)
         alt = {"flag": "SPIN_F_SUPPORT_FIRST", "value": pairs_all_est / (a_ms * 1e-3),
                "unit": UNIT, "ms_per_step": a_ms, "kernel_ms": ast["elapsed_ms"],
@@ -428,8 +492,8 @@ def run_spin(args):
                "note": "support test n.n_x >= cos_As on every pair in the hot loop; images identical"}
 
     if dealer is None:
-        pairs_all = allreduce_sum(pairs_step, dev)   # = pairs_step * world for weak scaling
-        M_all = int(allreduce_sum(M, dev))
+        pairs_all = allreduce_sum(pairs_step, cdev)   # = pairs_step * world for weak scaling
+        M_all = int(allreduce_sum(M, cdev))
     else:
         pairs_all, M_all = pairs_step, M             # one schedule of M images over all ranks
     value = pairs_all * args.steps / (total_ms * 1e-3)
@@ -452,7 +516,7 @@ def run_spin(args):
             eng.load_cloud(hP, hN)                                  # H2D 24 N bytes
             eng.generate_host(hC.numpy(), W, b, c, out=hO.numpy(), **ekw)   # H2D 4M, D2H 4MW^2
         torch.cuda.synchronize()
-        e2e_s = allreduce_max(time.perf_counter() - t0, dev)
+        e2e_s = allreduce_max(time.perf_counter() - t0, cdev)
         e2e = {"value": pairs_all * args.e2e_steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(24 * N + 4 * M), "d2h_bytes_per_step": int(4 * M * W * W),
                "images_per_s": M_all * args.e2e_steps / e2e_s,
@@ -461,6 +525,9 @@ def run_spin(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_dict(cfg, P, Nn, cen, mode, args.cpu_seconds)
+    dls = None
+    if world == 1 and not args.no_dls:
+        dls = dls_record(spin, torch, dev, args.dls_reps)
 
     # CELLS: the implementation-independent work measure (pairs within the region radius
     # R of their centre), counted by a separate diagnostic kernel after timing
@@ -511,6 +578,7 @@ def run_spin(args):
         "e2e": e2e,
         "gpu_launches": launches * args.steps,
         "cpu_baseline": cpu,
+        "dls": dls,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SPIN_ABI_VERSION 5
+#define SPIN_ABI_VERSION 6
 
 typedef struct spin_ctx* spin_handle;
 typedef struct CUstream_st* spin_stream; /* identical to cudaStream_t */
@@ -157,7 +157,10 @@ spin_status spin_create(const float* points, const float* normals, int64_t N,
 /*
  * spin_load_cloud — replace the handle's cloud (same rules as spin_create).
  * Reuses the device buffers when N fits the current capacity; cached cell grids
- * are invalidated.  Synchronises `stream`.
+ * are invalidated.  Synchronises `stream`.  If it fails after the argument checks
+ * (SPIN_E_INPUT, SPIN_E_NOMEM, SPIN_E_CUDA) the handle holds NO cloud: every later
+ * spin_generate / spin_count_in_sphere / spin_pair_codes returns SPIN_E_INVAL until a
+ * load succeeds (never a mix of the old and the new cloud).
  */
 spin_status spin_load_cloud(spin_handle h, const float* points, const float* normals,
                             int64_t N, spin_stream stream);
@@ -238,6 +241,24 @@ double spin_region_radius(int32_t W, double b, spin_mode mode, uint32_t flags);
  * synchronises `stream`. */
 spin_status spin_count_in_sphere(spin_handle h, const int32_t* d_centre_idx, int64_t M, double R,
                                  int64_t* count, spin_stream stream);
+
+/* spin_pair_codes — DIAGNOSTIC (tests only; not part of spin_generate).  For each of the
+ * M centres d_centre_idx[m] and EVERY cloud point j (handle order), the accept path's
+ * certified per-pair decision (the same device functions spin_generate runs on every
+ * candidate: fp32 with certified bounds, then fp64, then exact) under the same region
+ * constants (Alg. 1 lines P:166-174; readings of DESIGN.md §3):
+ *   d_codes[m * N + j] = -1 if the pair does not contribute, else
+ *                        NEAREST  k * W + l   (its bin),
+ *                        BILINEAR i0 * W + j0 (the splat's base corner, reading #12).
+ * d_codes is int32 [M][N] device memory owned by the caller.  NEAREST codes equal the
+ * exact definition's; BILINEAR region decisions do too, while (i0, j0) may differ from an
+ * exact evaluation only for pairs within fp32 rounding of an INTERIOR bin edge, where the
+ * splat is continuous (the "flips" the parity tests count and report).  Asynchronous on
+ * `stream`.  SPIN_E_INVAL as spin_generate (bad W, b, cos_As, mode, flags, null pointers)
+ * or when the handle holds no valid cloud. */
+spin_status spin_pair_codes(spin_handle h, const int32_t* d_centre_idx, int64_t M, int32_t W,
+                            double b, double cos_As, spin_mode mode, uint32_t flags,
+                            int32_t* d_codes, spin_stream stream);
 
 /* spin_cos_from_degrees — cos of an angle in degrees, exact at 0, 60, 90, 120, 180
  * (1, 0.5, 0, -0.5, -1); >= 180 degrees returns -INFINITY (test disabled). */

@@ -12,7 +12,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "spin_oracle.cpp")
 OUT = os.path.join(HERE, "libspin_oracle.so")
-CMD = ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+CMD = ["g++", "-O2", "-march=x86-64-v3", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
        "-pthread", "-Wall", "-o", OUT + ".tmp", SRC]
 
 

@@ -39,7 +39,8 @@
 // BILINEAR weights are evaluated in double from u and v (continuous inside the region).
 //
 // Oracle-CELLS: an independent uniform grid (edge 1.0001 R, R = the region radius), the
-// 27 cells around the centre's cell, the same per-pair decision -> equals oracle-BRUTE.
+// 27 cells around the centre's cell, the same per-pair decision -> equals oracle-BRUTE
+// (NEAREST bit for bit; BILINEAR up to the order of the double sums, ~1e-16).
 //
 // Pins (tests/test_oracle_cpp.py, -m "not gpu"): the hand-worked goldens X1-X4, the
 // config-1 closed form, total weight = in-region count, signed-permutation / dyadic
@@ -463,16 +464,17 @@ struct Unsure {
   int64_t m, j;
 };
 
-// the image of centre ci over the candidate points cand[0..nc) (all points: cand = null)
-void image_of(const Job& J, int64_t m, int64_t ci, const int64_t* cand, int64_t nc, ImageOut& io,
-              PairStats& ps, std::vector<Unsure>& uns) {
+// the image of centre ci over the points Xs[a..b) (Xs/Ns: the cloud itself, or the
+// grid's cell-sorted copy, whose original indices idx[] name the undecided pairs)
+void image_of(const Job& J, int64_t m, int64_t ci, const float* Xs, const float* Ns,
+              const int64_t* idx, int64_t a, int64_t b, ImageOut& io, PairStats& ps,
+              std::vector<Unsure>& uns) {
   const float* p = J.X + 3 * ci;
   const float* n = J.Nr + 3 * ci;
-  for (int64_t t = 0; t < nc; ++t) {
-    const int64_t j = cand ? cand[t] : t;
-    const Outcome o = decide_pair(J, p, n, J.X + 3 * j, J.Nr + 3 * j, ps);
+  for (int64_t t = a; t < b; ++t) {
+    const Outcome o = decide_pair(J, p, n, Xs + 3 * t, Ns + 3 * t, ps);
     if (o.state == 1) splat(J, o, io);
-    else if (o.state == 2) uns.push_back({m, j});
+    else if (o.state == 2) uns.push_back({m, idx ? idx[t] : t});
   }
 }
 
@@ -496,11 +498,12 @@ struct Grid {
   double h, o[3];
   int64_t dim[3];
   std::vector<int64_t> key_sorted, idx_sorted;
+  std::vector<float> Xs, Ns;   // the cloud in cell order (contiguous reads per cell)
   int64_t cell(const double* x, int64_t c3[3]) const {
     for (int a = 0; a < 3; ++a) c3[a] = (int64_t)std::floor((x[a] - o[a]) / h);
     return (c3[2] * dim[1] + c3[1]) * dim[0] + c3[0];
   }
-  void build(const float* X, int64_t N, double R) {
+  void build(const float* X, const float* Nr, int64_t N, double R) {
     h = 1.0001 * R;
     for (int a = 0; a < 3; ++a) {
       o[a] = INFINITY;
@@ -521,9 +524,19 @@ struct Grid {
     std::sort(kv.begin(), kv.end());
     key_sorted.resize((size_t)N);
     idx_sorted.resize((size_t)N);
-    for (int64_t i = 0; i < N; ++i) { key_sorted[i] = kv[i].first; idx_sorted[i] = kv[i].second; }
+    Xs.resize((size_t)N * 3);
+    Ns.resize((size_t)N * 3);
+    for (int64_t i = 0; i < N; ++i) {
+      key_sorted[i] = kv[i].first;
+      idx_sorted[i] = kv[i].second;
+      for (int a = 0; a < 3; ++a) {
+        Xs[3 * i + a] = X[3 * kv[i].second + a];
+        Ns[3 * i + a] = Nr[3 * kv[i].second + a];
+      }
+    }
   }
-  void neighbours(const float* p, std::vector<int64_t>& out) const {
+  // the [lo, hi) ranges (in cell order) of the 27 cells around p's cell
+  void neighbours(const float* p, std::vector<std::pair<int64_t, int64_t>>& out) const {
     out.clear();
     const double x[3] = {p[0], p[1], p[2]};
     int64_t c[3];
@@ -538,9 +551,8 @@ struct Grid {
           const int64_t key = (k3[2] * dim[1] + k3[1]) * dim[0] + k3[0];
           auto lo = std::lower_bound(key_sorted.begin(), key_sorted.end(), key);
           auto hi = std::upper_bound(lo, key_sorted.end(), key);
-          for (auto it = lo; it != hi; ++it) out.push_back(idx_sorted[it - key_sorted.begin()]);
+          if (hi > lo) out.push_back({lo - key_sorted.begin(), hi - key_sorted.begin()});
         }
-    std::sort(out.begin(), out.end());   // the brute-force visiting order (bit-equal sums)
   }
 };
 
@@ -572,7 +584,7 @@ int so_generate(const float* X, const float* Nr, int64_t N, const int32_t* cen, 
   std::memset(out, 0, sizeof(double) * (size_t)(M * WW));
   if (contrib) std::memset(contrib, 0, sizeof(int32_t) * (size_t)(M * WW));
   Grid grid;
-  if (cells) grid.build(X, N, region_radius(W, b, mode, flags));
+  if (cells) grid.build(X, Nr, N, region_radius(W, b, mode, flags));
   std::atomic<int64_t> next(0);
   std::mutex mu;
   std::vector<Unsure> all_uns;
@@ -580,7 +592,7 @@ int so_generate(const float* X, const float* Nr, int64_t N, const int32_t* cen, 
   auto worker = [&]() {
     PairStats ps;
     std::vector<Unsure> uns;
-    std::vector<int64_t> cand;
+    std::vector<std::pair<int64_t, int64_t>> ranges;
     int64_t visited = 0;
     for (;;) {
       const int64_t m = next.fetch_add(1);
@@ -589,11 +601,14 @@ int so_generate(const float* X, const float* Nr, int64_t N, const int32_t* cen, 
       ImageOut io{out + m * WW, contrib ? contrib + m * WW : nullptr, 0};
       if (ci < 0 || ci >= N) continue;   // the caller validates; an invalid centre is empty
       if (cells) {
-        grid.neighbours(X + 3 * ci, cand);
-        image_of(J, m, ci, cand.data(), (int64_t)cand.size(), io, ps, uns);
-        visited += (int64_t)cand.size();
+        grid.neighbours(X + 3 * ci, ranges);
+        for (const auto& r : ranges) {
+          image_of(J, m, ci, grid.Xs.data(), grid.Ns.data(), grid.idx_sorted.data(), r.first,
+                   r.second, io, ps, uns);
+          visited += r.second - r.first;
+        }
       } else {
-        image_of(J, m, ci, nullptr, N, io, ps, uns);
+        image_of(J, m, ci, X, Nr, nullptr, 0, N, io, ps, uns);
         visited += N;
       }
       if (in_region) in_region[m] = io.in_region;

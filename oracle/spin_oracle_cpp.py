@@ -105,7 +105,10 @@ def _run(points, normals, centre_idx, W, b, cos_As, mode, flags, stats, cells, t
         stats["visited"] = stats.get("visited", 0) + int(st[3])
         stats.setdefault("in_region", []).extend(inr.tolist())
         if cnt is not None:
-            stats.setdefault("contributors", []).extend(list(cnt))
+            # one (M, W, W) block (np.stack of it is itself); appended blocks concatenate
+            prev = stats.get("contributors")
+            stats["contributors"] = cnt if prev is None or len(prev) == 0 else \
+                np.concatenate([np.asarray(prev), cnt])
     return out
 
 
@@ -124,6 +127,18 @@ def generate_cells(points, normals, centre_idx, W: int, b: float, cos_As: float,
 
 def region_radius(W: int, b: float, mode: int, flags: int = 0) -> float:
     return float(lib().so_region_radius(int(W), float(b), int(mode), int(flags)))
+
+
+def pair_codes(points, normals, centres, W: int, b: float, cos_As: float, mode: int,
+               flags: int = 0, threads: int = 0) -> np.ndarray:
+    """int32 [len(centres), N]: -1 or the pair's bin code (NEAREST k*W + l, BILINEAR
+    i0*W + j0) — the oracle side of the GPU's spin_pair_codes diagnostic."""
+    X = np.ascontiguousarray(points, np.float32)
+    out = np.empty((len(centres), len(X)), np.int32)
+    for i, c in enumerate(np.asarray(centres).reshape(-1)):
+        st, k, l, _, _ = pair_bins(X, normals, int(c), W, b, cos_As, mode, flags, threads)
+        out[i] = np.where(st == 1, k * W + l, -1)
+    return out
 
 
 def pair_bins(points, normals, c: int, W: int, b: float, cos_As: float, mode: int,
@@ -153,5 +168,5 @@ def pair_bins(points, normals, c: int, W: int, b: float, cos_As: float, mode: in
     return state, kk, ll, uu, vv
 
 
-__all__ = ["generate", "generate_cells", "region_radius", "pair_bins", "NEAREST", "BILINEAR",
+__all__ = ["generate", "generate_cells", "region_radius", "pair_bins", "pair_codes", "NEAREST", "BILINEAR",
            "F_LITERAL_HALF_WIDTH", "F_FLOOR_BINS", "math"]

@@ -263,6 +263,12 @@ spin_status load_cloud(spin_ctx* h, const float* points, const float* normals, i
   if (N < 1 || N >= ((int64_t)1 << 31) - 2 * TILE_POINTS)
     return fail(SPIN_E_INVAL, "N=%lld outside [1, 2^31 - 12288)", (long long)N);
   const int64_t Npad = ((N + 1 + TILE_POINTS - 1) / TILE_POINTS) * TILE_POINTS;  // >= 1 sentinel
+  // from here on the device copy is being replaced: until it is validated the handle holds
+  // NO cloud (spin_generate refuses with SPIN_E_INVAL), never a mix of old and new state
+  h->N = 0;
+  h->Npad = 0;
+  h->grid_valid = false;
+  h->cloud_version++;
   if (Npad > h->cap) {
     if (h->pos) cudaFree(h->pos);
     if (h->nrm) cudaFree(h->nrm);
@@ -306,8 +312,131 @@ spin_status load_cloud(spin_ctx* h, const float* points, const float* normals, i
   h->N = N;
   h->Npad = Npad;
   h->cloud_version++;
-  h->grid_valid = false;
   return SPIN_OK;
+}
+
+// a2: region constants and the certified fp32 thresholds of the hot loop and the accept
+// path, shared by spin_generate and the spin_pair_codes diagnostic
+void plan_thresholds(const spin_ctx* h, int32_t W, double b, double cos_As, bool has_support,
+                     spin_mode mode, spin_prune prune, uint32_t flags, const Region& rg,
+                     KParams& p) {
+  const double X = std::max((double)h->absmax, 1e-30) * (1.0 + 1e-6);
+  const double u = U32;
+  const double amid = std::fabs(rg.mid);
+  // hot loop (fp32): candidates are the pairs inside the sphere about the rounded window
+  // centre c~ = fl(2(p + mid n))/2 that contains the region cylinder (|beta - mid| <= h,
+  // alpha^2 <= Qmax), margin m = B.x - |x|^2 + K with B = 2c~, K = rho^2 - |c~|^2 + 2E
+  // (DESIGN.md 7.1).  |c~ - c'| <= u (X + |mid|) widens the radius.
+  // Two BRUTE filters share the margin: packed fp32 (FFMA2) and the tensor cores (tf32
+  // mma.sync), whose operands B and K are rounded to tf32: |c~ - c'| <= 2^-11 |c'|.
+  // fp32 error: 5u per term magnitude.  Tensor cores (x, y, z split into tf32 hi + lo,
+  // w = -|x|^2 and K rounded to tf32, exact products, fp32 accumulation): 2^-21 |B||x| +
+  // 2^-11 (|x|^2 + |K|) (round to nearest at 11 significant bits) plus an accumulation
+  // allowance of 2^-19 of the summed magnitudes
+  // (and 2^-100 absolute for flushed subnormals).  E bounds the filter in use, so every
+  // region pair keeps m > 0 (DESIGN.md 7.1).  The tensor cores are used unless their
+  // looser bound grows the candidate sphere by more than 6% (clouds far from the origin
+  // relative to the region size).
+  auto sphere = [&](bool mma, double& rho_o, double& E_o) {
+    const double shift = 1.01 * (mma ? std::ldexp(1.0, -11) : u) * (X + amid);
+    rho_o = std::sqrt(rg.h * rg.h + rg.Qmax) + shift;
+    const double Ms = rho_o * rho_o + (2.0 * X + amid) * (2.0 * X + amid) * 1.01;
+    E_o = 6.0 * u * Ms * 1.05;
+    if (mma) {
+      const double Kmax = 1.05 * (rho_o * rho_o + (X + amid) * (X + amid)) + 4.0 * E_o;
+      const double BX = 2.02 * (X + amid) * X;
+      E_o += 1.01 * (std::ldexp(1.0, -21) * BX + std::ldexp(1.0, -11) * (X * X + Kmax) +
+                     std::ldexp(1.0, -19) * (BX + X * X + Kmax)) + std::ldexp(1.0, -100);
+    }
+  };
+  double rho, E_sph, rho_f, E_f;
+  sphere(true, rho, E_sph);
+  sphere(false, rho_f, E_f);
+  const bool use_mma = prune == SPIN_BRUTE && std::getenv("SPIN_NO_MMA") == nullptr &&
+                       rho * rho + 3.0 * E_sph <= 1.06 * (rho_f * rho_f + 3.0 * E_f);
+  if (!use_mma) {
+    rho = rho_f;
+    E_sph = E_f;
+  }
+  const double shift = 1.01 * (use_mma ? std::ldexp(1.0, -11) : u) * (X + amid);
+  const double Es_h = 4.0 * u * 1.01;
+  // CELLS hot loop: the region cylinder in expanded forms (bounds hold inside the region)
+  const double Eb_h = 8.0 * u * (X + amid) * 1.01;
+  const double Et_h = 16.0 * u * (X + amid) * (X + amid) * 1.01;
+  const double Eq_h = Et_h + Eb_h * (2.0 * rg.h + Eb_h) + 2.0 * u * (rg.Qmax + 2.0 * (X + amid) * (X + amid));
+  p.b = b;
+  p.cos_As = has_support ? cos_As : -INFINITY;
+  p.A = 0.5 * W;
+  p.mid = rg.mid;
+  p.Qmax = rg.Qmax;
+  p.rho2 = rho * rho;
+  p.E_sph = E_sph;
+  p.mma = use_mma ? 1 : 0;
+  p.Eq_hot = Eq_h;
+  p.h_test = f32_up(rg.h + Eb_h);
+  p.c_test = has_support ? f32_down(cos_As - Es_h) : -INFINITY;
+  p.has_support = has_support ? 1 : 0;
+  // where the support test runs (same images either way): not at all without one; in the
+  // accept path only (SPIN_F_SUPPORT_LAST); on every pair (SPIN_F_SUPPORT_FIRST, and CELLS
+  // by default); BRUTE by default adaptively per warp (2)
+  p.support_in_hot = !has_support ? 0
+                     : (flags & SPIN_F_SUPPORT_LAST) ? 0
+                     : (flags & SPIN_F_SUPPORT_FIRST) ? 1
+                     : (prune == SPIN_BRUTE ? 2 : 1);
+  // candidates satisfy |d| <= D.  BRUTE: |x - c~|^2 <= rho^2 + 4E, so
+  // |d| <= |c~ - p| + sqrt(rho^2 + 4E).  CELLS: q <= Qmax + 2Eq, |beta| <= |mid| + h_test + Eb.
+  const double Dh = (amid + shift + std::sqrt(rho * rho + 4.0 * E_sph)) * 1.001;
+  const double Cmax = (X + amid) * (X + amid) * 1.01;
+  const double bmax = amid + (double)p.h_test + Eb_h;
+  const double D2c = (rg.Qmax + 2.0 * Eq_h + 4.0 * u * (rg.Qmax + Cmax) + bmax * bmax) * 1.001;
+  const double D2 = (prune == SPIN_BRUTE ? Dh * Dh : D2c) + 1e-30;
+  const double D = std::sqrt(D2);
+  // accept path, fp32 direct forms, valid while |d| <= D
+  const double Es_a = 5.5 * u * 1.01;
+  const double Eb_a = 4.2 * u * D * 1.002;
+  const double Edd_a = 5.2 * u * D2;
+  const double Eq_a = Edd_a + Eb_a * (2.0 * D + Eb_a) + 1.01 * u * D2;
+  double Eu_a;
+  if (!(flags & SPIN_F_LITERAL_HALF_WIDTH))
+    Eu_a = ((Eb_a + 1.01 * u * D) / b + u * (p.A + D / b)) * 1.01;
+  else  // u = fma(-beta, fl(1/b), fl(W/(2b))): rounding of both constants and the fma
+    Eu_a = (Eb_a + 4.01 * u * (p.A + D)) / b * 1.05;
+  const double Ew_a = (Eq_a + 2.01 * u * D2) / (b * b) * 1.01;
+  p.c_f = has_support ? (float)cos_As : -INFINITY;
+  p.inv_b = (float)(1.0 / b);
+  p.inv_b2 = (float)(1.0 / (b * b));
+  p.Af = (float)p.A;
+  p.Wf = (float)W;
+  p.Au = (flags & SPIN_F_LITERAL_HALF_WIDTH) ? (float)(p.A / b) : (float)p.A;
+  p.floor_f = (flags & SPIN_F_FLOOR_BINS) ? 1.0f : 0.0f;
+  p.Es_a = f32_up(Es_a);
+  p.Eu_a = f32_up(Eu_a);
+  p.Ew_a = f32_up(Ew_a);
+  p.D2g = f32_down(D2);
+  p.literal = (flags & SPIN_F_LITERAL_HALF_WIDTH) ? 1 : 0;
+  p.floor_bins = (flags & SPIN_F_FLOOR_BINS) ? 1 : 0;
+  p.no_fast_cert = (flags & SPIN_F_NO_FAST_CERT) ? 1 : 0;
+#ifdef SPIN_MEASURE
+  if (const char* dbg = std::getenv("SPIN_DEBUG_SKIP")) p.debug_skip = std::atoi(dbg);   // measurement builds only
+#endif
+  // self pair (d = 0): beta = q = 0 exactly, u = W/2 (scaled reading only)
+  p.self_fast = p.literal ? 0 : 1;
+  if (mode == SPIN_NEAREST) {
+    const int k = p.floor_bins ? (int)std::floor(p.A) : (int)std::ceil(p.A);
+    p.self_k = (k >= 0 && k < W) ? k : -1;
+    p.self_kf = (float)p.self_k;
+    p.self_l = 0;
+    p.self_a = 0.f;
+  } else {
+    const double i0 = std::floor(p.A);
+    const bool in = p.A >= 0.0 && p.A < W - 1.0;
+    p.self_k = in ? (int)i0 : -1;
+    p.self_l = 0;
+    p.self_a = (float)(p.A - i0);
+  }
+  if (!(Eu_a < 0.25 && Ew_a < 0.25)) p.no_fast_cert = 1;  // fp32 cannot resolve bins: skip it
+  if (p.no_fast_cert) p.D2g = -1.0f;   // the fp32 stage certifies nothing (decide: dd <= D2g fails)
+
 }
 
 spin_status ensure_grid(spin_ctx* h, float R, cudaStream_t s, double* build_ms) {
@@ -315,7 +444,9 @@ spin_status ensure_grid(spin_ctx* h, float R, cudaStream_t s, double* build_ms) 
   // measured against R/3 .. R/16: C3 41.9, C5 152.4, C5 W=24 561.7 ms at R/8, 42.4 /
   // 159.0 / 570.2 at R/4); grow it if the grid would exceed 2^24 cells
   double hh = 0.125 * R;
-  if (const char* c = std::getenv("SPIN_DEBUG_CELLS_PER_R")) hh = R / std::atof(c);   // measurement knob
+#ifdef SPIN_MEASURE
+  if (const char* c = std::getenv("SPIN_DEBUG_CELLS_PER_R")) hh = R / std::atof(c);   // measurement builds only
+#endif
   const double ex = std::max(1e-30, (double)h->aabb[3] - h->aabb[0]);
   const double ey = std::max(1e-30, (double)h->aabb[4] - h->aabb[1]);
   const double ez = std::max(1e-30, (double)h->aabb[5] - h->aabb[2]);
@@ -378,6 +509,7 @@ double spin_cos_from_degrees(double deg) {
 spin_status spin_count_in_sphere(spin_handle h, const int32_t* d_centre_idx, int64_t M, double R,
                                  int64_t* count, spin_stream stream) {
   if (!h || !count) return fail(SPIN_E_INVAL, "null handle or count");
+  if (h->N <= 0) return fail(SPIN_E_INVAL, "no valid cloud loaded (the last spin_load_cloud failed)");
   if (M < 0 || M >= ((int64_t)1 << 31)) return fail(SPIN_E_INVAL, "M=%lld out of range", (long long)M);
   if (!std::isfinite(R) || R <= 0.0 || R > 1e30) return fail(SPIN_E_INVAL, "R=%g must be positive and finite", R);
   *count = 0;
@@ -397,6 +529,36 @@ spin_status spin_count_in_sphere(spin_handle h, const int32_t* d_centre_idx, int
   CK(cudaMemcpyAsync(&c, d_cnt, sizeof c, cudaMemcpyDeviceToHost, s), "count readback");
   CK(cudaStreamSynchronize(s), "count sync");
   *count = (int64_t)c;
+  return SPIN_OK;
+}
+
+spin_status spin_pair_codes(spin_handle h, const int32_t* d_centre_idx, int64_t M, int32_t W,
+                            double b, double cos_As, spin_mode mode, uint32_t flags,
+                            int32_t* d_codes, spin_stream stream) {
+  if (!h) return fail(SPIN_E_INVAL, "null handle");
+  if (h->N <= 0) return fail(SPIN_E_INVAL, "no valid cloud loaded (the last spin_load_cloud failed)");
+  if (M < 0 || M >= ((int64_t)1 << 31)) return fail(SPIN_E_INVAL, "M=%lld out of range", (long long)M);
+  if (W < 1 || W > 64) return fail(SPIN_E_INVAL, "W=%d outside [1, 64]", W);
+  if (mode != SPIN_NEAREST && mode != SPIN_BILINEAR) return fail(SPIN_E_INVAL, "bad mode %d", (int)mode);
+  if (mode == SPIN_BILINEAR && W < 2) return fail(SPIN_E_INVAL, "BILINEAR needs W >= 2");
+  if (!std::isfinite(b) || b < 1e-30 || b > 1e30) return fail(SPIN_E_INVAL, "b=%g must be finite in [1e-30, 1e30]", b);
+  const bool has_support = !(std::isinf(cos_As) && cos_As < 0);
+  if (has_support && !(cos_As >= -1.0 && cos_As <= 1.0))
+    return fail(SPIN_E_INVAL, "cos_As=%g must be in [-1, 1] or -inf", cos_As);
+  if (flags & ~0x3fu) return fail(SPIN_E_INVAL, "unknown flag bits 0x%x", flags);
+  if (M == 0) return SPIN_OK;
+  if (!d_centre_idx || !d_codes) return fail(SPIN_E_INVAL, "null d_centre_idx or d_codes");
+  const Region rg = region_of(W, b, (int)mode, flags);
+  KParams p{};
+  plan_thresholds(h, W, b, cos_As, has_support, mode, SPIN_BRUTE, flags, rg, p);
+  p.cpos = h->pos;
+  p.cnrm = h->nrm;
+  p.pos = h->pos;
+  p.nrm = h->nrm;
+  p.N = (int32_t)h->N;
+  p.W = W;
+  p.err_flags = h->err;
+  CK(launch_pair_codes(p, (int)mode, d_centre_idx, M, d_codes, (cudaStream_t)stream), "pair codes");
   return SPIN_OK;
 }
 
@@ -496,6 +658,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
                           const spin_chunk_params* cp, spin_mode mode, spin_prune prune,
                           float* d_out, spin_stats* stats, spin_stream stream) {
   if (!h) return fail(SPIN_E_INVAL, "null handle");
+  if (h->N <= 0) return fail(SPIN_E_INVAL, "no valid cloud loaded (the last spin_load_cloud failed)");
   cudaStream_t s = (cudaStream_t)stream;
   // inside a stream capture (CUDA graphs) nothing may synchronise or query events: the
   // deferred error report is skipped and stats are refused
@@ -504,10 +667,17 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   const bool capturing = cap != cudaStreamCaptureStatusNone;
   if (capturing && stats) return fail(SPIN_E_INVAL, "stats synchronise the stream: not inside a stream capture");
   // ---- a deferred SPIN_E_RANGE / overflow from an earlier asynchronous call
+  // (the device word is sticky: every call's readback carries the flags of all calls since
+  // the last report, so a flag whose own readback was never inspected is not lost)
   if (!capturing && h->err_pending && cudaEventQuery(h->ev_err) == cudaSuccess) {
     h->err_pending = false;
-    if (h->h_err[0]) { h->h_err[0] = 0; return fail(SPIN_E_RANGE, "an earlier call saw a centre index outside [0, N)"); }
-    if (h->h_err[1]) { h->h_err[1] = 0; return fail(SPIN_E_OVERFLOW, "an earlier call overflowed a bin accumulator"); }
+    if (h->h_err[0] || h->h_err[1]) {
+      const bool range = h->h_err[0] != 0;
+      h->h_err[0] = h->h_err[1] = 0;
+      CK(cudaMemsetAsync(h->err, 0, 2 * sizeof(int32_t), s), "memset");
+      return range ? fail(SPIN_E_RANGE, "an earlier call saw a centre index outside [0, N)")
+                   : fail(SPIN_E_OVERFLOW, "an earlier call overflowed a bin accumulator");
+    }
   }
   // ---- synchronous argument checks (§8(b) SPIN_E_INVAL)
   if (M < 0) return fail(SPIN_E_INVAL, "M=%lld must be >= 0", (long long)M);
@@ -592,121 +762,8 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   // ---- a2: region constants and certified thresholds
   const uint32_t flags = cpar.flags;
   const Region rg = region_of(W, b, (int)mode, flags);
-  const double X = std::max((double)h->absmax, 1e-30) * (1.0 + 1e-6);
-  const double u = U32;
-  const double amid = std::fabs(rg.mid);
-  // hot loop (fp32): candidates are the pairs inside the sphere about the rounded window
-  // centre c~ = fl(2(p + mid n))/2 that contains the region cylinder (|beta - mid| <= h,
-  // alpha^2 <= Qmax), margin m = B.x - |x|^2 + K with B = 2c~, K = rho^2 - |c~|^2 + 2E
-  // (DESIGN.md 7.1).  |c~ - c'| <= u (X + |mid|) widens the radius.
-  // Two BRUTE filters share the margin: packed fp32 (FFMA2) and the tensor cores (tf32
-  // mma.sync), whose operands B and K are rounded to tf32: |c~ - c'| <= 2^-11 |c'|.
-  // fp32 error: 5u per term magnitude.  Tensor cores (x, y, z split into tf32 hi + lo,
-  // w = -|x|^2 and K rounded to tf32, exact products, fp32 accumulation): 2^-21 |B||x| +
-  // 2^-11 (|x|^2 + |K|) (round to nearest at 11 significant bits) plus an accumulation
-  // allowance of 2^-19 of the summed magnitudes
-  // (and 2^-100 absolute for flushed subnormals).  E bounds the filter in use, so every
-  // region pair keeps m > 0 (DESIGN.md 7.1).  The tensor cores are used unless their
-  // looser bound grows the candidate sphere by more than 6% (clouds far from the origin
-  // relative to the region size).
-  auto sphere = [&](bool mma, double& rho_o, double& E_o) {
-    const double shift = 1.01 * (mma ? std::ldexp(1.0, -11) : u) * (X + amid);
-    rho_o = std::sqrt(rg.h * rg.h + rg.Qmax) + shift;
-    const double Ms = rho_o * rho_o + (2.0 * X + amid) * (2.0 * X + amid) * 1.01;
-    E_o = 6.0 * u * Ms * 1.05;
-    if (mma) {
-      const double Kmax = 1.05 * (rho_o * rho_o + (X + amid) * (X + amid)) + 4.0 * E_o;
-      const double BX = 2.02 * (X + amid) * X;
-      E_o += 1.01 * (std::ldexp(1.0, -21) * BX + std::ldexp(1.0, -11) * (X * X + Kmax) +
-                     std::ldexp(1.0, -19) * (BX + X * X + Kmax)) + std::ldexp(1.0, -100);
-    }
-  };
-  double rho, E_sph, rho_f, E_f;
-  sphere(true, rho, E_sph);
-  sphere(false, rho_f, E_f);
-  const bool use_mma = prune == SPIN_BRUTE && std::getenv("SPIN_NO_MMA") == nullptr &&
-                       rho * rho + 3.0 * E_sph <= 1.06 * (rho_f * rho_f + 3.0 * E_f);
-  if (!use_mma) {
-    rho = rho_f;
-    E_sph = E_f;
-  }
-  const double shift = 1.01 * (use_mma ? std::ldexp(1.0, -11) : u) * (X + amid);
-  const double Es_h = 4.0 * u * 1.01;
-  // CELLS hot loop: the region cylinder in expanded forms (bounds hold inside the region)
-  const double Eb_h = 8.0 * u * (X + amid) * 1.01;
-  const double Et_h = 16.0 * u * (X + amid) * (X + amid) * 1.01;
-  const double Eq_h = Et_h + Eb_h * (2.0 * rg.h + Eb_h) + 2.0 * u * (rg.Qmax + 2.0 * (X + amid) * (X + amid));
   KParams p{};
-  p.b = b;
-  p.cos_As = has_support ? cos_As : -INFINITY;
-  p.A = 0.5 * W;
-  p.mid = rg.mid;
-  p.Qmax = rg.Qmax;
-  p.rho2 = rho * rho;
-  p.E_sph = E_sph;
-  p.mma = use_mma ? 1 : 0;
-  p.Eq_hot = Eq_h;
-  p.h_test = f32_up(rg.h + Eb_h);
-  p.c_test = has_support ? f32_down(cos_As - Es_h) : -INFINITY;
-  p.has_support = has_support ? 1 : 0;
-  // where the support test runs (same images either way): not at all without one; in the
-  // accept path only (SPIN_F_SUPPORT_LAST); on every pair (SPIN_F_SUPPORT_FIRST, and CELLS
-  // by default); BRUTE by default adaptively per warp (2)
-  p.support_in_hot = !has_support ? 0
-                     : (cpar.flags & SPIN_F_SUPPORT_LAST) ? 0
-                     : (cpar.flags & SPIN_F_SUPPORT_FIRST) ? 1
-                     : (prune == SPIN_BRUTE ? 2 : 1);
-  // candidates satisfy |d| <= D.  BRUTE: |x - c~|^2 <= rho^2 + 4E, so
-  // |d| <= |c~ - p| + sqrt(rho^2 + 4E).  CELLS: q <= Qmax + 2Eq, |beta| <= |mid| + h_test + Eb.
-  const double Dh = (amid + shift + std::sqrt(rho * rho + 4.0 * E_sph)) * 1.001;
-  const double Cmax = (X + amid) * (X + amid) * 1.01;
-  const double bmax = amid + (double)p.h_test + Eb_h;
-  const double D2c = (rg.Qmax + 2.0 * Eq_h + 4.0 * u * (rg.Qmax + Cmax) + bmax * bmax) * 1.001;
-  const double D2 = (prune == SPIN_BRUTE ? Dh * Dh : D2c) + 1e-30;
-  const double D = std::sqrt(D2);
-  // accept path, fp32 direct forms, valid while |d| <= D
-  const double Es_a = 5.5 * u * 1.01;
-  const double Eb_a = 4.2 * u * D * 1.002;
-  const double Edd_a = 5.2 * u * D2;
-  const double Eq_a = Edd_a + Eb_a * (2.0 * D + Eb_a) + 1.01 * u * D2;
-  double Eu_a;
-  if (!(flags & SPIN_F_LITERAL_HALF_WIDTH))
-    Eu_a = ((Eb_a + 1.01 * u * D) / b + u * (p.A + D / b)) * 1.01;
-  else  // u = fma(-beta, fl(1/b), fl(W/(2b))): rounding of both constants and the fma
-    Eu_a = (Eb_a + 4.01 * u * (p.A + D)) / b * 1.05;
-  const double Ew_a = (Eq_a + 2.01 * u * D2) / (b * b) * 1.01;
-  p.c_f = has_support ? (float)cos_As : -INFINITY;
-  p.inv_b = (float)(1.0 / b);
-  p.inv_b2 = (float)(1.0 / (b * b));
-  p.Af = (float)p.A;
-  p.Wf = (float)W;
-  p.Au = (flags & SPIN_F_LITERAL_HALF_WIDTH) ? (float)(p.A / b) : (float)p.A;
-  p.floor_f = (flags & SPIN_F_FLOOR_BINS) ? 1.0f : 0.0f;
-  p.Es_a = f32_up(Es_a);
-  p.Eu_a = f32_up(Eu_a);
-  p.Ew_a = f32_up(Ew_a);
-  p.D2g = f32_down(D2);
-  p.literal = (flags & SPIN_F_LITERAL_HALF_WIDTH) ? 1 : 0;
-  p.floor_bins = (flags & SPIN_F_FLOOR_BINS) ? 1 : 0;
-  p.no_fast_cert = (flags & SPIN_F_NO_FAST_CERT) ? 1 : 0;
-  if (const char* dbg = std::getenv("SPIN_DEBUG_SKIP")) p.debug_skip = std::atoi(dbg);
-  // self pair (d = 0): beta = q = 0 exactly, u = W/2 (scaled reading only)
-  p.self_fast = p.literal ? 0 : 1;
-  if (mode == SPIN_NEAREST) {
-    const int k = p.floor_bins ? (int)std::floor(p.A) : (int)std::ceil(p.A);
-    p.self_k = (k >= 0 && k < W) ? k : -1;
-    p.self_kf = (float)p.self_k;
-    p.self_l = 0;
-    p.self_a = 0.f;
-  } else {
-    const double i0 = std::floor(p.A);
-    const bool in = p.A >= 0.0 && p.A < W - 1.0;
-    p.self_k = in ? (int)i0 : -1;
-    p.self_l = 0;
-    p.self_a = (float)(p.A - i0);
-  }
-  if (!(Eu_a < 0.25 && Ew_a < 0.25)) p.no_fast_cert = 1;  // fp32 cannot resolve bins: skip it
-  if (p.no_fast_cert) p.D2g = -1.0f;   // the fp32 stage certifies nothing (decide: dd <= D2g fails)
+  plan_thresholds(h, W, b, cos_As, has_support, mode, prune, flags, rg, p);
 
   // ---- cloud, centres, dealing, outputs
   p.cpos = h->pos;
@@ -777,7 +834,9 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
       // counting-sort buckets stay within 64 M
       int ob = 6;
       while (ob < 8 && ((int64_t)1 << (3 * (ob + 1))) <= 64 * M) ++ob;
+#ifdef SPIN_MEASURE
       if (const char* e = std::getenv("SPIN_ORDER_BITS")) ob = std::min(std::max(std::atoi(e), 1), 8);
+#endif
       int shift = 0, sub = 0;
       const int dmax = std::max(h->dx, std::max(h->dy, h->dz));
       while ((dmax >> shift) > (1 << ob)) ++shift;
@@ -835,11 +894,8 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   if (!capturing) {
     CK(cudaEventRecord(h->ev1, s), "event");
     CK(cudaMemcpyAsync(h->h_err, h->err, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s), "err readback");
-    CK(cudaMemsetAsync(h->err, 0, 2 * sizeof(int32_t), s), "memset");
     CK(cudaEventRecord(h->ev_err, s), "event");
     h->err_pending = true;
-  } else {
-    CK(cudaMemsetAsync(h->err, 0, 2 * sizeof(int32_t), s), "memset");
   }
 
   if (stats) {
@@ -877,8 +933,13 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
       if (stats->h_cta_units) CK(cudaMemcpy(stats->h_cta_units, h->cta_units, nc * 4, cudaMemcpyDeviceToHost), "cta");
     }
     h->err_pending = false;
-    if (h->h_err[0]) { h->h_err[0] = 0; return fail(SPIN_E_RANGE, "a centre index is outside [0, N); its image is zero"); }
-    if (h->h_err[1]) { h->h_err[1] = 0; return fail(SPIN_E_OVERFLOW, "a bin accumulator overflowed"); }
+    if (h->h_err[0] || h->h_err[1]) {
+      const bool range = h->h_err[0] != 0;
+      h->h_err[0] = h->h_err[1] = 0;
+      CK(cudaMemsetAsync(h->err, 0, 2 * sizeof(int32_t), s), "memset");
+      return range ? fail(SPIN_E_RANGE, "a centre index is outside [0, N); its image is zero")
+                   : fail(SPIN_E_OVERFLOW, "a bin accumulator overflowed");
+    }
   }
   return SPIN_OK;
 }

@@ -188,13 +188,15 @@ static __device__ __noinline__ SlowOut slow_decide(const PairD& P, int W, double
       ++n_exact;
       // ceil: k = smallest integer with u <= k  (u <= k <=> sign(beta - T(k)) >= 0)
       // floor: k = largest integer with u >= k  (u >= k <=> sign(beta - T(k)) <= 0)
-      k = (int)rr;
+      // (start clamped to [-1, W] and every step bounded: a k outside [0, W) is rejected
+      // anyway, so a huge eu cannot make the search walk 2^31 rows)
+      k = (int)fmin(fmax(rr, -1.0), (double)W);
       if (!floor_bins) {
-        while (exact_sign_beta_minus_T(P, A, b, k - 1, literal) >= 0) --k;
-        while (exact_sign_beta_minus_T(P, A, b, k, literal) < 0) ++k;
+        while (k >= 0 && exact_sign_beta_minus_T(P, A, b, k - 1, literal) >= 0) --k;
+        while (k < W && exact_sign_beta_minus_T(P, A, b, k, literal) < 0) ++k;
       } else {
-        while (exact_sign_beta_minus_T(P, A, b, k, literal) > 0) --k;
-        while (exact_sign_beta_minus_T(P, A, b, k + 1, literal) <= 0) ++k;
+        while (k >= 0 && exact_sign_beta_minus_T(P, A, b, k, literal) > 0) --k;
+        while (k < W && exact_sign_beta_minus_T(P, A, b, k + 1, literal) <= 0) ++k;
       }
     }
     if (k < 0 || k >= W) return r;

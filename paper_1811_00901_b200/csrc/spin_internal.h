@@ -135,6 +135,9 @@ cudaError_t launch_centre_order(const int32_t* centre_idx, int64_t M, const floa
                                 int dy, int dz, int shift, int bits, int32_t* keys,
                                 int32_t* counts, int32_t* starts, int32_t* cursor,
                                 int32_t* scan_tmp, int32_t* order, cudaStream_t s);
+// diagnostic: the accept path's per-pair decision for every (centre, point) pair
+cudaError_t launch_pair_codes(const KParams& p, int mode, const int32_t* centre_idx, int64_t M,
+                              int32_t* codes, cudaStream_t s);
 cudaError_t launch_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, int32_t* tmp,
                                   cudaStream_t s);
 size_t scan_tmp_elems(int64_t n);

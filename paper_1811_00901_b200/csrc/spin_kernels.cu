@@ -28,8 +28,13 @@ LaunchCfg choose_launch(int W, int mode, int prune) {
   constexpr int LIMIT = 220 * 1024;
   LaunchCfg lc;
   lc.threads = NT_DEFAULT;
-  const char* dg = std::getenv("SPIN_DEBUG_G");   // measurement knobs
+#ifdef SPIN_MEASURE
+  const char* dg = std::getenv("SPIN_DEBUG_G");   // measurement builds only (unvalidated)
   const char* dn = std::getenv("SPIN_DEBUG_NT");
+#else
+  const char* dg = nullptr;
+  const char* dn = nullptr;
+#endif
   if (dg) {
     lc.G = std::atoi(dg);
     if (dn) lc.threads = std::atoi(dn);
@@ -331,6 +336,46 @@ cudaError_t launch_centre_order(const int32_t* centre_idx, int64_t M, const floa
                                  keys, counts);
   if ((e = launch_exclusive_scan(counts, starts, nb, scan_tmp, s)) != cudaSuccess) return e;
   k_centre_scatter<<<g, tb, 0, s>>>(M, keys, starts, cursor, order);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ diagnostic: per-pair decisions
+// The accept path's own decision (decide -> resolve, the device functions the persistent
+// kernel runs on every candidate) for EVERY (centre, point) pair of a few centres, so the
+// tests can compare each pair's bin with the oracle's: NEAREST bins must be identical,
+// BILINEAR region decisions identical and (i0, j0) may differ only at interior bin edges
+// ("flips", counted).  codes[m][j] = -1 (no contribution) or k*W + l / i0*W + j0.
+template <int MODE>
+__global__ void k_pair_codes(const __grid_constant__ KParams p, const int32_t* __restrict__ centre_idx,
+                             int32_t* __restrict__ codes) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= p.N) return;
+  const int64_t m = blockIdx.y;
+  const int c = centre_idx[m];
+  int32_t code = -1;
+  if (c >= 0 && c < p.N) {
+    const float4 P4 = p.cpos[c];
+    float4 N4 = p.cnrm[c];
+    N4.w = (float)((double)N4.x * N4.x + (double)N4.y * N4.y + (double)N4.z * N4.z - 1.0);
+    const float4 A = p.pos[j], B = p.nrm[j];
+    const float4 X4 = make_float4(A.x, A.y, A.z, 0.f), NX4 = make_float4(B.x, B.y, B.z, 0.f);
+    Ctr ct{0, 0, 0, 0, 0};
+    Dec d = decide<MODE>(p, P4, N4, X4, NX4);
+    if (d.status == 2) resolve<MODE>(p, d, P4, N4, X4, NX4, ct);
+    if (d.status) code = d.bin;
+  }
+  codes[m * (int64_t)p.N + j] = code;
+}
+
+cudaError_t launch_pair_codes(const KParams& p, int mode, const int32_t* centre_idx, int64_t M,
+                              int32_t* codes, cudaStream_t s) {
+  for (int64_t m0 = 0; m0 < M; m0 += 65535) {
+    const dim3 grid((unsigned)((p.N + 255) / 256), (unsigned)std::min<int64_t>(65535, M - m0));
+    if (mode == 0)
+      k_pair_codes<0><<<grid, 256, 0, s>>>(p, centre_idx + m0, codes + m0 * (int64_t)p.N);
+    else
+      k_pair_codes<1><<<grid, 256, 0, s>>>(p, centre_idx + m0, codes + m0 * (int64_t)p.N);
+  }
   return cudaGetLastError();
 }
 

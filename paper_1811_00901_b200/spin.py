@@ -119,13 +119,16 @@ class Dealer:
 
 _lib.spin_count_in_sphere.argtypes = [_vp, _vp, C.c_int64, C.c_double, C.POINTER(C.c_int64), _vp]
 _lib.spin_count_in_sphere.restype = C.c_int
+_lib.spin_pair_codes.argtypes = [_vp, _vp, C.c_int64, C.c_int32, C.c_double, C.c_double, C.c_int,
+                                 C.c_uint32, _vp, _vp]
+_lib.spin_pair_codes.restype = C.c_int
 
 EXPORTS = ["spin_create", "spin_load_cloud", "spin_generate", "spin_generate_host",
            "spin_chunk_sequence", "spin_region_radius", "spin_cos_from_degrees", "spin_default_P",
            "spin_destroy", "spin_last_error", "spin_abi_version",
            "spin_read_xyzn", "spin_read_off", "spin_vertex_normals",
            "spin_dealer_alloc", "spin_dealer_ipc_handle", "spin_dealer_ipc_open",
-           "spin_dealer_reset", "spin_dealer_free", "spin_count_in_sphere"]
+           "spin_dealer_reset", "spin_dealer_free", "spin_count_in_sphere", "spin_pair_codes"]
 
 
 def read_xyzn(path):
@@ -183,10 +186,39 @@ def _enum(v, table):
 def _ptr(t):
     """Device or host pointer of a torch tensor or numpy array (must be contiguous)."""
     if isinstance(t, np.ndarray):
-        assert t.flags["C_CONTIGUOUS"]
+        if not t.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
         return t.ctypes.data
-    assert t.is_contiguous()
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
     return t.data_ptr()
+
+
+def _dtype_name(t):
+    return str(t.dtype).replace("torch.", "")
+
+
+def _check_array(t, what, dtype, shape, device=None):
+    """Refuse (ValueError) anything but a contiguous `dtype` array of `shape` — no silent
+    casts: a float64 cloud or a short output buffer would be reinterpreted or overrun."""
+    if _dtype_name(t) != dtype:
+        raise ValueError(f"{what} must be {dtype}, got {_dtype_name(t)}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{what} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if device is not None:
+        on_dev = (not isinstance(t, np.ndarray)) and t.is_cuda
+        if device == "host" and on_dev:
+            raise ValueError(f"{what} must be host memory")
+        if device != "host" and (not on_dev or t.device != device):
+            raise ValueError(f"{what} must be on {device}")
+    _ptr(t)
+
+
+def _check_cloud(points, normals):
+    n = int(points.shape[0]) if len(points.shape) == 2 else -1
+    _check_array(points, "points", "float32", (n, 3))
+    _check_array(normals, "normals", "float32", (n, 3))
+    return n
 
 
 def _stream(stream):
@@ -244,8 +276,7 @@ class SpinEngine:
     """A libspin handle: the oriented point cloud resident in HBM (spin_create)."""
 
     def __init__(self, points, normals, stream=None):
-        n = int(points.shape[0])
-        assert tuple(points.shape) == (n, 3) and tuple(normals.shape) == (n, 3)
+        n = _check_cloud(points, normals)
         h = _vp()
         _check(_lib.spin_create(_ptr(points), _ptr(normals), n, _stream(stream), C.byref(h)))
         self._h = h
@@ -263,7 +294,7 @@ class SpinEngine:
             pass
 
     def load_cloud(self, points, normals, stream=None):
-        n = int(points.shape[0])
+        n = _check_cloud(points, normals)
         _check(_lib.spin_load_cloud(self._h, _ptr(points), _ptr(normals), n, _stream(stream)))
         self.N = n
 
@@ -286,9 +317,12 @@ class SpinEngine:
         dealt across devices; only this device's chunks are written to `out`."""
         import torch
         M = int(centre_idx.shape[0])
-        assert centre_idx.dtype == torch.int32 and centre_idx.is_cuda
+        if isinstance(centre_idx, np.ndarray) or not centre_idx.is_cuda:
+            raise ValueError("centre_idx must be a CUDA tensor (generate_host takes host arrays)")
+        _check_array(centre_idx, "centre_idx", "int32", (M,))
         if out is None:
             out = torch.empty((M, W, W), dtype=torch.float32, device=centre_idx.device)
+        _check_array(out, "out", "float32", (M, W, W), centre_idx.device)
         cp = self._params(P, unit, gss_min_chunk, fac_divisor, flags, slow_ctas, slowdown, slow_first,
                           grid, cta_offset, shared_counter)
         st = Stats()
@@ -318,6 +352,23 @@ class SpinEngine:
                                          C.byref(n), _stream(stream)))
         return n.value
 
+    def pair_codes(self, centre_idx, W, b, cos_As, mode="nearest", flags=0, out=None, stream=None):
+        """spin_pair_codes (diagnostic): int32 [M, N] device codes of every (centre, point)
+        pair — -1 or the pair's bin (NEAREST k*W+l, BILINEAR i0*W+j0) as the accept path
+        decides it."""
+        import torch
+        M = int(centre_idx.shape[0])
+        if isinstance(centre_idx, np.ndarray) or not centre_idx.is_cuda:
+            raise ValueError("centre_idx must be a CUDA tensor")
+        _check_array(centre_idx, "centre_idx", "int32", (M,))
+        if out is None:
+            out = torch.empty((M, self.N), dtype=torch.int32, device=centre_idx.device)
+        _check_array(out, "out", "int32", (M, self.N), centre_idx.device)
+        _check(_lib.spin_pair_codes(self._h, _ptr(centre_idx) if M else None, M, int(W), float(b),
+                                    float(cos_As), _enum(mode, MODES), int(flags),
+                                    _ptr(out) if M else None, _stream(stream)))
+        return out
+
     def generate_host(self, centre_idx: np.ndarray, W, b, cos_As, schedule="STATIC",
                       mode="nearest", prune="brute", P=0, unit=0, gss_min_chunk=0,
                       fac_divisor=0, flags=0, out: np.ndarray | None = None, stats=False,
@@ -327,6 +378,7 @@ class SpinEngine:
         M = int(centre_idx.shape[0])
         if out is None:
             out = np.empty((M, W, W), np.float32)
+        _check_array(out, "out", "float32", (M, W, W), "host")
         cp = self._params(P, unit, gss_min_chunk, fac_divisor, flags)
         st = Stats()
         _check(_lib.spin_generate_host(self._h, _ptr(centre_idx) if M else None, M, int(W),

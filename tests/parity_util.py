@@ -28,3 +28,31 @@ def assert_bilinear_close(gpu, ora, contributors, what=""):
     ratio = err / (PER_BIN * cnt)
     assert ratio.max() <= 1.0, f"{what}: per-bin error {ratio.max():.3f}x the bound"
     return float(rel.max()) if rel.size else 0.0
+
+
+def flip_counts(gpu_codes, ora_codes):
+    """Per-pair decisions (spin_pair_codes vs the oracle's pair codes, -1 = no contribution,
+    else the pair's bin / BILINEAR base corner i0*W + j0): returns (region mismatches =
+    pairs only one side lets contribute, flips = pairs both let contribute at different
+    (i0, j0), pairs both let contribute).  Region decisions are certified exact on both
+    sides, so mismatches must be 0; NEAREST bins are exact, so NEAREST flips must be 0;
+    BILINEAR flips are pairs within fp32 rounding of an interior bin edge, where the splat
+    is continuous (north star: "bin-edge rounding flips counted and reported")."""
+    g = np.asarray(gpu_codes)
+    o = np.asarray(ora_codes)
+    both = (g >= 0) & (o >= 0)
+    return (int(np.count_nonzero((g >= 0) != (o >= 0))), int(np.count_nonzero(both & (g != o))),
+            int(np.count_nonzero(both)))
+
+
+def log_parity(record: dict):
+    """Print one parity record and append it (JSON) to $SPIN_PARITY_LOG when set (the
+    committed campaign logs under profiles/ come from this)."""
+    import json
+    import os
+    line = json.dumps(record)
+    print("PARITY", line)
+    path = os.environ.get("SPIN_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(line + "\n")

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), f"libspin.so does not export {n}"
     assert set(names) == set(spin.EXPORTS)
-    assert spin.abi_version() == 5
+    assert spin.abi_version() == 6
 
 
 def test_binding_has_no_cpu_fallback():
@@ -123,3 +123,23 @@ def test_header_documents_every_entry_point():
         # each declaration is preceded by a comment block naming it or its family
         assert n in txt
     assert "PAPER.md:146-182" in txt and "PAPER.md:286-319" in txt
+
+
+def test_binding_refuses_bad_clouds_before_any_cuda_call():
+    """spin.py marshals only contiguous float32 [N, 3] clouds; anything else is a
+    ValueError raised before the C ABI is called (no silent reinterpretation)."""
+    from paper_1811_00901_b200 import spin
+    P = np.zeros((10, 3), np.float32)
+    for bad in (P.astype(np.float64), P[:, :2], np.asfortranarray(np.zeros((10, 3), np.float32))[::2]):
+        with pytest.raises(ValueError):
+            spin.SpinEngine(bad, P)
+    with pytest.raises(ValueError):
+        spin.SpinEngine(P, np.zeros((9, 3), np.float32))
+
+
+def test_oracle_sources_are_independent_of_the_product():
+    """The C++ oracle includes nothing from the product tree and the product never names it."""
+    src = open(os.path.join(ROOT, "oracle", "spin_oracle.cpp")).read()
+    assert "spin.h" not in src and "spin_internal" not in src and "csrc" not in src
+    for inc in re.findall(r'#include\s+[<"]([^>"]+)[>"]', src):
+        assert "/" not in inc and not inc.startswith("spin"), inc

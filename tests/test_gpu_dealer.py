@@ -2,8 +2,9 @@
 processes through a counter mapped with CUDA IPC.  Run on one GPU (both processes share
 it; neither waits on the other: each CTA only grabs chunks until the table is
 exhausted), it exercises the same dealing and partial-output contract a multi-GPU run
-uses.  The partial images of the two processes must sum to the single-process images
-(NEAREST counts: exact), every chunk dealt exactly once."""
+uses (the paper's master dealing to workers on many nodes).  The partial
+images of the two processes must sum to the ORACLE's images (NEAREST counts: exact), every
+chunk dealt exactly once."""
 import os
 import sys
 
@@ -51,10 +52,11 @@ def test_shared_dealer_two_processes():
     sys.path.insert(0, ROOT)
     from paper_1811_00901_b200 import spin
     from synth import clouds
+    from oracle import spin_oracle_cpp as OC
     P, Nn = clouds.bumpy_sphere(20000, 41)
     eng = spin.SpinEngine(torch.from_numpy(P).cuda(), torch.from_numpy(Nn).cuda())
-    ref = eng.generate(torch.arange(20000, dtype=torch.int32, device="cuda"), 16, 0.02, 0.5,
-                       schedule="SS", mode="nearest").cpu().numpy()
+    # the expected images come from the oracle (Alg. 1), not from the GPU
+    ref = OC.generate(P, Nn, np.arange(20000), 16, 0.02, 0.5, OC.NEAREST).astype(np.float32)
     dealer = spin.Dealer()
     ctx = mp.get_context("spawn")
     barrier, q = ctx.Barrier(3), ctx.Queue()
@@ -81,3 +83,32 @@ def test_shared_dealer_two_processes():
         assert not np.any((a.reshape(20000, -1).sum(1) > 0) & (b.reshape(20000, -1).sum(1) > 0))
     dealer.close()
     eng.close()
+
+
+def test_bench_torchrun_shared_dealer_two_ranks():
+    """bench.py under torchrun with two ranks and the shared dealer (the
+    paper's master dealing one schedule to every worker): both ranks on
+    cuda:0 (this pool has one GPU per call; the ranks never wait on each other), gloo for
+    the barrier and the max-over-ranks timing.  Rank 0 prints one parseable JSON line with
+    the whole job's pairs."""
+    import json
+    import socket
+    import subprocess
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
+           "--config", "1", "--dealer", "shared", "--steps", "3", "--warmup", "3",
+           "--dist-backend", "gloo", "--same-device", "--no-cpu-baseline", "--no-e2e", "--no-dls"]
+    r = subprocess.run(cmd, cwd=ROOT, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert d["pairs"]["visited"] == 2000 * 2000          # one schedule of C1 over both ranks
+    assert "shared counter" in d["config"]["parallelism"]
+    assert d["value"] > 0 and d["ms_per_step"] > 0

@@ -12,6 +12,7 @@ import numpy as np
 import pytest
 
 from oracle import spin_oracle as O
+from oracle import spin_oracle_cpp as OC
 from synth import clouds
 from parity_util import assert_bilinear_close, assert_nearest_exact
 
@@ -407,56 +408,7 @@ def test_host_path_and_reload(spin, torch):
         eng.close()
 
 
-# ------------------------------------------------------------------ full-size configs, sampled
-
-def _full(spin, torch, cfg_id, mode, prune, n_check, W=None, sched="STATIC"):
-    cfg = clouds.CONFIGS[cfg_id]
-    P, Nn = clouds.make_cloud(cfg_id)
-    cen = clouds.make_centres(cfg_id, cfg["N"])
-    W = W or cfg["W"]
-    gpu, st = run_gpu(spin, torch, P, Nn, cen, W, cfg["b"], cfg["cos_As"], mode, prune=prune,
-                      stats=True, schedule=sched)
-    pick = clouds.subsample(len(cen), n_check, 200 + cfg_id)
-    ora, so = oracle(P, Nn, cen[pick], W, cfg["b"], cfg["cos_As"], mode, cells=(prune == "cells"))
-    check(gpu[pick], ora, so, mode, f"C{cfg_id} {mode} {prune} W={W}")
-    if mode == "nearest":
-        assert gpu.sum(dtype=np.float64) == st["pairs_accepted"]
-    return gpu, st
-
-
-@pytest.mark.parametrize("mode", ["nearest", "bilinear"])
-def test_config2_full_sampled(spin, torch, mode):
-    """C2 in full in bench.py's launch configuration (SS, unit G, default P and flags)."""
-    _full(spin, torch, 2, mode, "brute", 40, sched="SS")
-
-
-def test_config3_full_sampled(spin, torch):
-    for mode in ("bilinear", "nearest"):
-        _full(spin, torch, 3, mode, "cells", 30, sched="SS")
-
-
-def test_config4_full_sampled(spin, torch):
-    _full(spin, torch, 4, "bilinear", "brute", 12, sched="SS")
-
-
-def test_config6_paper_shape_sampled(spin, torch):
-    """NEXT-3, the paper's workload shape (826K-point surface, W = 5, b = 0.1, no support
-    test, 10% of the points as centres), in full on the GPU, sampled against the oracle;
-    plus the literal-formula reading (#2) on the same subsample."""
-    gpu, st = _full(spin, torch, 6, "nearest", "brute", 16, sched="SS")
-    cfg = clouds.CONFIGS[6]
-    P, Nn = clouds.make_cloud(6)
-    pick = clouds.subsample(cfg["M"], 8, 206)
-    cen = clouds.make_centres(6, cfg["N"])[pick]
-    lit = run_gpu(spin, torch, P, Nn, cen, cfg["W"], cfg["b"], cfg["cos_As"], "nearest",
-                  flags=spin.F_LITERAL_HALF_WIDTH)
-    ora, so = oracle(P, Nn, cen, cfg["W"], cfg["b"], cfg["cos_As"], "nearest", flags=1)
-    check(lit, ora, so, "nearest", "P6 literal")
-
-
-@pytest.mark.parametrize("W", [8, 24])
-def test_config5_full_sampled(spin, torch, W):
-    _full(spin, torch, 5, "nearest", "cells", 20, W=W, sched="SS")
+# (full-size configs at the BASELINE sample sizes: tests/test_gpu_scale.py)
 
 
 def test_bilinear_fixed_point_carries(spin, torch):
@@ -545,7 +497,8 @@ def test_support_last_same_images(spin, torch, prune):
 
 def test_heterogeneous_workers_same_images_and_trend(spin, torch):
     """Heterogeneity emulation (the paper's Type1/Type2 runs):
-    slow CTAs change timing only, never images; with a quarter of the CTAs 4x slower, a
+    slow CTAs change timing only, never images (every slowed run equals the ORACLE's images
+    of all 30,000 centres); with a quarter of the CTAs 4x slower, a
     dynamic schedule beats STATIC (ideal ratio 4 * (111 + 37/4) / 148 = 3.25, SPEC
     acceptance #5 asks >= 1.5), and the slow CTAs process fewer units under SS."""
     P, Nn = clouds.bumpy_sphere(30000, 31)
@@ -553,7 +506,8 @@ def test_heterogeneous_workers_same_images_and_trend(spin, torch):
     eng = spin.SpinEngine(_dev(torch, P), _dev(torch, Nn))
     try:
         d_cen = _dev(torch, cen)
-        ref = eng.generate(d_cen, 16, 0.02, 0.5, schedule="STATIC").clone()
+        ora = OC.generate(P, Nn, cen, 16, 0.02, 0.5, OC.NEAREST)
+        ref = torch.from_numpy(ora.astype(np.float32)).cuda()
         times = {}
         for sched in ("STATIC", "SS", "GSS", "FAC", "WF", "AWF"):
             for slow_first in (False, True):
@@ -656,10 +610,35 @@ def _fuzz_cloud(rng, kind, n):
     return (P * scale + off).astype(np.float32), np.asarray(Nn, np.float32), scale
 
 
+def _split_launches(spin, torch, P, Nn, cen, W, b, c, mode, kw):
+    """The shared-dealer contract in one process: two launches of ONE schedule (global P,
+    grid = P/2 each, cta_offset 0 / P/2, one counter); each writes only the images of the
+    chunks its CTAs took, so the two zero-initialised outputs sum to the full result."""
+    Pg = max(2, kw["P"] or 2 * 148)
+    half = Pg // 2
+    eng = spin.SpinEngine(_dev(torch, P), _dev(torch, Nn))
+    dealer = spin.Dealer()
+    try:
+        d_cen = _dev(torch, np.asarray(cen, np.int32))
+        outs = []
+        for off, g in ((0, half), (half, Pg - half)):
+            out = torch.zeros((len(cen), W, W), dtype=torch.float32, device="cuda")
+            k2 = dict(kw, P=Pg, grid=g, cta_offset=off, shared_counter=dealer.ptr)
+            k2.pop("slow_first", None)
+            eng.generate(d_cen, W, b, c, mode=mode, out=out, **k2)
+            outs.append(out)
+        torch.cuda.synchronize()
+        return (outs[0] + outs[1]).cpu().numpy()
+    finally:
+        dealer.close()
+        eng.close()
+
+
 def test_fuzz_against_oracle(spin, torch):
     """Seeded random configurations (widths, bin sizes, support angles, modes, flags,
-    pruning, every schedule incl. WF/AWF, P, unit) on small structured clouds: NEAREST
-    bit-exact and BILINEAR within tolerance against the oracle, CELLS = BRUTE."""
+    pruning, every schedule incl. WF/AWF, P, unit, slow-worker emulation, schedules split
+    over two launches sharing one dealer) on small structured clouds: NEAREST bit-exact and
+    BILINEAR within tolerance against the oracle, CELLS = BRUTE."""
     # (SPIN_FUZZ_CASES / SPIN_FUZZ_SEED widen the campaign for one-off runs)
     rng = np.random.default_rng(int(os.environ.get("SPIN_FUZZ_SEED", "20261020")))
     kinds = ["bumpy", "clustered", "dyadic", "planar", "collinear"]
@@ -679,8 +658,18 @@ def test_fuzz_against_oracle(spin, torch):
         knobs = int(rng.choice([0, 0, 0x4, 0x8, 0x10, 0x20]))
         kw = dict(schedule=scheds[case % len(scheds)], P=int(rng.choice([0, 1, 5, 148])),
                   unit=int(rng.choice([0, 1, 3])), flags=flags | knobs)
-        what = f"case {case} {kind} n={n} M={M} W={W} b={b:g} c={c:g} {mode} {kw}"
-        brute = run_gpu(spin, torch, P, Nn, cen, W, b, c, mode, **kw)
+        # heterogeneous-worker emulation (NEXT-1: timing only, never images)
+        if rng.random() < 0.3:
+            kw.update(slow_ctas=int(rng.integers(1, 40)), slowdown=float(rng.choice([2.0, 4.0])),
+                      slow_first=bool(rng.random() < 0.5))
+        split = kw["schedule"] not in ("WF", "AWF") and rng.random() < 0.25
+        what = f"case {case} {kind} n={n} M={M} W={W} b={b:g} c={c:g} {mode} {kw} split={split}"
+        if split:
+            # one schedule dealt to two launches (the shared-dealer contract of NEXT-2):
+            # global P, each launch its grid and cta_offset, one shared counter
+            brute = _split_launches(spin, torch, P, Nn, cen, W, b, c, mode, kw)
+        else:
+            brute = run_gpu(spin, torch, P, Nn, cen, W, b, c, mode, **kw)
         ora, st = oracle(P, Nn, cen, W, b, c, mode, flags=flags)
         check(brute, ora, st, mode, what + " brute")
         cells = run_gpu(spin, torch, P, Nn, cen, W, b, c, mode, prune="cells", **kw)
@@ -746,5 +735,72 @@ def test_cuda_graph_capture(spin, torch):
                 with torch.cuda.graph(g2, stream=s):
                     eng.generate(cen, 16, 0.02, 0.5, schedule="SS", stats=True)
         torch.cuda.synchronize()
+    finally:
+        eng.close()
+
+
+def test_failed_load_leaves_no_cloud(spin, torch):
+    """A spin_load_cloud that fails validation on a live handle leaves NO cloud (never the
+    old grid with new centres, stale bounds or NaN points): generate refuses with
+    SPIN_E_INVAL until a good load, which then gives the oracle's images again."""
+    P, Nn = clouds.bumpy_sphere(3000, 61)
+    cen = _dev(torch, np.arange(0, 3000, 31, dtype=np.int32))
+    eng = spin.SpinEngine(_dev(torch, P), _dev(torch, Nn))
+    try:
+        eng.generate(cen, 16, 0.02, 0.5, prune="cells")
+        bad = P.copy()
+        bad[100, 0] = np.nan
+        with pytest.raises(spin.SpinError) as ei:
+            eng.load_cloud(_dev(torch, bad), _dev(torch, Nn))
+        assert ei.value.status == 3
+        for prune in ("brute", "cells"):
+            with pytest.raises(spin.SpinError) as ei:
+                eng.generate(cen, 16, 0.02, 0.5, prune=prune)
+            assert ei.value.status == 1 and "no valid cloud" in str(ei.value)
+        eng.load_cloud(_dev(torch, P), _dev(torch, Nn))
+        got = eng.generate(cen, 16, 0.02, 0.5, prune="cells").cpu().numpy()
+        ora, _ = oracle(P, Nn, np.arange(0, 3000, 31), 16, 0.02, 0.5, "nearest")
+        assert_nearest_exact(got, ora, "after a failed load")
+    finally:
+        eng.close()
+
+
+def test_deferred_range_error_not_lost(spin, torch):
+    """Back-to-back asynchronous calls: the first has an out-of-range centre index; the
+    error must be reported by a later call (spin.h: "returned by the next call"), even
+    though the second call's own readback is queued before anyone looks."""
+    P, Nn = clouds.bumpy_sphere(2000, 62)
+    eng = spin.SpinEngine(_dev(torch, P), _dev(torch, Nn))
+    try:
+        bad = _dev(torch, np.array([3, 5000, 4], np.int32))
+        good = _dev(torch, np.array([1, 2], np.int32))
+        eng.generate(bad, 8, 0.05, 0.5)          # asynchronous: no error yet
+        eng.generate(good, 8, 0.05, 0.5)         # queued before the first readback is checked
+        torch.cuda.synchronize()
+        with pytest.raises(spin.SpinError) as ei:
+            eng.generate(good, 8, 0.05, 0.5)
+        assert ei.value.status == 2
+        eng.generate(good, 8, 0.05, 0.5, stats=True)   # reported once, then clean
+    finally:
+        eng.close()
+
+
+def test_python_binding_refuses_bad_buffers(spin, torch):
+    """spin.py validates dtype / shape / device of every buffer it passes (no silent
+    reinterpretation of a float64 cloud, no overrun of a short output)."""
+    P, Nn = clouds.bumpy_sphere(500, 63)
+    with pytest.raises(ValueError):
+        spin.SpinEngine(_dev(torch, P.astype(np.float64)), _dev(torch, Nn))
+    eng = spin.SpinEngine(_dev(torch, P), _dev(torch, Nn))
+    try:
+        cen = _dev(torch, np.arange(10, dtype=np.int32))
+        for out in (torch.empty((9, 8, 8), device="cuda"), torch.empty((10, 8, 8), dtype=torch.float64, device="cuda"),
+                    torch.empty((10, 8, 8)), torch.empty((10, 8, 16), device="cuda")[:, :, :8]):
+            with pytest.raises(ValueError):
+                eng.generate(cen, 8, 0.05, 0.5, out=out)
+        with pytest.raises(ValueError):
+            eng.generate(cen.to(torch.int64), 8, 0.05, 0.5)
+        with pytest.raises(ValueError):
+            eng.generate_host(np.arange(10), 8, 0.05, 0.5, out=np.empty((10, 8, 7), np.float32))
     finally:
         eng.close()

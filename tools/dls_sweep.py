@@ -51,6 +51,7 @@ def main(argv=None):
     import torch
     from paper_1811_00901_b200 import spin
     from synth import clouds
+    from bench import ClockSampler          # clocks during every line's repetitions
 
     cfg = dict(clouds.CONFIGS[args.config])
     W = args.W or cfg["W"]
@@ -80,6 +81,8 @@ def main(argv=None):
                 eng.generate(d_cen, W, cfg["b"], cfg["cos_As"], **kw)   # warm-up
                 times, busy_max_over_mean, busy_cov, finish_cov = [], [], [], []
                 st = None
+                clock = ClockSampler(torch.cuda.current_device())
+                clock.start()
                 for _ in range(args.reps):
                     _, st = eng.generate(d_cen, W, cfg["b"], cfg["cos_As"], stats=True,
                                          cta_capacity=4096, **kw)
@@ -93,6 +96,7 @@ def main(argv=None):
                     busy_cov.append(busy.std() / busy.mean())
                     finish_cov.append(fin.std() / fin.mean())
                 torch.cuda.synchronize()
+                clocks = clock.stop()
                 if ref is None:
                     ref = out.clone()
                 elif mode == "nearest" or True:
@@ -113,7 +117,7 @@ def main(argv=None):
                                   "cta_finish_cov": float(np.median(finish_cov)),
                                   "pairs_visited": st["pairs_visited"],
                                   "pairs_accepted": st["pairs_accepted"],
-                                  "sorted": not args.no_sort}), flush=True)
+                                  "sorted": not args.no_sort, "clocks": clocks}), flush=True)
     summary = []
     for (pol, Pn, unit), q in results.items():
         s = results.get(("STATIC", Pn, unit))
