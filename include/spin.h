@@ -126,7 +126,7 @@ typedef struct {
   int64_t fp64_fallbacks;   /* decisions the fp32 stage could not certify                  */
   int64_t exact_fallbacks;  /* decisions the fp64 stage could not certify (exact stage)    */
   int32_t P;                /* CTAs launched on this device (the grid)                      */
-  int32_t G;                /* images per CTA group                                        */
+  int32_t G;                /* images per group (a two-CTA cluster shares one group)       */
   int32_t n_units;          /* scheduling units                                            */
   int32_t n_chunks;         /* chunks in the schedule                                      */
   uint64_t* h_cta_start_ns; /* caller array [P] or NULL: %globaltimer at CTA start         */
@@ -138,6 +138,10 @@ typedef struct {
   int32_t filter_mma;       /* BRUTE: 1 if the sphere filter ran on the tensor cores (tf32
                                mma.sync), 0 if on packed fp32 (far-from-origin clouds,
                                SPIN_NO_MMA, or CELLS)                                         */
+  int32_t cta_per_worker;   /* 1, or 2 when a worker of the schedule is a two-CTA cluster
+                               (BRUTE at large W: the pair shares one group of G images, each
+                               CTA holding G/2 in shared memory, DSMEM adds); workers =
+                               P / cta_per_worker; units are counted on the first CTA      */
 } spin_stats;
 
 /*

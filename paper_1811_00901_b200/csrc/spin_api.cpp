@@ -592,8 +592,8 @@ int32_t spin_default_P(int32_t W, spin_mode mode, spin_prune prune) {
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const LaunchCfg lc = choose_launch(W, (int)mode, (int)prune);
-  return occupancy_blocks(lc, W, (int)mode, (int)prune) * sms;
+  const LaunchCfg lc = choose_launch(W, (int)mode, (int)prune, prune == SPIN_BRUTE && mode == SPIN_NEAREST);
+  return resident_workers(lc, W, (int)mode, (int)prune, sms);
 }
 
 spin_status spin_create(const float* points, const float* normals, int64_t N, spin_stream stream,
@@ -707,23 +707,32 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
     stats->pairs_visited = stats->pairs_candidate = stats->pairs_accepted = 0;
     stats->fp64_fallbacks = stats->exact_fallbacks = 0;
     stats->P = stats->G = stats->n_units = stats->n_chunks = 0;
+    stats->cta_per_worker = 1;
   }
   if (M == 0) return SPIN_OK;
 
   // ---- launch shape, P, units, chunk table (a3)
-  const LaunchCfg lc = choose_launch(W, (int)mode, (int)prune);
-  const int occ = occupancy_blocks(lc, W, (int)mode, (int)prune);
-  if (occ <= 0) return fail(SPIN_E_CUDA, "kernel does not fit on the device (smem %zu)", lc.smem);
-  const int P = cpar.P > 0 ? cpar.P : occ * h->sms;     // workers of the schedule
+  const bool wf = sched == SPIN_WF || sched == SPIN_AWF;   // dealt on the device by CAS
+  // a worker is one CTA, or (BRUTE, table dealer, one device, no slow-worker emulation) a
+  // two-CTA cluster sharing a group of centres
+  // (NEAREST only: its partner adds are fire-and-forget DSMEM reductions, C4 NEAREST 376 ->
+  // 343 ms; BILINEAR's fixed-point carries need the old value back, and four returning DSMEM
+  // atomics per splat made C4 BILINEAR slower, 405 -> 529 ms)
+  const bool allow_cluster = prune == SPIN_BRUTE && mode == SPIN_NEAREST && !wf && !cpar.d_counter &&
+                             cpar.grid == 0 && cpar.cta_offset == 0 &&
+                             !(cpar.slowdown > 1.0f && cpar.slow_ctas > 0);
+  const LaunchCfg lc = choose_launch(W, (int)mode, (int)prune, allow_cluster);
+  const int workers = resident_workers(lc, W, (int)mode, (int)prune, h->sms);
+  if (workers <= 0) return fail(SPIN_E_CUDA, "kernel does not fit on the device (smem %zu)", lc.smem);
+  const int P = cpar.P > 0 ? cpar.P : workers;          // workers of the schedule
   if (P > 1 << 20) return fail(SPIN_E_INVAL, "P=%d too large", P);
-  const int grid = cpar.grid > 0 ? cpar.grid : P;       // CTAs on this device
-  if ((int64_t)cpar.cta_offset + grid > P)
+  const int grid = cpar.grid > 0 ? cpar.grid : P * lc.cl;   // CTAs on this device
+  if ((int64_t)cpar.cta_offset + grid / lc.cl > P)
     return fail(SPIN_E_INVAL, "cta_offset %d + grid %d exceeds P %d", cpar.cta_offset, grid, P);
   const int unit = cpar.unit > 0 ? cpar.unit : lc.G;
   const int64_t n_units = (M + unit - 1) / unit;
   const int gmin = cpar.gss_min_chunk ? cpar.gss_min_chunk : 1;
   const int fdiv = cpar.fac_divisor ? cpar.fac_divisor : 2;
-  const bool wf = sched == SPIN_WF || sched == SPIN_AWF;   // dealt on the device by CAS
   if (wf && (n_units >= (1 << 24) || P >= (1 << 16) || cpar.d_counter))
     return fail(SPIN_E_INVAL, "WF/AWF need n_units < 2^24 (have %lld), P < 2^16 (have %d) and no shared dealer",
                 (long long)n_units, P);
@@ -791,7 +800,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   p.slow_ctas = cpar.slowdown > 1.0f ? std::min(cpar.slow_ctas, grid) : 0;
   p.slowdown = cpar.slowdown > 1.0f ? cpar.slowdown : 1.0f;
   // (the wait needs every slow CTA resident: only for a persistent launch)
-  p.slow_first = (cpar.slow_first && !p.is_static && grid <= occ * h->sms && !cpar.d_counter) ? 1 : 0;
+  p.slow_first = (cpar.slow_first && !p.is_static && grid / lc.cl <= workers && !cpar.d_counter) ? 1 : 0;
   p.counter = cpar.d_counter ? cpar.d_counter : h->counter;
   p.stats = h->stats;
   p.cta_t0 = h->cta_t0;
@@ -918,6 +927,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
     stats->tiles_support_hot = (int64_t)sv[ST_SUPHOT];
     stats->filter_mma = p.mma;
     stats->P = grid;
+    stats->cta_per_worker = lc.cl;
     stats->G = lc.G;
     stats->n_units = (int32_t)n_units;
     stats->n_chunks = n_chunks;

@@ -95,20 +95,21 @@ enum StatSlot {
 
 // Launch configuration chosen by the planner.
 struct LaunchCfg {
-  int G;           // images per group (4 .. 64)
+  int G;           // images per group (4 .. 64; 48 over a two-CTA cluster)
   int threads;     // threads per CTA (768, or 512 for G = 32 at W > 24)
+  int cl;          // CTAs per cluster: 1, or 2 (BRUTE: one worker = a CTA pair, DSMEM images)
   size_t smem;     // dynamic shared memory bytes
 };
 
 // ---- launchers implemented in spin_kernels.cu
-LaunchCfg choose_launch(int W, int mode, int prune);
+LaunchCfg choose_launch(int W, int mode, int prune, bool allow_cluster);
 int tile_points();   // cloud padding: a multiple of every CTA tile (threads x KP points)
 // padding sentinel |x|^2 (finite: the tensor-core filter splits it into tf32 hi/lo parts)
 constexpr float SENTINEL_R2 = 0x1p100f;
 // largest accepted |coordinate| (SPIN_E_INPUT above): |x|^2 and the filter products stay finite
 constexpr float COORD_MAX = 0x1p40f;
 constexpr int KP_POINTS = 4;   // points per thread (register blocking; SPIN_KP)
-int occupancy_blocks(const LaunchCfg& lc, int W, int mode, int prune);
+int resident_workers(const LaunchCfg& lc, int W, int mode, int prune, int sms);
 cudaError_t launch_spin(const LaunchCfg& lc, int mode, int prune, int grid, const KParams& p,
                         cudaStream_t s);
 

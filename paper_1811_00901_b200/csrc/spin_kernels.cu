@@ -8,26 +8,27 @@ namespace spin {
 // ------------------------------------------------------------------ dispatch
 // kernel_ptr_M_S_D: MODE M, support placement S, dealer D (0 chunk table, 1 WF / AWF
 // compare-and-swap; a separate instantiation, so the table dealer's code is unchanged)
-#define SPIN_DECL(m, s, d) const void* kernel_ptr_##m##_##s##_##d(int prune, int G, int nt);
+#define SPIN_DECL(m, s, d) const void* kernel_ptr_##m##_##s##_##d(int prune, int G, int nt, int cl);
 SPIN_DECL(0, 0, 0) SPIN_DECL(0, 1, 0) SPIN_DECL(0, 2, 0) SPIN_DECL(1, 0, 0) SPIN_DECL(1, 1, 0) SPIN_DECL(1, 2, 0)
 SPIN_DECL(0, 0, 1) SPIN_DECL(0, 1, 1) SPIN_DECL(0, 2, 1) SPIN_DECL(1, 0, 1) SPIN_DECL(1, 1, 1) SPIN_DECL(1, 2, 1)
 #undef SPIN_DECL
-static const void* kernel_for(int mode, int prune, int G, int sup, int nt, int deal) {
+static const void* kernel_for(int mode, int prune, int G, int sup, int nt, int deal, int cl) {
   if (prune == 1 && sup == 2) sup = 1;   // adaptive placement is BRUTE-only
-  typedef const void* (*Fn)(int, int, int);
+  typedef const void* (*Fn)(int, int, int, int);
   static const Fn tab[2][2][3] = {
       {{kernel_ptr_0_0_0, kernel_ptr_0_1_0, kernel_ptr_0_2_0}, {kernel_ptr_1_0_0, kernel_ptr_1_1_0, kernel_ptr_1_2_0}},
       {{kernel_ptr_0_0_1, kernel_ptr_0_1_1, kernel_ptr_0_2_1}, {kernel_ptr_1_0_1, kernel_ptr_1_1_1, kernel_ptr_1_2_1}}};
-  return tab[deal ? 1 : 0][mode ? 1 : 0][sup](prune, G, nt);
+  return tab[deal ? 1 : 0][mode ? 1 : 0][sup](prune, G, nt, cl);
 }
 
-LaunchCfg choose_launch(int W, int mode, int prune) {
+LaunchCfg choose_launch(int W, int mode, int prune, bool allow_cluster) {
   // One CTA per SM.  Images live in shared memory (NEAREST 4 B/bin, BILINEAR 6 B/bin);
   // CELLS take the largest G <= 32 whose 768-thread layout fits; BRUTE the first entry
   // of the measured preference list below that fits.
   constexpr int LIMIT = 220 * 1024;
   LaunchCfg lc;
   lc.threads = NT_DEFAULT;
+  lc.cl = 1;
 #ifdef SPIN_MEASURE
   const char* dg = std::getenv("SPIN_DEBUG_G");   // measurement builds only (unvalidated)
   const char* dn = std::getenv("SPIN_DEBUG_NT");
@@ -45,41 +46,84 @@ LaunchCfg choose_launch(int W, int mode, int prune) {
     lc.G = G;
   } else {
     // BRUTE, in order of preference (measured on C2 / C4): 768 threads with G = 64 or
-    // 32; 768 threads with G = 24 (W = 32: C4 451 ms vs 467 ms for 512 threads with
-    // G = 32 and 524 ms for 768 threads with G = 16); 512 threads with G = 32; then
-    // 768 threads with smaller G
-    static const int pref[][2] = {{768, 64}, {768, 32}, {768, 24}, {512, 32},
-                                  {768, 16}, {768, 8}, {768, 4}};
+    // 32; a two-CTA cluster sharing G = 48 (24 images per CTA) where 32 images do not fit
+    // beside the staged tiles (W = 28 .. 32); 768 threads with G = 24
+    // (W = 32 without clusters: C4 451 ms vs 467 ms for 512 threads with G = 32 and 524 ms
+    // for 768 threads with G = 16); 512 threads with G = 32; then 768 threads with
+    // smaller G.  (The cluster layout may use the whole 227 KB opt-in.)
+    static const int pref[][3] = {{768, 64, 1}, {768, 32, 1}, {768, 48, 2}, {768, 24, 1},
+                                  {512, 32, 1}, {768, 16, 1}, {768, 8, 1}, {768, 4, 1}};
+#ifdef SPIN_MEASURE
+    if (std::getenv("SPIN_NO_CLUSTER")) allow_cluster = false;   // measurement builds only
+#endif
     for (const auto& c : pref) {
+      if (c[2] > 1 && !allow_cluster) continue;
       lc.threads = c[0];
       lc.G = c[1];
-      if (make_layout(lc.G, W, mode, prune, lc.threads).total <= LIMIT) break;
+      lc.cl = c[2];
+      const size_t lim = c[2] > 1 ? 227 * 1024 - 1024 : LIMIT;   // (static smem < 1 KB)
+      if (make_layout(lc.G, W, mode, prune, lc.threads, lc.cl).total <= lim) break;
     }
   }
-  lc.smem = make_layout(lc.G, W, mode, prune, lc.threads).total;
+  lc.smem = make_layout(lc.G, W, mode, prune, lc.threads, lc.cl).total;
   return lc;
 }
 
 // cloud padding: a multiple of every CTA tile (768 x 4 and 512 x 4 points)
 int tile_points() { return 6144; }
 
-int occupancy_blocks(const LaunchCfg& lc, int W, int mode, int prune) {
-  const void* f = kernel_for(mode, prune, lc.G, 1, lc.threads, 0);
+// resident workers of a persistent launch: CTAs (cl = 1) or two-CTA clusters (cl = 2)
+int resident_workers(const LaunchCfg& lc, int W, int mode, int prune, int sms) {
+  const void* f = kernel_for(mode, prune, lc.G, 1, lc.threads, 0, lc.cl);
+  if (!f) return 0;
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.smem);
-  int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, lc.threads, lc.smem) != cudaSuccess)
-    return 0;
   (void)W;
-  return nb;
+  if (lc.cl == 1) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, lc.threads, lc.smem) != cudaSuccess)
+      return 0;
+    return nb * sms;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)lc.cl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)(lc.cl * sms));
+  cfg.blockDim = dim3((unsigned)lc.threads);
+  cfg.dynamicSmemBytes = lc.smem;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nc = 0;
+  if (cudaOccupancyMaxActiveClusters(&nc, f, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return nc;
 }
 
 cudaError_t launch_spin(const LaunchCfg& lc, int mode, int prune, int grid, const KParams& p,
                         cudaStream_t s) {
-  const void* f = kernel_for(mode, prune, lc.G, p.support_in_hot, lc.threads, p.wf ? 1 : 0);
+  const void* f = kernel_for(mode, prune, lc.G, p.support_in_hot, lc.threads, p.wf ? 1 : 0, lc.cl);
+  if (!f) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lc.smem);
   if (e != cudaSuccess) return e;
   void* args[] = {(void*)&p};
-  return cudaLaunchKernel(f, dim3(grid), dim3(lc.threads), args, lc.smem, s);
+  if (lc.cl == 1) return cudaLaunchKernel(f, dim3(grid), dim3(lc.threads), args, lc.smem, s);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)lc.cl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)lc.threads);
+  cfg.dynamicSmemBytes = lc.smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, f, args);
 }
 
 // ------------------------------------------------------------------ a1: relayout + validation

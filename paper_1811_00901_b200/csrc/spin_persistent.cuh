@@ -70,6 +70,12 @@
 #ifndef SPIN_QCAP_CELLS
 #define SPIN_QCAP_CELLS 1024  // CELLS per-warp candidate ring (entries)
 #endif
+#ifndef SPIN_APL_CL
+#define SPIN_APL_CL 1         // two-CTA cluster variant: candidates per lane per accept pass
+#endif
+#ifndef SPIN_MMA_BATCH
+#define SPIN_MMA_BATCH 3      // tensor-core filter: column blocks in flight before their sign gather
+#endif
 #ifndef SPIN_APL_BRUTE512
 #define SPIN_APL_BRUTE512 1   // the same for the 512-thread (W = 32) variant
 #endif
@@ -88,7 +94,7 @@ __host__ __device__ constexpr int cb_of(int G) { return G < CB_MAX ? G : CB_MAX;
 // (G <= 32 BRUTE groups hold ~100 candidates per warp tile: a 256-entry ring frees the
 // shared memory that lets W = 32 run 768-thread CTAs with G = 24)
 __host__ __device__ constexpr int qcap_of(int prune, int G = 64) {
-  return prune ? SPIN_QCAP_CELLS : (G <= 32 ? 256 : 512);
+  return prune ? SPIN_QCAP_CELLS : (G <= 48 ? 256 : 512);
 }
 
 static_assert(CB_MAX * KP == 32 && KP == 4 && KP == KP_POINTS, "mask is one u32: bit (k << 3) | c");
@@ -129,6 +135,28 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
+}
+
+// ---- thread-block clusters (BRUTE, two CTAs sharing one group of centres; DSMEM)
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {   // every thread of every CTA
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// the shared::cluster address of a local shared-memory object in CTA `rank`'s copy
+__device__ __forceinline__ unsigned mapa_rank(const void* local, unsigned rank) {
+  unsigned r;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((unsigned)__cvta_generic_to_shared(local)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void red_cluster_add(unsigned addr, unsigned v) {
+  asm volatile("red.shared::cluster.add.u32 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_s32(unsigned addr, int v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
 }
 
 // The ONE cell-coordinate function used for binning points and for bounding the
@@ -255,7 +283,9 @@ struct Layout {
   size_t oA, oB, oP, oN, oM, oImg, oHi, oQ, oTP, oTN, oMask, oRowS, oRowO, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
-__host__ __device__ inline Layout make_layout(int G, int W, int mode, int prune, int nt) {
+// G: the group's centres (constants, mask words, entries); the CTA holds G / cl of their
+// images (cl = 2: a two-CTA cluster shares one group, each CTA owning half the images)
+__host__ __device__ inline Layout make_layout(int G, int W, int mode, int prune, int nt, int cl = 1) {
   const int NWARP = nt / 32, ROWCAP = nt;   // CELLS: grid rows staged per batch = threads
   Layout L;
   size_t o = 0;
@@ -279,7 +309,7 @@ __host__ __device__ inline Layout make_layout(int G, int W, int mode, int prune,
     o += 4 * (ROWCAP + 1);
     o = align16(o);
   }
-  L.oImg = o; o = align16(o + 4 * (size_t)img_stride(W, mode, prune) * G);
+  L.oImg = o; o = align16(o + 4 * (size_t)img_stride(W, mode, prune) * (G / cl));
   L.oHi = o;
   L.total = o;
   return L;
@@ -432,6 +462,19 @@ __device__ __forceinline__ void resolve(const KParams& p, Dec& d, const float4 P
 }
 
 // Splat an accepted pair into its image (tempSpinImage[k,l]++).
+// CL = 2 (NEAREST): the image of group slot g lives in CTA g / (G/2) of the cluster; the
+// count goes through a shared::cluster address (a fire-and-forget DSMEM reduction when the
+// owner is the partner CTA).  (BILINEAR stays on one-CTA workers: its fixed-point carries
+// need the old value back, and four returning DSMEM atomics per splat measured slower.)
+template <int MODE, int G, int CL>
+__device__ __forceinline__ void apply_cl(const Dec& d, uint32_t* sImg, int IS, int g) {
+  static_assert(MODE == 0, "clusters: NEAREST only");
+  constexpr int GL = G / CL;
+  const unsigned owner = (unsigned)(g / GL);
+  const int ls = g - (int)owner * GL;
+  red_cluster_add(mapa_rank(sImg + ls * IS, owner) + 4u * (unsigned)d.bin, 1u);
+}
+
 template <int MODE, int G>
 __device__ __forceinline__ void apply(const KParams& p, const Dec& d, uint32_t* img, int slot,
                                       int* carry_flag) {
@@ -517,8 +560,16 @@ static __device__ __noinline__ void wf_claim(const KParams& p, int lane, int* wu
 // SUP = 1: the hot loop evaluates the support test for every pair (the paper's order,
 // P:166 before P:169-171); SUP = 0: the hot loop tests the region only and the support
 // test is decided in the accept path (SPIN_F_SUPPORT_LAST, or no support test at all).
-template <int MODE, int PRUNE, int G, int SUP, int NT, int DEAL>
+// CL = 2 (BRUTE NEAREST, table dealer): a two-CTA thread-block cluster is ONE worker: both CTAs take
+// the same chunk (dealt by rank 0, passed through DSMEM) and the same groups of G centres;
+// each owns G/2 of the images and streams every other point tile, so the per-tile work
+// (bulk copy, tf32 split, compaction) is shared by G centres while each SM holds only
+// G/2 images.
+template <int MODE, int PRUNE, int G, int SUP, int NT, int DEAL, int CL>
 __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__ KParams p) {
+  static_assert(CL == 1 || (CL == 2 && MODE == 0 && PRUNE == 0 && DEAL == 0 && G % 2 == 0),
+                "clusters: BRUTE NEAREST, table dealer");
+  constexpr int GL = G / CL;        // images this CTA owns
   constexpr int NWARP = NT / 32;
   constexpr int ROWCAP = NT;        // CELLS: grid rows staged per batch
   extern __shared__ __align__(16) unsigned char smem[];
@@ -530,7 +581,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   const int W = p.W;
   const int WW = W * W;
   const int IS = img_stride(W, MODE, PRUNE);   // shared-memory image stride (words)
-  const Layout L = make_layout(G, W, MODE, PRUNE, NT);
+  const Layout L = make_layout(G, W, MODE, PRUNE, NT, CL);
+  const unsigned crank = CL > 1 ? cluster_rank() : 0u;
   float4* sA = reinterpret_cast<float4*>(smem + L.oA);
   float4* sB = reinterpret_cast<float4*>(smem + L.oB);
   float4* sP = reinterpret_cast<float4*>(smem + L.oP);
@@ -568,8 +620,9 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   static_assert(!MMA_FILTER || (NCB == G / CB && KP == 4), "mma mask layout: NCB words per lane");
   unsigned* sMask = reinterpret_cast<unsigned*>(smem + L.oMask) + warp * 32 * (G / CB);
   const int hiWords = (WW + 1) / 2;
-  uint32_t* gHi = p.hi_scratch + (size_t)blockIdx.x * G * hiWords;   // zero outside groups
+  uint32_t* gHi = p.hi_scratch + (size_t)blockIdx.x * GL * hiWords;   // zero outside groups
   if (tid == 0) s_carry = 0;
+  if (CL > 1) cluster_sync_all();   // every CTA of the cluster has started (DSMEM rule)
 
   if (tid < 6) s_ctr[tid] = 0ull;
   const unsigned long long t0 = gtimer();
@@ -602,12 +655,16 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       if (DEAL) {
         __syncwarp();
         wf_claim(p, lane, s_wu, s_awf[0]);   // warp 0 (AWF reads the rates), lane 0 claims
-      } else {
-        s_chunk = p.is_static ? (first ? p.cta_offset + (int)blockIdx.x : p.n_chunks)
-                              : (int)atomicAdd(p.counter, 1u);
+      } else if (CL == 1 || crank == 0) {
+        // (a cluster is one worker: rank 0 asks and hands the chunk to its partner)
+        const int ch = p.is_static ? (first ? p.cta_offset + (int)(blockIdx.x / CL) : p.n_chunks)
+                                   : (int)atomicAdd(p.counter, 1u);
+        s_chunk = ch;
+        if (CL > 1) st_cluster_s32(mapa_rank(&s_chunk, 1u), ch);
       }
     }
-    __syncthreads();
+    if (CL > 1) cluster_sync_all();
+    else __syncthreads();
     first = false;
     int u0, u1;
     if (DEAL) {
@@ -683,7 +740,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         sN[slot] = N4;
         sM[slot] = mm;
       }
-      for (int i = tid; i < G * IS; i += NT) sImg[i] = 0u;
+      for (int i = tid; i < GL * IS; i += NT) sImg[i] = 0u;
       int nrows = 0;
       if (PRUNE == 1) {
         __syncthreads();
@@ -723,7 +780,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         __syncthreads();
         if (s_live) nrows = (s_rng[3] - s_rng[2] + 1) * (s_rng[5] - s_rng[4] + 1);
       }
-      __syncthreads();
+      if (CL > 1) cluster_sync_all();   // both CTAs zeroed their images before any remote add
+      else __syncthreads();
 
       // ---- a8-a10: stream points, pair test, compact, accept
       // Each thread holds KP points in registers for all G centres.  Per batch of CB
@@ -736,8 +794,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       // candidate operands: centre slot gs, point (source lane, k) from the staged tile
       // entry = (mask word w << 10) | (source lane << 5) | mask bit (k << 3 | c)
       // Tiles filtered on the tensor cores (BRUTE, support test not in the hot loop) use
-      // the mma layout: mask word w of lane L holds bit (j << 3) | (s & 7) for output j
-      // of HMMA s = 8w + (s & 7) = rb * NCB + cb: centre slot (2(L&3) + (j&1)) * NCB + cb
+      // the mma layout: mask word w = column block cb of lane L holds bit (j << 3) | rb for
+      // output j of the HMMA of row block rb: centre slot (2(L&3) + (j&1)) * NCB + cb
       // and row r = (L>>2) + 8(j>>1) of row block rb, staged at lane (rb&3)*8 + ((r+rb)&7),
       // point (rb>>2)*2 + (r>>3).  (Slots and rows are spread so that one lane's
       // candidates read different shared-memory banks in the accept passes.)
@@ -745,8 +803,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       auto decode_entry = [&](unsigned e, int& gs, int& sl, int& kk) {
         if (MMA_FILTER && tile_mma) {
           const int bit = (int)(e & 31u), ln = (int)(e >> 5) & 31;
-          const int sidx = (int)(e >> 10) * 8 + (bit & 7), jv = bit >> 3;
-          const int rb = sidx / NCB, cbk = sidx - rb * NCB;
+          const int cbk = (int)(e >> 10), rb = bit & 7, jv = bit >> 3;
           gs = (2 * (ln & 3) + (jv & 1)) * NCB + cbk;
           const int r = (ln >> 2) + 8 * (jv >> 1);
           sl = (rb & 3) * 8 + ((r + rb) & 7);
@@ -772,6 +829,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       // (CELLS: two per lane for BILINEAR, one for NEAREST, as measured: C3 47.3 vs 48.0 ms,
       // C5 188 vs 191 ms)
       constexpr int APL = PRUNE == 1 ? (MODE == 1 ? SPIN_APL_CELLS : SPIN_APL_CELLS_NEAREST)
+                                     : CL > 1 ? SPIN_APL_CL
                                      : (NT == 512 ? SPIN_APL_BRUTE512 : SPIN_APL_BRUTE);
       auto process_pair = [&](unsigned e0, bool v0, unsigned e1, bool v1) {
         float4 P0, N0, X0, NX0, P1, N1, X1, NX1;
@@ -790,10 +848,15 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         if (SUP == 2) ct.srej += (unsigned)(v0 & (d0.sup_out != 0));
         if (d0.status == 2) resolve<MODE>(p, d0, P0, N0, X0, NX0, ct);
         if (APL == 2 && d1.status == 2) resolve<MODE>(p, d1, P1, N1, X1, NX1, ct);
-        if (d0.status) { ++ct.acc; apply<MODE, G>(p, d0, sImg + g0 * IS, g0, &s_carry); }
+        if (d0.status) {
+          ++ct.acc;
+          if constexpr (CL > 1) apply_cl<MODE, G, CL>(d0, sImg, IS, g0);
+          else apply<MODE, G>(p, d0, sImg + g0 * IS, g0, &s_carry);
+        }
         if (APL == 2 && d1.status) {
           ++ct.acc;
-          apply<MODE, G>(p, d1, sImg + g1 * IS, g1, &s_carry);
+          if constexpr (CL > 1) apply_cl<MODE, G, CL>(d1, sImg, IS, g1);
+          else apply<MODE, G>(p, d1, sImg + g1 * IS, g1, &s_carry);
         }
       };
       auto compact_and_accept = [&]() {
@@ -1016,17 +1079,23 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             const unsigned h1 = (__float_as_uint(v1) + 0x1000u) & 0xffffe000u;
             const unsigned l0 = tig == 3 ? 0x3f800000u : __float_as_uint(v0 - __uint_as_float(h0)) & 0xffffe000u;
             const unsigned l1 = tig == 3 ? 0x3f800000u : __float_as_uint(v1 - __uint_as_float(h1)) & 0xffffe000u;
-            // all NCB products of the row block in flight before their sign gather
-            float d[NCB][4];
+            // up to MB products of the row block in flight before their sign gather (all of
+            // them for NCB <= 3; NCB = 6 (the cluster's 48 centres) in two batches of three,
+            // which keeps the register count within the 768-thread budget)
+            constexpr int MB = (CL == 1 || NCB < SPIN_MMA_BATCH) ? NCB : SPIN_MMA_BATCH;
 #pragma unroll
-            for (int cb = 0; cb < NCB; ++cb)
-              mma_tf32(d[cb][0], d[cb][1], d[cb][2], d[cb][3], h0, h1, l0, l1, bu0[cb], bu1[cb], 0.0f, 0.0f);
+            for (int c0 = 0; c0 < NCB; c0 += MB) {
+              float d[MB][4];
 #pragma unroll
-            for (int cb = 0; cb < NCB; ++cb) {
-              const int sidx = rb * NCB + cb;
-              accm[sidx >> 3] = accept_bits4(accm[sidx >> 3], __float_as_uint(d[cb][0]), __float_as_uint(d[cb][1]),
-                                             __float_as_uint(d[cb][2]), __float_as_uint(d[cb][3]),
-                                             0x01010101u << (sidx & 7));
+              for (int i = 0; i < MB; ++i)
+                if (c0 + i < NCB)
+                  mma_tf32(d[i][0], d[i][1], d[i][2], d[i][3], h0, h1, l0, l1, bu0[c0 + i], bu1[c0 + i], 0.0f, 0.0f);
+#pragma unroll
+              for (int i = 0; i < MB; ++i)
+                if (c0 + i < NCB)
+                  accm[c0 + i] = accept_bits4(accm[c0 + i], __float_as_uint(d[i][0]), __float_as_uint(d[i][1]),
+                                              __float_as_uint(d[i][2]), __float_as_uint(d[i][3]),
+                                              0x01010101u << rb);
             }
           }
 #pragma unroll
@@ -1146,7 +1215,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       };
 
       if (PRUNE == 0) {
-        for (int t = 0; t < p.n_tiles; ++t) {
+        for (int t = (int)crank; t < p.n_tiles; t += CL) {   // (a cluster splits the tiles)
           const int base = t * (NT * KP) + tid;
           int j[KP];
 #pragma unroll
@@ -1257,24 +1326,26 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           __syncthreads();
         }
       }
-      __syncthreads();
+      if (CL > 1) cluster_sync_all();   // every (remote) add into this CTA's images is done
+      else __syncthreads();
       // ---- a12: write the images back in the caller's order
-      for (int i = tid; i < G * WW; i += NT) {
-        const int slot = i / WW;
-        const int e = i - slot * WW;
+      for (int i = tid; i < GL * WW; i += NT) {
+        const int ls = i / WW;            // local image; group slot crank * GL + ls
+        const int slot = (int)crank * GL + ls;
+        const int e = i - ls * WW;
         int mm = sM[slot];
         if (mm == -1) continue;
         float val = 0.0f;
         if (mm < -1) {
           mm = -(mm + 2);
         } else if (MODE == 0) {
-          const uint32_t cnt = sImg[slot * IS + e];
+          const uint32_t cnt = sImg[ls * IS + e];
           if (cnt >= (1u << 24)) atomicOr(&p.err_flags[1], 1);
           val = (float)cnt;
         } else {
           const uint32_t h =
-              s_carry ? (gHi[slot * hiWords + (e >> 1)] >> ((e & 1) * 16)) & 0xffffu : 0u;
-          const double fx = (double)h * 4294967296.0 + (double)sImg[slot * IS + e];
+              s_carry ? (gHi[ls * hiWords + (e >> 1)] >> ((e & 1) * 16)) & 0xffffu : 0u;
+          const double fx = (double)h * 4294967296.0 + (double)sImg[ls * IS + e];
           val = (float)(fx * (1.0 / 8388608.0));
         }
         __stcs(&p.out[(long long)mm * WW + e], val);
@@ -1285,8 +1356,9 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         __threadfence_system();
         __syncthreads();
         if (tid == 0) {
-          long long a = g0;
-          const long long bnd = g0 + gcount;
+          // (this CTA's images: group slots crank * GL .. crank * GL + GL - 1)
+          long long a = g0 + (long long)crank * GL;
+          const long long bnd = g0 + min((long long)gcount, (long long)(crank + 1) * GL);
           while (a < bnd) {
             const long long sg = a / p.seg_images;
             const long long e = min(bnd, (sg + 1) * (long long)p.seg_images);
@@ -1298,7 +1370,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       if (MODE == 1) {
         __syncthreads();
         if (s_carry) {                       // leave the carry scratch zero for the next group
-          for (int i = tid; i < G * hiWords; i += NT) gHi[i] = 0u;
+          for (int i = tid; i < GL * hiWords; i += NT) gHi[i] = 0u;
           __syncthreads();
           if (tid == 0) s_carry = 0;
         }
@@ -1311,7 +1383,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       }
       __syncthreads();
     }
-    units_done += u1 - u0;
+    if (crank == 0) units_done += u1 - u0;   // (a cluster's units are counted once)
     if (DEAL && p.wf == 2 && tid == 0) {
       // AWF: my rate so far, units per microsecond of chunk time (incl. any emulated idling)
       s_awf[2] += (unsigned long long)(u1 - u0);

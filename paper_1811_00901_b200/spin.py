@@ -45,7 +45,8 @@ class Stats(C.Structure):
                 ("n_units", C.c_int32), ("n_chunks", C.c_int32),
                 ("h_cta_start_ns", C.POINTER(C.c_uint64)), ("h_cta_end_ns", C.POINTER(C.c_uint64)),
                 ("h_cta_units", C.POINTER(C.c_int32)), ("cta_capacity", C.c_int32),
-                ("tiles_support_hot", C.c_int64), ("filter_mma", C.c_int32)]
+                ("tiles_support_hot", C.c_int64), ("filter_mma", C.c_int32),
+                ("cta_per_worker", C.c_int32)]
 
 
 _vp = C.c_void_p

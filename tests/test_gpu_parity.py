@@ -804,3 +804,30 @@ def test_python_binding_refuses_bad_buffers(spin, torch):
             eng.generate_host(np.arange(10), 8, 0.05, 0.5, out=np.empty((10, 8, 7), np.float32))
     finally:
         eng.close()
+
+
+@pytest.mark.parametrize("mode", ["nearest"])
+def test_cluster_workers_w32(spin, torch, mode):
+    """W = 28 / 32 BRUTE NEAREST runs on two-CTA clusters (one worker = a CTA pair sharing
+    G = 48 images over DSMEM): every schedule x P x unit gives the oracle's images,
+    units are dealt exactly once, and the non-cluster launches (WF, slow-worker emulation)
+    give the identical images."""
+    P, Nn = clouds.bumpy_sphere(12000, 71)
+    cen = np.arange(0, 12000, 23, dtype=np.int32)
+    for W, b in ((32, 0.01), (28, 0.012)):
+        ora, st = oracle(P, Nn, cen, W, b, 0.0, mode)
+        ref, s0 = run_gpu(spin, torch, P, Nn, cen, W, b, 0.0, mode, stats=True, schedule="SS",
+                          cta_capacity=4096)
+        assert s0["cta_per_worker"] == 2 and s0["G"] == 48, s0
+        assert int(s0["cta_units"].sum()) == s0["n_units"]
+        check(ref, ora, st, mode, f"cluster W={W} {mode}")
+        for sched in ("STATIC", "SS", "GSS", "FAC"):
+            for Pn in (1, 7, 0):
+                for unit in (0, 1, 5):
+                    got = run_gpu(spin, torch, P, Nn, cen, W, b, 0.0, mode, schedule=sched, P=Pn,
+                                  unit=unit)
+                    np.testing.assert_array_equal(got, ref, err_msg=f"W={W} {sched} P={Pn} u={unit}")
+        for kw in (dict(schedule="WF"), dict(schedule="SS", slow_ctas=20, slowdown=2.0)):
+            got, s1 = run_gpu(spin, torch, P, Nn, cen, W, b, 0.0, mode, stats=True, **kw)
+            assert s1["cta_per_worker"] == 1
+            np.testing.assert_array_equal(got, ref, err_msg=str(kw))
