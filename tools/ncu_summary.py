@@ -29,6 +29,24 @@ KEYS = [
     "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
     "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "smsp__warps_eligible.avg.per_cycle_active",
+    # the counters that justify the design: tensor pipe and its HMMA
+    # sub-pipe, ALU pipe, L2 sectors (-> GB/s), shared-memory wavefronts by op, DSMEM atomics
+    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg",
+    "sm__inst_executed_pipe_alu_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "lts__t_sectors.sum", "lts__t_sectors.sum.per_second", "lts__t_sectors.sum.pct_of_peak_sustained_elapsed",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sectors_lookup_hit.sum",
+    "lts__t_sectors_lookup_miss.sum", "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum",
+    "l1tex__t_requests_pipe_lsu_mem_dshared_op_atom.sum",
+    "l1tex__m_l1tex2xbar_write_sectors_mem_dshared_op_atom.sum",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed",
 ]
 
 
@@ -41,8 +59,13 @@ def ncu_csv(rep, page, extra=()):
 def full_summary(rep):
     rows = ncu_csv(rep, "raw")
     hdr, units, vals = rows[0], rows[1], rows[2]
-    d = dict(zip(hdr, vals))
-    u = dict(zip(hdr, units))
+    d, u = {}, {}
+    for k, unit, v in zip(hdr, units, vals):
+        short = k.split(".", 2)[2] if k.count(".") >= 3 and k.split(".")[1] == "TriageCompute" else k
+        d.setdefault(short, v)
+        u.setdefault(short, unit)
+        d[k] = v
+        u[k] = unit
     res = {"kernel": d.get("Kernel Name"), "metrics": {}}
     for k in KEYS:
         if k in d:
@@ -50,6 +73,19 @@ def full_summary(rep):
                 res["metrics"][k] = {"value": float(d[k].replace(",", "")), "unit": u.get(k, "")}
             except ValueError:
                 res["metrics"][k] = {"value": d[k], "unit": u.get(k, "")}
+    m = res["metrics"]
+    try:   # derived: L2 and DRAM bytes per second over the kernel's duration
+        scale = {"ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3,
+                 "msecond": 1e-3, "s": 1.0, "second": 1.0}
+        dur = m["gpu__time_duration.sum"]["value"] * scale[m["gpu__time_duration.sum"]["unit"]]
+        res["derived"] = {
+            "l2_GBps": m["lts__t_sectors.sum"]["value"] * 32 / dur / 1e9,
+            "dram_GBps": sum(m[k]["value"] * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
+                                              "Tbyte": 1e12}.get(m[k]["unit"], 1)
+                             for k in ("dram__bytes_read.sum", "dram__bytes_write.sum")) / dur / 1e9,
+            "duration_s": dur}
+    except (KeyError, TypeError, ZeroDivisionError):
+        pass
     stalls = {}
     for k in hdr:
         if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"):
