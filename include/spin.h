@@ -85,6 +85,13 @@ typedef enum { SPIN_BRUTE = 0, SPIN_CELLS = 1 } spin_prune;
 #define SPIN_F_SUPPORT_FIRST      0x20u /* evaluate the support test for every pair, as P:166 orders it.  With
                                            neither flag, CELLS does so and BRUTE places it adaptively per warp
                                            (accept path while it rejects few candidates)         */
+#define SPIN_F_CLUSTER_PAIR       0x40u /* BRUTE NEAREST, table dealer, one device: run each worker as a two-CTA
+                                           thread-block cluster sharing a group of 48 centres (24 images per
+                                           CTA, partner counts as DSMEM reductions) where that layout fits
+                                           (W <= 32).  Same images; by default one-CTA workers (faster since
+                                           the dense lane-per-centre tiles)                   */
+#define SPIN_F_NO_DENSE           0x80u /* BRUTE: always compact candidates, never the dense lane-per-centre
+                                           tiles (control run; same images)                               */
 
 /* Scheduling parameters.  All-zero = defaults. */
 typedef struct {
@@ -142,6 +149,9 @@ typedef struct {
                                (BRUTE at large W: the pair shares one group of G images, each
                                CTA holding G/2 in shared memory, DSMEM adds); workers =
                                P / cta_per_worker; units are counted on the first CTA      */
+  int64_t tiles_dense;      /* BRUTE: warp tiles whose candidates took the lane-per-centre
+                               path (dense tiles of the Morton-ordered cloud)              */
+  int64_t dense_rows;       /* BRUTE: live points those tiles walked (one warp step each)   */
 } spin_stats;
 
 /*

@@ -201,7 +201,16 @@ struct spin_ctx {
   int64_t N = 0, Npad = 0, cap = 0;
   float4* pos = nullptr;
   float4* nrm = nullptr;
-  float4* tpos = nullptr;   // BRUTE warp-tile pair layout (2 float4 per point)
+  float4* tpos = nullptr;   // BRUTE warp-tile pair layout (2 float4 per point), Morton order
+  float4* bpos = nullptr;   // BRUTE: the cloud in Morton order (bpos[i] = pos[perm[i]])
+  float4* bnrm = nullptr;
+  MortonGrid mgrid{0.f, 0.f, 0.f, 0.f};
+  // Morton sort scratch (cloud at load time, centres per BRUTE call)
+  uint32_t* mk0 = nullptr; int64_t mk0_cap = 0;
+  uint32_t* mk1 = nullptr; int64_t mk1_cap = 0;
+  int32_t* mv0 = nullptr; int64_t mv0_cap = 0;
+  int32_t* mperm = nullptr; int64_t mperm_cap = 0;
+  unsigned char* mtemp = nullptr; int64_t mtemp_cap = 0;
   float absmax = 0.f;
   float aabb[6] = {0, 0, 0, 0, 0, 0};
   uint64_t cloud_version = 0;
@@ -256,6 +265,15 @@ struct spin_ctx {
 
 namespace {
 
+spin_status ensure_morton_scratch(spin_ctx* h, int64_t n) {
+  spin_status st;
+  if ((st = ensure(h->mk0, h->mk0_cap, n, "sort keys")) != SPIN_OK) return st;
+  if ((st = ensure(h->mk1, h->mk1_cap, n, "sort keys")) != SPIN_OK) return st;
+  if ((st = ensure(h->mv0, h->mv0_cap, n, "sort values")) != SPIN_OK) return st;
+  if ((st = ensure(h->mperm, h->mperm_cap, n, "sort order")) != SPIN_OK) return st;
+  return ensure(h->mtemp, h->mtemp_cap, (int64_t)morton_sort_temp_bytes(n), "sort scratch");
+}
+
 spin_status load_cloud(spin_ctx* h, const float* points, const float* normals, int64_t N,
                        cudaStream_t s) {
   if (!points || !normals) return fail(SPIN_E_INVAL, "points/normals must be non-null");
@@ -273,10 +291,14 @@ spin_status load_cloud(spin_ctx* h, const float* points, const float* normals, i
     if (h->pos) cudaFree(h->pos);
     if (h->nrm) cudaFree(h->nrm);
     if (h->tpos) cudaFree(h->tpos);
-    h->pos = h->nrm = h->tpos = nullptr;
+    if (h->bpos) cudaFree(h->bpos);
+    if (h->bnrm) cudaFree(h->bnrm);
+    h->pos = h->nrm = h->tpos = h->bpos = h->bnrm = nullptr;
     h->cap = 0;
     if (cudaMalloc((void**)&h->pos, Npad * sizeof(float4)) != cudaSuccess ||
         cudaMalloc((void**)&h->nrm, Npad * sizeof(float4)) != cudaSuccess ||
+        cudaMalloc((void**)&h->bpos, Npad * sizeof(float4)) != cudaSuccess ||
+        cudaMalloc((void**)&h->bnrm, Npad * sizeof(float4)) != cudaSuccess ||
         cudaMalloc((void**)&h->tpos, 2 * Npad * sizeof(float4)) != cudaSuccess) {
       cudaGetLastError();
       return fail(SPIN_E_NOMEM, "cudaMalloc of the cloud (%lld points) failed", (long long)N);
@@ -298,7 +320,6 @@ spin_status load_cloud(spin_ctx* h, const float* points, const float* normals, i
   CK(launch_relayout(h->stage_p, h->stage_n, N, Npad, h->pos, h->nrm, h->red,
                      reinterpret_cast<float*>(h->red + 1), reinterpret_cast<float*>(h->red + 2), s),
      "relayout");
-  CK(launch_pair_layout(h->pos, h->nrm, Npad, h->tpos, s), "pair layout");
   CK(cudaMemcpyAsync(h->h_red, h->red, sizeof init, cudaMemcpyDeviceToHost, s), "readback");
   CK(cudaStreamSynchronize(s), "spin_create sync");
   int32_t red[8];
@@ -309,6 +330,20 @@ spin_status load_cloud(spin_ctx* h, const float* points, const float* normals, i
   auto unflip = [](int32_t i) { int32_t v = i >= 0 ? i : i ^ 0x7fffffff; float f; std::memcpy(&f, &v, 4); return f; };
   std::memcpy(&h->absmax, &red[1], 4);
   for (int a = 0; a < 6; ++a) h->aabb[a] = unflip(red[2 + a]);
+  // BRUTE layout: the cloud in Morton order (bpos, bnrm) and its warp-tile pair layout
+  // (tpos); a layout choice only, the images are invariant under point order
+  {
+    const float ext = std::max(std::max(h->aabb[3] - h->aabb[0], h->aabb[4] - h->aabb[1]),
+                               std::max(h->aabb[5] - h->aabb[2], 1e-30f));
+    h->mgrid = MortonGrid{h->aabb[0], h->aabb[1], h->aabb[2], (float)(1024.0 / ((double)ext * (1.0 + 1e-6)))};
+    if ((st = ensure_morton_scratch(h, N)) != SPIN_OK) return st;
+    CK(launch_morton_order(nullptr, N, h->pos, (int32_t)N, h->mgrid, h->mk0, h->mk1, h->mv0, h->mperm,
+                           h->mtemp, (size_t)h->mtemp_cap, s),
+       "cloud Morton order");
+    CK(launch_gather_cloud(h->mperm, (int32_t)N, Npad, h->pos, h->nrm, h->bpos, h->bnrm, s), "gather");
+    CK(launch_pair_layout(h->bpos, h->bnrm, Npad, h->tpos, s), "pair layout");
+    CK(cudaStreamSynchronize(s), "spin_create sync");
+  }
   h->N = N;
   h->Npad = Npad;
   h->cloud_version++;
@@ -416,8 +451,12 @@ void plan_thresholds(const spin_ctx* h, int32_t W, double b, double cos_As, bool
   p.literal = (flags & SPIN_F_LITERAL_HALF_WIDTH) ? 1 : 0;
   p.floor_bins = (flags & SPIN_F_FLOOR_BINS) ? 1 : 0;
   p.no_fast_cert = (flags & SPIN_F_NO_FAST_CERT) ? 1 : 0;
+  // BRUTE tensor-core tiles go lane-per-centre when they hold >= dense_min candidates per
+  // live point (measured)
+  p.dense_min = (flags & SPIN_F_NO_DENSE) ? 0 : 8;
 #ifdef SPIN_MEASURE
   if (const char* dbg = std::getenv("SPIN_DEBUG_SKIP")) p.debug_skip = std::atoi(dbg);   // measurement builds only
+  if (const char* dm = std::getenv("SPIN_DENSE_MIN")) p.dense_min = std::atoi(dm);
 #endif
   // self pair (d = 0): beta = q = 0 exactly, u = W/2 (scaled reading only)
   p.self_fast = p.literal ? 0 : 1;
@@ -545,7 +584,7 @@ spin_status spin_pair_codes(spin_handle h, const int32_t* d_centre_idx, int64_t 
   const bool has_support = !(std::isinf(cos_As) && cos_As < 0);
   if (has_support && !(cos_As >= -1.0 && cos_As <= 1.0))
     return fail(SPIN_E_INVAL, "cos_As=%g must be in [-1, 1] or -inf", cos_As);
-  if (flags & ~0x3fu) return fail(SPIN_E_INVAL, "unknown flag bits 0x%x", flags);
+  if (flags & ~0xffu) return fail(SPIN_E_INVAL, "unknown flag bits 0x%x", flags);
   if (M == 0) return SPIN_OK;
   if (!d_centre_idx || !d_codes) return fail(SPIN_E_INVAL, "null d_centre_idx or d_codes");
   const Region rg = region_of(W, b, (int)mode, flags);
@@ -592,7 +631,7 @@ int32_t spin_default_P(int32_t W, spin_mode mode, spin_prune prune) {
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const LaunchCfg lc = choose_launch(W, (int)mode, (int)prune, prune == SPIN_BRUTE && mode == SPIN_NEAREST);
+  const LaunchCfg lc = choose_launch(W, (int)mode, (int)prune, false);
   return resident_workers(lc, W, (int)mode, (int)prune, sms);
 }
 
@@ -637,7 +676,7 @@ spin_status spin_load_cloud(spin_handle h, const float* points, const float* nor
 
 void spin_destroy(spin_handle h) {
   if (!h) return;
-  void* ptrs[] = {h->pos, h->nrm, h->tpos, h->cell_start, h->spos, h->snrm, h->keys, h->counts,
+  void* ptrs[] = {h->pos, h->nrm, h->tpos, h->bpos, h->bnrm, h->mk0, h->mk1, h->mv0, h->mperm, h->mtemp, h->cell_start, h->spos, h->snrm, h->keys, h->counts,
                   h->cursor, h->scan_tmp, h->ckeys, h->cstarts, h->order, h->bounds,
                   h->counter, h->stats, h->err, h->cta_t0, h->cta_t1, h->cta_units, h->cidx,
                   h->outbuf, h->stage_p, h->stage_n, h->red, h->hi_scratch, h->seg_done,
@@ -696,7 +735,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   if (cpar.P < 0 || cpar.unit < 0 || cpar.gss_min_chunk < 0 || cpar.fac_divisor < 0 ||
       cpar.grid < 0 || cpar.cta_offset < 0)
     return fail(SPIN_E_INVAL, "negative chunk parameter");
-  if (cpar.flags & ~0x3fu) return fail(SPIN_E_INVAL, "unknown flag bits 0x%x", cpar.flags);
+  if (cpar.flags & ~0xffu) return fail(SPIN_E_INVAL, "unknown flag bits 0x%x", cpar.flags);
   if (cpar.slow_ctas < 0 || !(cpar.slowdown == 0.0f || (cpar.slowdown >= 1.0f && cpar.slowdown <= 1e6f)))
     return fail(SPIN_E_INVAL, "slow_ctas must be >= 0 and slowdown 0 or in [1, 1e6]");
   if ((cpar.flags & SPIN_F_SUPPORT_LAST) && (cpar.flags & SPIN_F_SUPPORT_FIRST))
@@ -713,12 +752,14 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
 
   // ---- launch shape, P, units, chunk table (a3)
   const bool wf = sched == SPIN_WF || sched == SPIN_AWF;   // dealt on the device by CAS
-  // a worker is one CTA, or (BRUTE, table dealer, one device, no slow-worker emulation) a
-  // two-CTA cluster sharing a group of centres
+  // a worker is one CTA, or on request (SPIN_F_CLUSTER_PAIR; BRUTE, table dealer, one
+  // device, no slow-worker emulation) a two-CTA cluster sharing a group of centres
+  //
   // (NEAREST only: its partner adds are fire-and-forget DSMEM reductions, C4 NEAREST 376 ->
   // 343 ms; BILINEAR's fixed-point carries need the old value back, and four returning DSMEM
   // atomics per splat made C4 BILINEAR slower, 405 -> 529 ms)
-  const bool allow_cluster = prune == SPIN_BRUTE && mode == SPIN_NEAREST && !wf && !cpar.d_counter &&
+  const bool allow_cluster = (cpar.flags & SPIN_F_CLUSTER_PAIR) && prune == SPIN_BRUTE &&
+                             mode == SPIN_NEAREST && !wf && !cpar.d_counter &&
                              cpar.grid == 0 && cpar.cta_offset == 0 &&
                              !(cpar.slowdown > 1.0f && cpar.slow_ctas > 0);
   const LaunchCfg lc = choose_launch(W, (int)mode, (int)prune, allow_cluster);
@@ -819,10 +860,21 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
   p.row_cap = 256;
   double grid_ms = 0.0;
   if (prune == SPIN_BRUTE) {
-    p.pos = h->pos;
-    p.nrm = h->nrm;
+    p.pos = h->bpos;
+    p.nrm = h->bnrm;
     p.tpos = h->tpos;
     p.n_tiles = (int32_t)((h->N + lc.threads * KP_POINTS - 1) / (lc.threads * KP_POINTS));
+    if (!(flags & SPIN_F_NO_SORT)) {
+      // a5: centres in the cloud's Morton order, so that a group's G centres are neighbours
+      // and their candidates fill few warp tiles (stable sort: the same order on every device)
+      spin_status st = ensure_morton_scratch(h, M);
+      if (st == SPIN_OK) st = ensure(h->order, h->order_cap, M, "centre order");
+      if (st != SPIN_OK) return st;
+      CK(launch_morton_order(d_centre_idx, M, h->pos, (int32_t)h->N, h->mgrid, h->mk0, h->mk1, h->mv0,
+                             h->order, h->mtemp, (size_t)h->mtemp_cap, s),
+         "centre Morton order");
+      p.order = h->order;
+    }
   } else {
     const float R = f32_up(rg.R * (1.0 + 1e-6) + 1e-30);
     spin_status st = ensure_grid(h, R, s, &grid_ms);
@@ -925,6 +977,8 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
     stats->fp64_fallbacks = (int64_t)sv[ST_F64];
     stats->exact_fallbacks = (int64_t)sv[ST_EXACT];
     stats->tiles_support_hot = (int64_t)sv[ST_SUPHOT];
+    stats->tiles_dense = (int64_t)sv[ST_DENSE];
+    stats->dense_rows = (int64_t)sv[ST_DROWS];
     stats->filter_mma = p.mma;
     stats->P = grid;
     stats->cta_per_worker = lc.cl;

@@ -65,6 +65,8 @@ struct KParams {
   float self_kf;             // (float)self_k
   float Es_a, Eu_a, Ew_a, D2g;
   int32_t literal, floor_bins, no_fast_cert;
+  int32_t dense_min;         // BRUTE tensor-core tiles: lane-per-centre accept when candidates >=
+                             // dense_min x live points (0: always compact)
   int32_t debug_skip;        // measurement only (env SPIN_DEBUG_SKIP): 1 skip accept, 2 skip compaction too
   int32_t self_fast;         // d == 0 pairs can be decided exactly without arithmetic
   int32_t self_k, self_l;    // their (k, l) (NEAREST) or (i0, -) ; self_k = -1: no contribution
@@ -90,7 +92,7 @@ struct KParams {
 };
 
 enum StatSlot {
-  ST_VISITED = 0, ST_CAND = 1, ST_ACC = 2, ST_F64 = 3, ST_EXACT = 4, ST_SUPHOT = 5, ST_NSLOTS = 8
+  ST_VISITED = 0, ST_CAND = 1, ST_ACC = 2, ST_F64 = 3, ST_EXACT = 4, ST_SUPHOT = 5, ST_DENSE = 6, ST_DROWS = 7, ST_NSLOTS = 8
 };
 
 // Launch configuration chosen by the planner.
@@ -136,6 +138,17 @@ cudaError_t launch_centre_order(const int32_t* centre_idx, int64_t M, const floa
                                 int dy, int dz, int shift, int bits, int32_t* keys,
                                 int32_t* counts, int32_t* starts, int32_t* cursor,
                                 int32_t* scan_tmp, int32_t* order, cudaStream_t s);
+// BRUTE Morton order (a1 cloud copy, a5 centre order): 10 bits per axis over the cubic
+// hull of the AABB, q = min(1023, floor((x - o) * inv))
+struct MortonGrid {
+  float ox, oy, oz, inv;
+};
+size_t morton_sort_temp_bytes(int64_t n);
+cudaError_t launch_morton_order(const int32_t* idx, int64_t n, const float4* pos, int32_t N,
+                                MortonGrid mg, uint32_t* k0, uint32_t* k1, int32_t* v0,
+                                int32_t* order, void* temp, size_t temp_bytes, cudaStream_t s);
+cudaError_t launch_gather_cloud(const int32_t* perm, int32_t N, int64_t Npad, const float4* pos,
+                                const float4* nrm, float4* bpos, float4* bnrm, cudaStream_t s);
 // diagnostic: the accept path's per-pair decision for every (centre, point) pair
 cudaError_t launch_pair_codes(const KParams& p, int mode, const int32_t* centre_idx, int64_t M,
                               int32_t* codes, cudaStream_t s);

@@ -2,6 +2,7 @@
 // and the HBM-bound helper kernels: cloud re-layout/validation (a1), exclusive scan,
 // CELLS grid build (a4) and centre ordering (a5).
 #include "spin_persistent.cuh"
+#include <cub/device/device_radix_sort.cuh>
 
 namespace spin {
 
@@ -46,16 +47,14 @@ LaunchCfg choose_launch(int W, int mode, int prune, bool allow_cluster) {
     lc.G = G;
   } else {
     // BRUTE, in order of preference (measured on C2 / C4): 768 threads with G = 64 or
-    // 32; a two-CTA cluster sharing G = 48 (24 images per CTA) where 32 images do not fit
-    // beside the staged tiles (W = 28 .. 32); 768 threads with G = 24
-    // (W = 32 without clusters: C4 451 ms vs 467 ms for 512 threads with G = 32 and 524 ms
-    // for 768 threads with G = 16); 512 threads with G = 32; then 768 threads with
-    // smaller G.  (The cluster layout may use the whole 227 KB opt-in.)
-    static const int pref[][3] = {{768, 64, 1}, {768, 32, 1}, {768, 48, 2}, {768, 24, 1},
-                                  {512, 32, 1}, {768, 16, 1}, {768, 8, 1}, {768, 4, 1}};
-#ifdef SPIN_MEASURE
-    if (std::getenv("SPIN_NO_CLUSTER")) allow_cluster = false;   // measurement builds only
-#endif
+    // 32; 512 threads with G = 32 where 32 images no longer fit beside 24 staged warp tiles
+    // (W = 28 .. 32: with the dense lane-per-centre tiles one lane per centre fills the warp;
+    // C4 BILINEAR 372 ms with 768 threads / G = 24 -> 306 ms, NEAREST 332 ms on two-CTA
+    // clusters -> 279 ms); then 768 threads with smaller G.  Two-CTA clusters
+    // sharing G = 48 (24 images per CTA, DSMEM adds; the cluster layout may use the whole
+    // 227 KB opt-in) only on request (SPIN_F_CLUSTER_PAIR, BRUTE NEAREST).
+    static const int pref[][3] = {{768, 48, 2}, {768, 64, 1}, {768, 32, 1}, {512, 32, 1},
+                                  {768, 24, 1}, {768, 16, 1}, {768, 8, 1}, {768, 4, 1}};
     for (const auto& c : pref) {
       if (c[2] > 1 && !allow_cluster) continue;
       lc.threads = c[0];
@@ -380,6 +379,67 @@ cudaError_t launch_centre_order(const int32_t* centre_idx, int64_t M, const floa
                                  keys, counts);
   if ((e = launch_exclusive_scan(counts, starts, nb, scan_tmp, s)) != cudaSuccess) return e;
   k_centre_scatter<<<g, tb, 0, s>>>(M, keys, starts, cursor, order);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ a1/a5 BRUTE: Morton order
+// BRUTE streams the cloud in a spatially sorted copy (Morton order of a 2^10-per-axis grid
+// over the cubic hull of the AABB) and takes its centres in the same order, so that the
+// candidates of a group of G neighbouring centres concentrate in few warp tiles (DESIGN.md
+// 7.1 "dense tiles").  The images are a permutation-invariant function of the cloud (integer
+// counts / fixed-point sums), so this is a layout choice only.  The sort is CUB's stable
+// radix sort on (key, index): deterministic, so every device of a shared dealer derives the
+// same chunk -> image map.
+__device__ __forceinline__ uint32_t morton_key(float4 a, MortonGrid mg) {
+  auto q = [&](float x, float o) {
+    const float t = fminf(fmaxf(__fmul_rn(__fsub_rn(x, o), mg.inv), 0.0f), 1023.0f);
+    return (uint32_t)t;
+  };
+  return spread3(q(a.x, mg.ox)) | (spread3(q(a.y, mg.oy)) << 1) | (spread3(q(a.z, mg.oz)) << 2);
+}
+__global__ void k_morton_keys(const int32_t* __restrict__ idx, int64_t n, const float4* __restrict__ pos,
+                              int32_t N, MortonGrid mg, uint32_t* keys, int32_t* vals) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = idx ? idx[i] : (int)i;
+  keys[i] = (c >= 0 && c < N) ? morton_key(pos[c], mg) : 0u;
+  vals[i] = (int32_t)i;
+}
+__global__ void k_gather_cloud(const int32_t* __restrict__ perm, int32_t N, int64_t Npad,
+                               const float4* __restrict__ pos, const float4* __restrict__ nrm,
+                               float4* bpos, float4* bnrm) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= Npad) return;
+  const int64_t j = i < N ? perm[i] : i;   // the sentinel padding stays at the end
+  bpos[i] = pos[j];
+  bnrm[i] = nrm[j];
+}
+
+size_t morton_sort_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)n, 0, 30);
+  return bytes;
+}
+
+// order[0..n) = the positions 0..n-1 sorted by the Morton key of pos[idx[i]] (idx null:
+// of pos[i]); scratch: k0, k1 (keys), v0 (values) of n elements, temp of
+// morton_sort_temp_bytes(n)
+cudaError_t launch_morton_order(const int32_t* idx, int64_t n, const float4* pos, int32_t N,
+                                MortonGrid mg, uint32_t* k0, uint32_t* k1, int32_t* v0,
+                                int32_t* order, void* temp, size_t temp_bytes, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int tb = 256;
+  k_morton_keys<<<(unsigned)((n + tb - 1) / tb), tb, 0, s>>>(idx, n, pos, N, mg, k0, v0);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k0, k1, v0, order, (int)n, 0, 30, s);
+}
+
+cudaError_t launch_gather_cloud(const int32_t* perm, int32_t N, int64_t Npad, const float4* pos,
+                                const float4* nrm, float4* bpos, float4* bnrm, cudaStream_t s) {
+  const int tb = 256;
+  k_gather_cloud<<<(unsigned)((Npad + tb - 1) / tb), tb, 0, s>>>(perm, N, Npad, pos, nrm, bpos, bnrm);
   return cudaGetLastError();
 }
 

@@ -67,6 +67,10 @@
 #ifndef SPIN_IMG_PAD_BRUTE
 #define SPIN_IMG_PAD_BRUTE 1  // the odd stride for BRUTE BILINEAR too (C4 401 -> 398 ms)
 #endif
+#ifndef SPIN_IMG_PAD_NEAREST_BRUTE
+#define SPIN_IMG_PAD_NEAREST_BRUTE 1  // BRUTE NEAREST: odd stride (the dense lane-per-centre path
+                                      // adds to G images at once: bank = (slot + bin) mod 32)
+#endif
 #ifndef SPIN_QCAP_CELLS
 #define SPIN_QCAP_CELLS 1024  // CELLS per-warp candidate ring (entries)
 #endif
@@ -277,7 +281,8 @@ __device__ __forceinline__ unsigned accept_bits4(unsigned acc, unsigned m0, unsi
 // of neighbouring images falls in different banks (measured: C3 43.8 -> 41.8 ms, C4 401 ->
 // 398 ms; for NEAREST the padding measured 1-3% slower)
 __host__ __device__ constexpr int img_stride(int W, int mode, int prune) {
-  return (mode == 1 && (prune == 1 || SPIN_IMG_PAD_BRUTE)) ? ((W * W) | SPIN_IMG_PAD) : W * W;
+  return ((mode == 1 && (prune == 1 || SPIN_IMG_PAD_BRUTE)) || (mode == 0 && prune == 0 && SPIN_IMG_PAD_NEAREST_BRUTE))
+             ? ((W * W) | SPIN_IMG_PAD) : W * W;
 }
 struct Layout {
   size_t oA, oB, oP, oN, oM, oImg, oHi, oQ, oTP, oTN, oMask, oRowS, oRowO, total;
@@ -365,6 +370,7 @@ static __device__ __noinline__ SlowOut slow_pair(float4 P4, float4 N4, float4 X4
 //   2: some decision is not certified in fp32 -> slow_pair (fp64, then exact).
 struct Dec {
   int status;
+  int far;      // |d|^2 certainly beyond the certified domain: certainly outside the region
   int sup_out;  // certainly rejected by the support test
   int bin;      // NEAREST: k*W + l; BILINEAR: i0*W + j0
   float a, c;   // BILINEAR fractional offsets along k and l
@@ -393,6 +399,10 @@ __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const f
   r.a = 0.f;
   r.c = 0.f;
   r.sup_out = sup_out;
+  // fl(dd) carries a relative error below 6u, and D2g exceeds the region's largest |d|^2
+  // by more than 0.2% (spin_api.cpp plan_thresholds), so dd > D2g certainly leaves the
+  // region (D2g < 0: SPIN_F_NO_FAST_CERT, every decision goes to the slow stages)
+  r.far = (dd > p.D2g) & (p.D2g >= 0.0f);
   if (MODE == 0) {
     // the self pair (d == 0): beta = q = 0 exactly, k = ceil(W/2) (or floor), l = 0 (#8)
     const bool self = (fabsf(d0) + fabsf(d1) + fabsf(d2) == 0.f) & (p.self_fast != 0);
@@ -473,6 +483,39 @@ __device__ __forceinline__ void apply_cl(const Dec& d, uint32_t* sImg, int IS, i
   const unsigned owner = (unsigned)(g / GL);
   const int ls = g - (int)owner * GL;
   red_cluster_add(mapa_rank(sImg + ls * IS, owner) + 4u * (unsigned)d.bin, 1u);
+}
+
+__device__ __forceinline__ uint32_t atoms_add(unsigned addr, uint32_t v) {
+  uint32_t r;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(addr), "r"(v) : "memory");
+  return r;
+}
+__device__ __forceinline__ void reds_add(unsigned addr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
+}
+// apply() with the image as a 32-bit shared-window address (no generic-address
+// conversion per pair)
+template <int MODE, int G>
+__device__ __forceinline__ void apply_s(const KParams& p, const Dec& d, unsigned img, int slot,
+                                        int* carry_flag) {
+  if (MODE == 0) {
+    reds_add(img + 4u * (unsigned)d.bin, 1u);
+  } else {
+    const int W = p.W;
+    const unsigned a0 = img + 4u * (unsigned)d.bin, a1 = a0 + 4u * (unsigned)W;
+    const uint32_t v0 = fixed23((1.0f - d.a) * (1.0f - d.c)), v1 = fixed23(d.a * (1.0f - d.c));
+    const uint32_t v2 = fixed23((1.0f - d.a) * d.c), v3 = fixed23(d.a * d.c);
+    const uint32_t o0 = atoms_add(a0, v0), o1 = atoms_add(a1, v1);
+    const uint32_t o2 = atoms_add(a0 + 4u, v2), o3 = atoms_add(a1 + 4u, v3);
+    if (max(max(o0, o1), max(o2, o3)) >= 0xff800000u) {
+      const int hiWords = (W * W + 1) / 2;
+      uint32_t* hi = p.hi_scratch + ((size_t)blockIdx.x * G + slot) * hiWords;
+      if (o0 + v0 < o0) carry_fixed(hi, d.bin, p.err_flags, carry_flag);
+      if (o1 + v1 < o1) carry_fixed(hi, d.bin + W, p.err_flags, carry_flag);
+      if (o2 + v2 < o2) carry_fixed(hi, d.bin + 1, p.err_flags, carry_flag);
+      if (o3 + v3 < o3) carry_fixed(hi, d.bin + W + 1, p.err_flags, carry_flag);
+    }
+  }
 }
 
 template <int MODE, int G>
@@ -576,7 +619,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   __shared__ int s_chunk;
   __shared__ int s_total, s_live;
   __shared__ int s_rng[6];
-  __shared__ unsigned long long s_ctr[6];
+  __shared__ unsigned long long s_ctr[8];
 
   const int W = p.W;
   const int WW = W * W;
@@ -624,7 +667,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   if (tid == 0) s_carry = 0;
   if (CL > 1) cluster_sync_all();   // every CTA of the cluster has started (DSMEM rule)
 
-  if (tid < 6) s_ctr[tid] = 0ull;
+  if (tid < 8) s_ctr[tid] = 0ull;
   const unsigned long long t0 = gtimer();
   Ctr ct{0, 0, 0, 0, 0};
   // SUP = 2 (BRUTE, adaptive support placement, per warp): a warp starts with the support
@@ -636,6 +679,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   bool sup_on = false;
   int sup_count = 0;
   unsigned sup_tiles = 0;
+  unsigned dense_tiles = 0, dense_rows = 0;   // lane 0 of each warp (stats)
   int units_done = 0;
   unsigned long long visited = 0;
   bool first = true;
@@ -859,6 +903,85 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           else apply<MODE, G>(p, d1, sImg + g1 * IS, g1, &s_carry);
         }
       };
+      // Dense tensor-core tiles (BRUTE, one-CTA workers; DESIGN.md 7.1 "dense tiles"): with
+      // the cloud and the centres in Morton order a group's candidates fill few warp tiles,
+      // and those densely.  There lane l takes centre slot l (+ 32 s) and the warp walks the
+      // tile's live points (those with any candidate), reading each point once by broadcast:
+      // no entries to write or decode, one image per lane (no same-address atomics), and
+      // each lane tests its own pair's bit in the mma-layout mask.  Used when the tile holds
+      // at least dense_min candidates per live point, else the compaction path.
+      constexpr bool DENSE = PRUNE == 0 && CL == 1 && MMA_FILTER;
+      auto run_dense = [&](unsigned mor, int mcnt) -> bool {
+        const int total = __reduce_add_sync(0xffffffffu, mcnt);
+        if (total == 0) return false;
+        // live rows: OR over this lane's column blocks, then over the 4 lanes of a row group
+        // (tig), then over the centre parity j & 1: bit half * 8 + rb = row gid + 8 half of
+        // row block rb
+        unsigned v = mor | __shfl_xor_sync(0xffffffffu, mor, 1);
+        v |= __shfl_xor_sync(0xffffffffu, v, 2);
+        v |= v >> 8;
+        const unsigned v16 = (v & 0xffu) | ((v >> 8) & 0xff00u);
+        unsigned lw[4];
+        int live = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {   // word i: row groups 2i (low half) and 2i + 1
+          lw[i] = __shfl_sync(0xffffffffu, v16, 8 * i) | (__shfl_sync(0xffffffffu, v16, 8 * i + 4) << 16);
+          live += __popc(lw[i]);
+        }
+        if (total < live * p.dense_min) return false;
+        if (lane == 0) {
+          ++dense_tiles;
+          dense_rows += (unsigned)live;
+          ct.cand += (unsigned)total;   // the tile's filter candidates (mask bits)
+        }
+        if (skip_accept) return true;
+        // no per-pair mask bit: decide() is exact on its own, and a pair the filter rejected
+        // is either certainly far (status 0) or decided like any candidate
+        constexpr int GS = (G + 31) / 32;
+        constexpr int RS = (KP / 2) * 32 * 4;   // floats between staged records
+        const float* sTf = reinterpret_cast<const float*>(sT);
+        float4 cP[GS], cN[GS];
+        unsigned glive = 0u;   // bit s: slot lane + 32 s holds a live centre
+#pragma unroll
+        for (int s = 0; s < GS; ++s) {
+          const int g = min(lane + 32 * s, G - 1);
+          cP[s] = sP[g];
+          cN[s] = sN[g];
+          glive |= (unsigned)(lane + 32 * s < G && sM[g] >= 0) << s;
+        }
+        const unsigned img0 = (unsigned)__cvta_generic_to_shared(sImg);
+        unsigned w0 = lw[0], w1 = lw[1], w2 = lw[2], w3 = lw[3];
+#pragma unroll 1
+        for (int i = 0; i < 4; ++i) {
+          unsigned wv = w0;
+          w0 = w1;
+          w1 = w2;
+          w2 = w3;
+          while (wv) {
+            const int bq = __ffs(wv) - 1;
+            wv &= wv - 1u;
+            const int gid = 2 * i + (bq >> 4), half = (bq >> 3) & 1, rb = bq & 7;
+            const int r = gid + 8 * half;
+            const int sl = (rb & 3) * 8 + ((r + rb) & 7);
+            const float* rec = sTf + ((rb >> 2) * 32 + sl) * 4 + half;
+            const float4 X4 = make_float4(rec[0], rec[2], rec[RS], 0.f);
+            const float4 NX4 = make_float4(rec[2 * RS], rec[2 * RS + 2], rec[3 * RS], 0.f);
+#pragma unroll
+            for (int s = 0; s < GS; ++s) {
+              const int g = lane + 32 * s;
+              Dec d = decide<MODE>(p, cP[s], cN[s], X4, NX4);
+              if (!((glive >> s) & 1u) || d.far) d.status = 0;
+              if (SUP == 2) ct.srej += (unsigned)(d.sup_out & (d.far == 0) & (int)((glive >> s) & 1u));
+              if (d.status == 2) resolve<MODE>(p, d, cP[s], cN[s], X4, NX4, ct);
+              if (d.status) {
+                ++ct.acc;
+                apply_s<MODE, G>(p, d, img0 + 4u * (unsigned)(g * IS), g, &s_carry);
+              }
+            }
+          }
+        }
+        return true;
+      };
       auto compact_and_accept = [&]() {
         int cnt = 0;
         unsigned wm = 0u;   // this lane's nonzero mask words
@@ -1032,6 +1155,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         __syncwarp();
         const bool sup_hot = SUP == 1 || (SUP == 2 && sup_on);
         tile_mma = MMA_FILTER && p.mma && !sup_hot;
+        unsigned dense_or = 0u;   // mma tiles: OR and popcount of this lane's mask words
+        int dense_cnt = 0;
         if (MMA_FILTER && p.mma && !sup_hot) {
           // sphere margins m = B.x - |x|^2 + K of 16 points x 8 centres per HMMA:
           // A = the points as (x, y, z, -|x|^2) split into tf32 hi and lo parts (columns
@@ -1099,7 +1224,11 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             }
           }
 #pragma unroll
-          for (int w = 0; w < NCB; ++w) sMask[w * 32 + lane] = accm[w];
+          for (int w = 0; w < NCB; ++w) {
+            sMask[w * 32 + lane] = accm[w];
+            dense_or |= accm[w];
+            dense_cnt += __popc(accm[w]);
+          }
         } else {
 #pragma unroll
         for (int pr = 0; pr < KP / 2; ++pr) {
@@ -1197,7 +1326,11 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         }
         }
         __syncwarp();
-        if (p.debug_skip < 2) compact_and_accept();
+        bool done = false;
+        if constexpr (DENSE) {
+          if (tile_mma && p.dense_min > 0 && p.debug_skip < 2) done = run_dense(dense_or, dense_cnt);
+        }
+        if (!done && p.debug_skip < 2) compact_and_accept();
         if (SUP == 2) {
           if (!sup_on) {
             const unsigned r = __reduce_add_sync(0xffffffffu, ct.srej);
@@ -1401,6 +1534,10 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   atomicAdd(&s_ctr[3], (unsigned long long)ct.exact);
   if (tid == 0) atomicAdd(&s_ctr[4], visited);
   if (lane == 0 && sup_tiles) atomicAdd(&s_ctr[5], (unsigned long long)sup_tiles);
+  if (lane == 0 && dense_tiles) {
+    atomicAdd(&s_ctr[6], (unsigned long long)dense_tiles);
+    atomicAdd(&s_ctr[7], (unsigned long long)dense_rows);
+  }
   __syncthreads();
   if (tid == 0) {
     atomicAdd(&p.stats[ST_CAND], s_ctr[0]);
@@ -1409,6 +1546,10 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
     atomicAdd(&p.stats[ST_EXACT], s_ctr[3]);
     atomicAdd(&p.stats[ST_VISITED], s_ctr[4]);
     if (s_ctr[5]) atomicAdd(&p.stats[ST_SUPHOT], s_ctr[5]);
+    if (s_ctr[6]) {
+      atomicAdd(&p.stats[ST_DENSE], s_ctr[6]);
+      atomicAdd(&p.stats[ST_DROWS], s_ctr[7]);
+    }
     p.cta_t0[blockIdx.x] = t0;
     p.cta_t1[blockIdx.x] = t1;
     p.cta_units[blockIdx.x] = units_done;

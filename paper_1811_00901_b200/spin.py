@@ -22,7 +22,7 @@ STATIC, SS, GSS, FAC, WF, AWF = 0, 1, 2, 3, 4, 5
 NEAREST, BILINEAR = 0, 1
 BRUTE, CELLS = 0, 1
 F_LITERAL_HALF_WIDTH, F_FLOOR_BINS, F_NO_SORT, F_NO_FAST_CERT, F_SUPPORT_LAST = 0x1, 0x2, 0x4, 0x8, 0x10
-F_SUPPORT_FIRST = 0x20
+F_SUPPORT_FIRST, F_CLUSTER_PAIR, F_NO_DENSE = 0x20, 0x40, 0x80
 SCHEDULES = {"STATIC": STATIC, "SS": SS, "GSS": GSS, "FAC": FAC, "WF": WF, "AWF": AWF}
 MODES = {"nearest": NEAREST, "bilinear": BILINEAR}
 PRUNES = {"brute": BRUTE, "cells": CELLS}
@@ -46,7 +46,8 @@ class Stats(C.Structure):
                 ("h_cta_start_ns", C.POINTER(C.c_uint64)), ("h_cta_end_ns", C.POINTER(C.c_uint64)),
                 ("h_cta_units", C.POINTER(C.c_int32)), ("cta_capacity", C.c_int32),
                 ("tiles_support_hot", C.c_int64), ("filter_mma", C.c_int32),
-                ("cta_per_worker", C.c_int32)]
+                ("cta_per_worker", C.c_int32), ("tiles_dense", C.c_int64),
+                ("dense_rows", C.c_int64)]
 
 
 _vp = C.c_void_p

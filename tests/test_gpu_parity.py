@@ -654,8 +654,9 @@ def test_fuzz_against_oracle(spin, torch):
         c = float(rng.choice([0.5, 0.0, -0.5, -math.inf, math.cos(math.radians(37.0))]))
         mode = "nearest" if case % 2 == 0 else "bilinear"
         flags = int(rng.choice([0, 0, 0, 1, 2])) if mode == "nearest" else 0
-        # knobs that must not change images: NO_SORT, NO_FAST_CERT, SUPPORT_LAST / FIRST
-        knobs = int(rng.choice([0, 0, 0x4, 0x8, 0x10, 0x20]))
+        # knobs that must not change images: NO_SORT, NO_FAST_CERT, SUPPORT_LAST / FIRST,
+        # CLUSTER_PAIR, NO_DENSE
+        knobs = int(rng.choice([0, 0, 0x4, 0x8, 0x10, 0x20, 0x40, 0x80]))
         kw = dict(schedule=scheds[case % len(scheds)], P=int(rng.choice([0, 1, 5, 148])),
                   unit=int(rng.choice([0, 1, 3])), flags=flags | knobs)
         # heterogeneous-worker emulation (NEXT-1: timing only, never images)
@@ -677,6 +678,27 @@ def test_fuzz_against_oracle(spin, torch):
             np.testing.assert_array_equal(cells, brute, err_msg=what + " cells != brute")
         else:
             check(cells, ora, st, mode, what + " cells")
+
+
+@pytest.mark.parametrize("mode", ["nearest", "bilinear"])
+def test_dense_tiles_same_images(spin, torch, mode):
+    """Dense lane-per-centre tiles (BRUTE on the Morton-ordered cloud): the
+    default run takes them (tiles_dense > 0) and gives the images of the compaction-only
+    control (SPIN_F_NO_DENSE) bit for bit, and the oracle's on a subsample; W = 32 runs the
+    512-thread G = 32 launch, W = 16 / 8 the 768-thread G = 64 one (two centres per lane)."""
+    P, Nn = clouds.bumpy_sphere(40000, 91)
+    cen = np.arange(40000, dtype=np.int32)
+    for W, b, c in ((32, 0.01, 0.0), (16, 0.02, 0.5), (8, 0.05, -math.inf)):
+        got, st = run_gpu(spin, torch, P, Nn, cen, W, b, c, mode, stats=True)
+        assert st["tiles_dense"] > 0 and st["dense_rows"] > 0, st
+        assert st["G"] == (32 if W == 32 else 64), st
+        ctl, st2 = run_gpu(spin, torch, P, Nn, cen, W, b, c, mode, stats=True, flags=spin.F_NO_DENSE)
+        assert st2["tiles_dense"] == 0
+        assert st["pairs_accepted"] == st2["pairs_accepted"]
+        np.testing.assert_array_equal(got, ctl, err_msg=f"dense vs compaction W={W} {mode}")
+        sub = cen[::331]
+        ora, ost = oracle(P, Nn, sub, W, b, c, mode)
+        check(got[sub], ora, ost, mode, f"dense W={W} {mode}")
 
 
 def test_bilinear_near_normal_axis(spin, torch):
@@ -808,16 +830,18 @@ def test_python_binding_refuses_bad_buffers(spin, torch):
 
 @pytest.mark.parametrize("mode", ["nearest"])
 def test_cluster_workers_w32(spin, torch, mode):
-    """W = 28 / 32 BRUTE NEAREST runs on two-CTA clusters (one worker = a CTA pair sharing
-    G = 48 images over DSMEM): every schedule x P x unit gives the oracle's images,
-    units are dealt exactly once, and the non-cluster launches (WF, slow-worker emulation)
-    give the identical images."""
+    """W = 28 / 32 BRUTE NEAREST on request (SPIN_F_CLUSTER_PAIR) runs on two-CTA clusters
+    (one worker = a CTA pair sharing G = 48 images over DSMEM): every schedule x
+    P x unit gives the oracle's images, units are dealt exactly once, and the one-CTA launches
+    (the default: 512 threads, G = 32 with dense tiles; WF; slow-worker emulation) give the
+    identical images."""
     P, Nn = clouds.bumpy_sphere(12000, 71)
     cen = np.arange(0, 12000, 23, dtype=np.int32)
+    CL = spin.F_CLUSTER_PAIR
     for W, b in ((32, 0.01), (28, 0.012)):
         ora, st = oracle(P, Nn, cen, W, b, 0.0, mode)
         ref, s0 = run_gpu(spin, torch, P, Nn, cen, W, b, 0.0, mode, stats=True, schedule="SS",
-                          cta_capacity=4096)
+                          cta_capacity=4096, flags=CL)
         assert s0["cta_per_worker"] == 2 and s0["G"] == 48, s0
         assert int(s0["cta_units"].sum()) == s0["n_units"]
         check(ref, ora, st, mode, f"cluster W={W} {mode}")
@@ -825,9 +849,10 @@ def test_cluster_workers_w32(spin, torch, mode):
             for Pn in (1, 7, 0):
                 for unit in (0, 1, 5):
                     got = run_gpu(spin, torch, P, Nn, cen, W, b, 0.0, mode, schedule=sched, P=Pn,
-                                  unit=unit)
+                                  unit=unit, flags=CL)
                     np.testing.assert_array_equal(got, ref, err_msg=f"W={W} {sched} P={Pn} u={unit}")
-        for kw in (dict(schedule="WF"), dict(schedule="SS", slow_ctas=20, slowdown=2.0)):
+        for kw in (dict(schedule="SS"), dict(schedule="WF", flags=CL),
+                   dict(schedule="SS", slow_ctas=20, slowdown=2.0, flags=CL)):
             got, s1 = run_gpu(spin, torch, P, Nn, cen, W, b, 0.0, mode, stats=True, **kw)
-            assert s1["cta_per_worker"] == 1
+            assert s1["cta_per_worker"] == 1 and s1["G"] == 32, s1
             np.testing.assert_array_equal(got, ref, err_msg=str(kw))

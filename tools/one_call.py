@@ -34,7 +34,8 @@ def main():
                              schedule=a.schedule, out=out, stats=True)
     torch.cuda.synchronize()
     print(f"{cfg['name']} W={W} {mode}: {st['elapsed_ms']:.3f} ms, G={st['G']}, "
-          f"cta_per_worker={st['cta_per_worker']}, candidates={st['pairs_candidate']}")
+          f"cta_per_worker={st['cta_per_worker']}, candidates={st['pairs_candidate']}, "
+          f"accepted={st['pairs_accepted']}, tiles_dense={st['tiles_dense']}, dense_rows={st['dense_rows']}")
     eng.close()
 
 
