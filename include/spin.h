@@ -217,14 +217,18 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
 
 /*
  * spin_generate_host — spin_generate with HOST buffers: copies h_centre_idx [M]
- * to the device, runs, copies the images to h_out [M][W][W] (pinned memory is
- * fastest; pageable works) and synchronises `stream`.  Device scratch for the
- * centres and images is owned by the handle and grown on demand.  For BRUTE runs
- * of >= 8 MB of images the D2H copy is pipelined with the kernel: the kernel counts
- * finished images per output segment (~2 MB each, 16 .. 256 segments) and a handle-owned copy stream
- * waits on each counter (cuStreamWaitValue32, resolved through
- * cudaGetDriverEntryPoint) before copying that segment.  A shared dealer
- * (cp->d_counter) is rejected with SPIN_E_INVAL: multi-device runs use spin_generate.
+ * to the device, runs, delivers the images to h_out [M][W][W] and synchronises
+ * `stream`.  If all of h_out is page-locked and mapped (cudaHostAlloc /
+ * cudaHostRegister / torch pin_memory under unified addressing) the kernel writes
+ * each finished group of images straight into it over the host link, overlapped with
+ * the groups still being computed, whatever the processing order.  Otherwise the
+ * images go to handle-owned device scratch and are copied afterwards; for BRUTE runs of
+ * >= 8 MB in the caller's centre order (SPIN_F_NO_SORT) that D2H copy is pipelined:
+ * the kernel counts finished images per output segment (~2 MB each, 16 .. 256
+ * segments) and a handle-owned copy stream waits on each counter
+ * (cuStreamWaitValue32, resolved through cudaGetDriverEntryPoint) before copying that
+ * segment.  A shared dealer (cp->d_counter) is rejected with SPIN_E_INVAL: multi-device
+ * runs use spin_generate.
  */
 spin_status spin_generate_host(spin_handle h, const int32_t* h_centre_idx, int64_t M,
                                int32_t W, double b, double cos_As, spin_schedule sched,

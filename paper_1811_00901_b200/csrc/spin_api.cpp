@@ -370,8 +370,9 @@ void plan_thresholds(const spin_ctx* h, int32_t W, double b, double cos_As, bool
   // allowance of 2^-19 of the summed magnitudes
   // (and 2^-100 absolute for flushed subnormals).  E bounds the filter in use, so every
   // region pair keeps m > 0.  The tensor cores are used unless their
-  // looser bound grows the candidate sphere by more than 6% (clouds far from the origin
-  // relative to the region size).
+  // looser bound grows the candidate sphere by more than 25% (clouds far from the origin
+  // relative to the region size; the packed-fp32 filter has neither the pre-pass nor the
+  // dense tiles, so the tensor cores win well beyond the 6% of round 1)
   auto sphere = [&](bool mma, double& rho_o, double& E_o) {
     const double shift = 1.01 * (mma ? std::ldexp(1.0, -11) : u) * (X + amid);
     rho_o = std::sqrt(rg.h * rg.h + rg.Qmax) + shift;
@@ -388,7 +389,7 @@ void plan_thresholds(const spin_ctx* h, int32_t W, double b, double cos_As, bool
   sphere(true, rho, E_sph);
   sphere(false, rho_f, E_f);
   const bool use_mma = prune == SPIN_BRUTE && std::getenv("SPIN_NO_MMA") == nullptr &&
-                       rho * rho + 3.0 * E_sph <= 1.06 * (rho_f * rho_f + 3.0 * E_f);
+                       rho * rho + 3.0 * E_sph <= 1.25 * (rho_f * rho_f + 3.0 * E_f);
   if (!use_mma) {
     rho = rho_f;
     E_sph = E_f;
@@ -1062,8 +1063,28 @@ spin_status spin_generate_host(spin_handle h, const int32_t* h_centre_idx, int64
   cudaStream_t s = (cudaStream_t)stream;
   spin_status st;
   if ((st = ensure(h->cidx, h->cidx_cap, M, "centre scratch")) != SPIN_OK) return st;
-  if ((st = ensure(h->outbuf, h->outbuf_cap, M * W * W, "image scratch")) != SPIN_OK) return st;
   CK(cudaMemcpyAsync(h->cidx, h_centre_idx, M * sizeof(int32_t), cudaMemcpyHostToDevice, s), "H2D centres");
+  // Page-locked (mapped) output: the kernel's write-back stores go straight to host memory
+  // over the host link, overlapped with the groups still being computed, in any processing
+  // order (BRUTE's Morton order, CELLS' cell order) -- no device copy, no D2H afterwards.
+  {
+    const size_t bytes = (size_t)M * W * W * sizeof(float);
+    cudaPointerAttributes a0{}, a1{};
+    const bool ok0 = cudaPointerGetAttributes(&a0, h_out) == cudaSuccess;
+    const bool ok1 = cudaPointerGetAttributes(&a1, reinterpret_cast<const char*>(h_out) + bytes - 1) == cudaSuccess;
+    cudaGetLastError();
+    if (ok0 && ok1 && a0.type == cudaMemoryTypeHost && a1.type == cudaMemoryTypeHost && a0.devicePointer &&
+        a1.devicePointer &&
+        reinterpret_cast<const char*>(a1.devicePointer) - reinterpret_cast<const char*>(a0.devicePointer) ==
+            (ptrdiff_t)(bytes - 1)) {
+      st = spin_generate(h, h->cidx, M, W, b, cos_As, sched, cp, mode, prune,
+                         reinterpret_cast<float*>(a0.devicePointer), stats, stream);
+      if (st != SPIN_OK) return st;
+      CK(cudaStreamSynchronize(s), "sync");
+      return SPIN_OK;
+    }
+  }
+  if ((st = ensure(h->outbuf, h->outbuf_cap, M * W * W, "image scratch")) != SPIN_OK) return st;
   // Pipeline the D2H of the images with the kernel: the kernel counts finished images
   // per output segment; a copy stream waits on each counter (cuStreamWaitValue32) and
   // copies that segment while later groups are still being computed.

@@ -46,9 +46,6 @@
 #ifndef SPIN_TMA_WAIT_ALL
 #define SPIN_TMA_WAIT_ALL 1   // every lane polls the tile mbarrier (0: lane 0 polls, warp barrier)
 #endif
-#ifndef SPIN_TMA_NEAREST
-#define SPIN_TMA_NEAREST 0    // bulk-copy staging for BRUTE NEAREST too
-#endif
 #ifndef SPIN_APL_CELLS
 #define SPIN_APL_CELLS 2      // CELLS candidates per lane per accept pass
 #endif
@@ -64,12 +61,19 @@
 #ifndef SPIN_IMG_PAD
 #define SPIN_IMG_PAD 1        // 1: odd image stride in shared memory for CELLS BILINEAR (0: W^2)
 #endif
-#ifndef SPIN_IMG_PAD_BRUTE
-#define SPIN_IMG_PAD_BRUTE 1  // the odd stride for BRUTE BILINEAR too (C4 401 -> 398 ms)
+#ifndef SPIN_IMG_RES
+#define SPIN_IMG_RES 1        // BRUTE image stride in shared memory = SPIN_IMG_RES (mod 32)
 #endif
-#ifndef SPIN_IMG_PAD_NEAREST_BRUTE
-#define SPIN_IMG_PAD_NEAREST_BRUTE 1  // BRUTE NEAREST: odd stride (the dense lane-per-centre path
-                                      // adds to G images at once: bank = (slot + bin) mod 32)
+#ifndef SPIN_DEFER_STAGE
+#define SPIN_DEFER_STAGE 1    // tensor-core tiles: A fragments prefetched from tpos into registers,
+                              // bulk copy into shared memory only for tiles with candidates
+#endif
+#ifndef SPIN_DENSE_ROWS
+#define SPIN_DENSE_ROWS 1     // dense tiles: live rows per step (2 measured slower: C4 275 -> 281 ms)
+#endif
+#ifndef SPIN_FILTER_PREPASS
+#define SPIN_FILTER_PREPASS 1 // tensor-core filter: AND the margins' sign bits first, gather only
+                              // tiles holding a candidate
 #endif
 #ifndef SPIN_QCAP_CELLS
 #define SPIN_QCAP_CELLS 1024  // CELLS per-warp candidate ring (entries)
@@ -280,9 +284,12 @@ __device__ __forceinline__ unsigned accept_bits4(unsigned acc, unsigned m0, unsi
 // Shared-memory image stride in words.  BILINEAR: odd (W^2 or W^2 + 1), so the same bin
 // of neighbouring images falls in different banks (measured: C3 43.8 -> 41.8 ms, C4 401 ->
 // 398 ms; for NEAREST the padding measured 1-3% slower)
+// BRUTE (both modes): W^2 padded to IS = SPIN_IMG_RES (mod 32), so that the dense
+// lane-per-centre adds (lane g -> word g * IS + bin) of neighbouring centres, whose bins for
+// one point differ by a few columns, spread over the banks as (SPIN_IMG_RES * g + bin) mod 32
 __host__ __device__ constexpr int img_stride(int W, int mode, int prune) {
-  return ((mode == 1 && (prune == 1 || SPIN_IMG_PAD_BRUTE)) || (mode == 0 && prune == 0 && SPIN_IMG_PAD_NEAREST_BRUTE))
-             ? ((W * W) | SPIN_IMG_PAD) : W * W;
+  return prune == 0 ? W * W + ((SPIN_IMG_RES - W * W) & 31)
+         : (mode == 1 && SPIN_IMG_PAD) ? ((W * W) | 1) : W * W;
 }
 struct Layout {
   size_t oA, oB, oP, oN, oM, oImg, oHi, oQ, oTP, oTN, oMask, oRowS, oRowO, total;
@@ -641,7 +648,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   // BRUTE BILINEAR stages tiles with one bulk copy (measured: C4 455 -> 435 ms, C2 3.68 ->
   // 3.66 ms); BRUTE NEAREST keeps per-lane loads (measured faster there: C2 3.39 vs 3.48,
   // P6 26.9 vs 27.5 ms with the bulk copy)
-  constexpr bool TMA_TILE = PRUNE == 0 && (MODE == 1 || SPIN_TMA_NEAREST) && SPIN_BRUTE_TMA;
+  constexpr bool TMA_TILE = PRUNE == 0 && SPIN_BRUTE_TMA;
   __shared__ __align__(8) uint64_t s_tile_bar[NWARP];   // BRUTE: tile bulk-copy barrier per warp
   unsigned tile_phase = 0;
   if (TMA_TILE) {
@@ -834,6 +841,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       // lane, mask bit) and processes them 32 at a time, reading the point from the
       // warp's staged copy of the tile (no global re-load).
       unsigned qhead = 0, qtail = 0;
+      float2 pf[8];            // DEFER: A-fragment pairs of this warp's next tile (prefetched)
+      bool have_pf = false;
       constexpr int NWD = G / CB;                      // mask words per lane per tile
       // candidate operands: centre slot gs, point (source lane, k) from the staged tile
       // entry = (mask word w << 10) | (source lane << 5) | mask bit (k << 3 | c)
@@ -950,7 +959,19 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           glive |= (unsigned)(lane + 32 * s < G && sM[g] >= 0) << s;
         }
         const unsigned img0 = (unsigned)__cvta_generic_to_shared(sImg);
+        // live rows by bit scan, two per step where the word holds two (two independent
+        // decisions in flight; 768-thread CTAs, with 80 registers, one).  (A row list in the
+        // entry ring measured slower: C4 NEAREST 243 -> 276 ms)
+        constexpr int DR = NT <= 512 ? SPIN_DENSE_ROWS : 1;
         unsigned w0 = lw[0], w1 = lw[1], w2 = lw[2], w3 = lw[3];
+        auto row_point = [&](int i, int bq, float4& X4, float4& NX4) {
+          const int gid = 2 * i + (bq >> 4), half = (bq >> 3) & 1, rb = bq & 7;
+          const int r = gid + 8 * half;
+          const int sl = (rb & 3) * 8 + ((r + rb) & 7);
+          const float* rec = sTf + ((rb >> 2) * 32 + sl) * 4 + half;
+          X4 = make_float4(rec[0], rec[2], rec[RS], 0.f);
+          NX4 = make_float4(rec[2 * RS], rec[2 * RS + 2], rec[3 * RS], 0.f);
+        };
 #pragma unroll 1
         for (int i = 0; i < 4; ++i) {
           unsigned wv = w0;
@@ -958,24 +979,36 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           w1 = w2;
           w2 = w3;
           while (wv) {
-            const int bq = __ffs(wv) - 1;
+            const int ba = __ffs(wv) - 1;
             wv &= wv - 1u;
-            const int gid = 2 * i + (bq >> 4), half = (bq >> 3) & 1, rb = bq & 7;
-            const int r = gid + 8 * half;
-            const int sl = (rb & 3) * 8 + ((r + rb) & 7);
-            const float* rec = sTf + ((rb >> 2) * 32 + sl) * 4 + half;
-            const float4 X4 = make_float4(rec[0], rec[2], rec[RS], 0.f);
-            const float4 NX4 = make_float4(rec[2 * RS], rec[2 * RS + 2], rec[3 * RS], 0.f);
+            const bool two = DR == 2 && wv != 0u;
+            const int bb = two ? __ffs(wv) - 1 : ba;
+            if (two) wv &= wv - 1u;
+            float4 Xa, NXa, Xb, NXb;
+            row_point(i, ba, Xa, NXa);
+            if (DR == 2) row_point(i, bb, Xb, NXb);
 #pragma unroll
             for (int s = 0; s < GS; ++s) {
               const int g = lane + 32 * s;
-              Dec d = decide<MODE>(p, cP[s], cN[s], X4, NX4);
-              if (!((glive >> s) & 1u) || d.far) d.status = 0;
-              if (SUP == 2) ct.srej += (unsigned)(d.sup_out & (d.far == 0) & (int)((glive >> s) & 1u));
-              if (d.status == 2) resolve<MODE>(p, d, cP[s], cN[s], X4, NX4, ct);
-              if (d.status) {
+              const bool gl = (glive >> s) & 1u;
+              Dec da = decide<MODE>(p, cP[s], cN[s], Xa, NXa);
+              Dec db;
+              if (DR == 2) db = decide<MODE>(p, cP[s], cN[s], Xb, NXb);
+              else db.status = 0, db.far = 1, db.sup_out = 0;
+              if (!gl || da.far) da.status = 0;
+              if (!gl || db.far || !two) db.status = 0;
+              if (SUP == 2) ct.srej += (unsigned)(da.sup_out & (da.far == 0) & (int)gl) +
+                                       (unsigned)(db.sup_out & (db.far == 0) & (int)gl & (int)two);
+              if (da.status == 2) resolve<MODE>(p, da, cP[s], cN[s], Xa, NXa, ct);
+              if (DR == 2 && db.status == 2) resolve<MODE>(p, db, cP[s], cN[s], Xb, NXb, ct);
+              const unsigned ia = img0 + 4u * (unsigned)(g * IS);
+              if (da.status) {
                 ++ct.acc;
-                apply_s<MODE, G>(p, d, img0 + 4u * (unsigned)(g * IS), g, &s_carry);
+                apply_s<MODE, G>(p, da, ia, g, &s_carry);
+              }
+              if (DR == 2 && db.status) {
+                ++ct.acc;
+                apply_s<MODE, G>(p, db, ia, g, &s_carry);
               }
             }
           }
@@ -1126,42 +1159,75 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           if (!more) break;
         }
       };
-      auto run_tile = [&](const int (&j)[KP]) {
-        // stage the tile in pair layout (also the accept path's copy), then read the
-        // records back so each f32x2 operand arrives as an aligned register pair
-        f2 X2[KP / 2], Y2[KP / 2], Z2[KP / 2], NXX2[KP / 2], NX2[KP / 2], NY2[KP / 2], NZ2[KP / 2];
-        if (TMA_TILE) {
-          // the warp's 128 points, already in staging layout in HBM (tpos): one bulk copy
-          // into the warp's staged tile; prior generic reads of the buffer are ordered
-          // before the async-proxy write by the proxy fence
-          if (lane == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            bulk_load(sT, p.tpos + (size_t)(j[0] >> 7) * 256, 4096u, &s_tile_bar[warp]);
-          }
-          if (SPIN_TMA_WAIT_ALL || lane == 0) mbar_wait(&s_tile_bar[warp], tile_phase);
-          if (!SPIN_TMA_WAIT_ALL) __syncwarp();   // lane 0 acquired the phase; the warp barrier orders the rest
-          tile_phase ^= 1u;
-        }
+      // the 8-byte A-fragment pair of row block rb of thread (gid, tig) within a 128-point
+      // chunk in pair layout (the same offset in the staged tile and in tpos)
+      auto frag_off = [&](int rb) {
+        const int gid = lane >> 2, tig = lane & 3;
+        const int sl = (rb & 3) * 8 + ((gid + rb) & 7);
+        return (((tig >> 1) * (KP / 2) + (rb >> 2)) * 32 + sl) * 4 + 2 * (tig & 1);
+      };
+      auto load_frags = [&](float2 (&dst)[8], int chunk) {
+        const float* src = reinterpret_cast<const float*>(p.tpos) + (size_t)chunk * 1024;
 #pragma unroll
-        for (int k = 0; !TMA_TILE && k < KP; k += 2) {
-          const float4 a0 = __ldg(&p.pos[j[k]]), a1 = __ldg(&p.pos[j[k + 1]]);
-          const float4 b0 = __ldg(&p.nrm[j[k]]), b1 = __ldg(&p.nrm[j[k + 1]]);
-          const int pr = k / 2;
-          sT[(0 * (KP / 2) + pr) * 32 + lane] = make_float4(a0.x, a1.x, a0.y, a1.y);
-          sT[(1 * (KP / 2) + pr) * 32 + lane] = make_float4(a0.z, a1.z, -a0.w, -a1.w);
-          sT[(2 * (KP / 2) + pr) * 32 + lane] = make_float4(b0.x, b1.x, b0.y, b1.y);
-          sT[(3 * (KP / 2) + pr) * 32 + lane] = make_float4(b0.z, b1.z, 0.f, 0.f);
+        for (int rb = 0; rb < 8; ++rb) {
+          float2 v;
+          asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];"
+                       : "=f"(v.x), "=f"(v.y) : "l"(src + frag_off(rb)));
+          dst[rb] = v;
         }
-        __syncwarp();
+      };
+      auto run_tile = [&](const int (&j)[KP], int next_chunk) {
+        // stage the tile in pair layout (the accept path's copy and the packed-fp32 filter's
+        // operands), read back so each f32x2 operand arrives as an aligned register pair
+        f2 X2[KP / 2], Y2[KP / 2], Z2[KP / 2], NXX2[KP / 2], NX2[KP / 2], NY2[KP / 2], NZ2[KP / 2];
+        auto stage = [&]() {
+          if (TMA_TILE) {
+            // the warp's 128 points, already in staging layout in HBM (tpos): one bulk copy
+            // into the warp's staged tile; prior generic reads of the buffer are ordered
+            // before the async-proxy write by the proxy fence
+            if (lane == 0) {
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              bulk_load(sT, p.tpos + (size_t)(j[0] >> 7) * 256, 4096u, &s_tile_bar[warp]);
+            }
+            if (SPIN_TMA_WAIT_ALL || lane == 0) mbar_wait(&s_tile_bar[warp], tile_phase);
+            if (!SPIN_TMA_WAIT_ALL) __syncwarp();   // lane 0 acquired the phase; the warp barrier orders the rest
+            tile_phase ^= 1u;
+          }
+#pragma unroll
+          for (int k = 0; !TMA_TILE && k < KP; k += 2) {
+            const float4 a0 = __ldg(&p.pos[j[k]]), a1 = __ldg(&p.pos[j[k + 1]]);
+            const float4 b0 = __ldg(&p.nrm[j[k]]), b1 = __ldg(&p.nrm[j[k + 1]]);
+            const int pr = k / 2;
+            sT[(0 * (KP / 2) + pr) * 32 + lane] = make_float4(a0.x, a1.x, a0.y, a1.y);
+            sT[(1 * (KP / 2) + pr) * 32 + lane] = make_float4(a0.z, a1.z, -a0.w, -a1.w);
+            sT[(2 * (KP / 2) + pr) * 32 + lane] = make_float4(b0.x, b1.x, b0.y, b1.y);
+            sT[(3 * (KP / 2) + pr) * 32 + lane] = make_float4(b0.z, b1.z, 0.f, 0.f);
+          }
+          __syncwarp();
+        };
         const bool sup_hot = SUP == 1 || (SUP == 2 && sup_on);
         tile_mma = MMA_FILTER && p.mma && !sup_hot;
+        // tensor-core tiles read their A fragments from registers loaded straight from tpos
+        // one tile ahead (software pipeline), and stage the tile in shared memory only when
+        // the pre-pass finds a candidate (most tiles of a group hold none); other tiles
+        // stage first
+        // (512-thread CTAs, whose 128 registers per thread hold the prefetch; 768-thread CTAs
+        // stage every tile: SPIN_DEFER_STAGE = 2 defers there too, loading A from tpos
+        // without the prefetch, which spills)
+        // (measured, C4: NEAREST 246.7 -> 242.8 ms deferred, BILINEAR 275.0 -> 279.4 ms: NEAREST only)
+        constexpr bool DEFER = PRUNE == 0 && MMA_FILTER && TMA_TILE &&
+                               (SPIN_DEFER_STAGE == 2 || (SPIN_DEFER_STAGE == 1 && NT <= 512 && MODE == 0));
+        constexpr bool PREFETCH = DEFER && NT <= 512;
+        if (!(DEFER && tile_mma)) stage();
+        if (PREFETCH && !tile_mma) have_pf = false;   // (a packed-fp32 tile consumes no prefetch)
         unsigned dense_or = 0u;   // mma tiles: OR and popcount of this lane's mask words
         int dense_cnt = 0;
+        bool tile_empty = false;  // mma tiles: the pre-pass found no candidate (masks not written)
         if (MMA_FILTER && p.mma && !sup_hot) {
           // sphere margins m = B.x - |x|^2 + K of 16 points x 8 centres per HMMA:
           // A = the points as (x, y, z, -|x|^2) split into tf32 hi and lo parts (columns
           // 0-3 and 4-7; x = hi + lo + O(2^-22 |x|)), B = (Bx, By, Bz, 1) twice (B is tf32
-          // exactly), C = K.  The planner's E bounds the tf32 / accumulation error, so
+          // exactly), and K.  The planner's E bounds the tf32 / accumulation error, so
           // every pair of the region still has m > 0.
           const int gid = lane >> 2, tig = lane & 3;
           // A = 16 points x 8: (x_hi, y_hi, z_hi, w_hi, x_lo, y_lo, z_lo, 1), w = -|x|^2;
@@ -1171,7 +1237,10 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           // r1 {z,z',-|x|^2,-|x'|^2} of the staged pair layout; see decode_entry).
           // hi = round to nearest tf32 (half an ulp of the 10-bit mantissa added, low 13
           // bits cleared; every |value| here is below 2^101), lo = x - hi (exact) cut to
-          // tf32: |x - hi - lo| <= 2^-21 |x|, |w - w_hi| <= 2^-11 |w| (planner's E_mma)
+          // tf32: |x - hi - lo| <= 2^-21 |x|, |w - w_hi| <= 2^-11 |w| (planner's E_mma).
+          // (w split hi/lo with K through the accumulator input -- a 2^-21 |w| bound, 3%
+          // fewer candidates -- measured slower: the {K, K', K, K'} accumulator quads cost
+          // registers and moves per HMMA, C4 275 -> 299 ms, NEAREST 243 -> 289 ms)
           const float* sTf = reinterpret_cast<const float*>(sT);
           // B fragments of the group's centres (column gid = centre slot gid*NCB + cb,
           // rows tig and tig + 4)
@@ -1189,21 +1258,62 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             bu0[cb] = __float_as_uint(b0);
             bu1[cb] = __float_as_uint(b1);
           }
+          // A fragment of row block rb: rows gid and gid + 8 at staged lane
+          // (rb&3)*8 + ((gid+rb)&7), points (rb>>2)*2 + 0 / 1 = the two halves of one pair
+          // record (adjacent floats) -- from the staged tile, or (DEFER) from registers
+          // holding the same 8 bytes of tpos
+          float2 cur[8];
+          if (DEFER && PREFETCH) {
+            if (!have_pf) load_frags(pf, j[0] >> 7);
+#pragma unroll
+            for (int rb = 0; rb < 8; ++rb) cur[rb] = pf[rb];
+            have_pf = next_chunk >= 0;
+            if (have_pf) load_frags(pf, next_chunk);
+          } else if (DEFER) {
+            load_frags(cur, j[0] >> 7);
+          } else {
+#pragma unroll
+            for (int rb = 0; rb < 8; ++rb) cur[rb] = *reinterpret_cast<const float2*>(sTf + frag_off(rb));
+          }
+          auto afrag = [&](int rb, unsigned& h0, unsigned& h1, unsigned& l0, unsigned& l1) {
+            const float v0 = cur[rb].x, v1 = cur[rb].y;
+            h0 = (__float_as_uint(v0) + 0x1000u) & 0xffffe000u;
+            h1 = (__float_as_uint(v1) + 0x1000u) & 0xffffe000u;
+            l0 = tig == 3 ? 0x3f800000u : __float_as_uint(v0 - __uint_as_float(h0)) & 0xffffe000u;
+            l1 = tig == 3 ? 0x3f800000u : __float_as_uint(v1 - __uint_as_float(h1)) & 0xffffe000u;
+          };
+          // pre-pass: every margin of the tile, reduced to "any sign bit clear" by 3-input
+          // ANDs (two LOP3 per HMMA instead of the four-instruction sign gather); with the
+          // Morton-ordered cloud most tiles hold no candidate for a group and stop here
+          bool tile_any = true;
+          if (SPIN_FILTER_PREPASS) {
+            // (one accumulator per column block, for shorter LOP3 chains, measured slower:
+            // C4 filter 127 -> 146 ms)
+            unsigned andv = 0xffffffffu;
+#pragma unroll
+            for (int rb = 0; rb < 8; ++rb) {
+              unsigned h0, h1, l0, l1;
+              afrag(rb, h0, h1, l0, l1);
+#pragma unroll
+              for (int cb = 0; cb < NCB; ++cb) {
+                float d0, d1, d2, d3;
+                mma_tf32(d0, d1, d2, d3, h0, h1, l0, l1, bu0[cb], bu1[cb], 0.0f, 0.0f);
+                andv &= __float_as_uint(d0) & __float_as_uint(d1);
+                andv &= __float_as_uint(d2) & __float_as_uint(d3);
+              }
+            }
+            tile_any = __any_sync(0xffffffffu, (int)andv >= 0);
+          }
+          tile_empty = !tile_any;
+          if (tile_any) {
+          if (DEFER) stage();   // the candidates' points for the accept path
           unsigned accm[NCB];
 #pragma unroll
           for (int w = 0; w < NCB; ++w) accm[w] = 0u;
 #pragma unroll
           for (int rb = 0; rb < 8; ++rb) {
-            // rows gid and gid + 8: staged lane (rb&3)*8 + ((gid+rb)&7), points
-            // (rb>>2)*2 + 0 / 1 = the two halves of one pair record (adjacent floats)
-            const int sl = (rb & 3) * 8 + ((gid + rb) & 7);
-            const float2 v01 = *reinterpret_cast<const float2*>(
-                sTf + (((tig >> 1) * (KP / 2) + (rb >> 2)) * 32 + sl) * 4 + 2 * (tig & 1));
-            const float v0 = v01.x, v1 = v01.y;
-            const unsigned h0 = (__float_as_uint(v0) + 0x1000u) & 0xffffe000u;
-            const unsigned h1 = (__float_as_uint(v1) + 0x1000u) & 0xffffe000u;
-            const unsigned l0 = tig == 3 ? 0x3f800000u : __float_as_uint(v0 - __uint_as_float(h0)) & 0xffffe000u;
-            const unsigned l1 = tig == 3 ? 0x3f800000u : __float_as_uint(v1 - __uint_as_float(h1)) & 0xffffe000u;
+            unsigned h0, h1, l0, l1;
+            afrag(rb, h0, h1, l0, l1);
             // up to MB products of the row block in flight before their sign gather (all of
             // them for NCB <= 3; NCB = 6 (the cluster's 48 centres) in two batches of three,
             // which keeps the register count within the 768-thread budget)
@@ -1228,6 +1338,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             sMask[w * 32 + lane] = accm[w];
             dense_or |= accm[w];
             dense_cnt += __popc(accm[w]);
+          }
           }
         } else {
 #pragma unroll
@@ -1326,9 +1437,9 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         }
         }
         __syncwarp();
-        bool done = false;
+        bool done = tile_empty;
         if constexpr (DENSE) {
-          if (tile_mma && p.dense_min > 0 && p.debug_skip < 2) done = run_dense(dense_or, dense_cnt);
+          if (!done && tile_mma && p.dense_min > 0 && p.debug_skip < 2) done = run_dense(dense_or, dense_cnt);
         }
         if (!done && p.debug_skip < 2) compact_and_accept();
         if (SUP == 2) {
@@ -1354,7 +1465,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
 #pragma unroll
           for (int k = 0; k < KP; ++k) j[k] = base + k * NT;
           if (TMA_TILE) j[0] = t * (NT * KP) + warp * 128;   // the warp's 128-point chunk
-          run_tile(j);
+          run_tile(j, t + CL < p.n_tiles ? (t + CL) * NWARP + warp : -1);
         }
       } else {
         // rows of the visited box, batched ROWCAP at a time
@@ -1454,7 +1565,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
                 j[k] = p.N;  // sentinel
               }
             }
-            run_tile(j);
+            run_tile(j, -1);
           }
           __syncthreads();
         }

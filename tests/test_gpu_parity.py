@@ -428,21 +428,28 @@ def test_bilinear_fixed_point_carries(spin, torch):
 
 
 def test_host_path_pipelined_d2h(spin, torch):
-    """spin_generate_host pipelines the image D2H with the kernel (per-segment completion
-    counters + a copy stream); the host images must equal the device path bit for bit."""
+    """spin_generate_host delivers the device path's images bit for bit on each of its three
+    routes: page-locked output written by the kernel directly (any processing order), pageable
+    output through device scratch with the D2H after the kernel (Morton order), and with the
+    D2H pipelined per output segment (caller order, SPIN_F_NO_SORT)."""
     P, Nn = clouds.bumpy_sphere(20000, 12)
     cen = np.arange(20000, dtype=np.int32)[::-1].copy()
     eng = spin.SpinEngine(P, Nn)
+    pinned = torch.empty((len(cen), 16, 16), dtype=torch.float32).pin_memory()
     try:
         for mode in ("nearest", "bilinear"):
             for sched, unit in (("SS", 0), ("GSS", 1), ("STATIC", 0)):
-                out = np.full((len(cen), 16, 16), -1.0, np.float32)
-                h = eng.generate_host(cen, 16, 0.02, 0.5, mode=mode, schedule=sched, unit=unit, out=out)
                 d = eng.generate(_dev(torch, cen), 16, 0.02, 0.5, mode=mode).cpu().numpy()
-                np.testing.assert_array_equal(h, d, err_msg=f"{mode} {sched} unit={unit}")
+                for route, flags in (("pinned", 0), ("pageable", 0), ("pageable", spin.F_NO_SORT)):
+                    out = pinned.numpy() if route == "pinned" else np.empty((len(cen), 16, 16), np.float32)
+                    out.fill(-1.0)
+                    h = eng.generate_host(cen, 16, 0.02, 0.5, mode=mode, schedule=sched, unit=unit,
+                                          out=out, flags=flags)
+                    np.testing.assert_array_equal(h, d, err_msg=f"{mode} {sched} unit={unit} {route} {flags}")
         pick = np.arange(0, 20000, 997)
         ora, _ = oracle(P, Nn, cen[pick], 16, 0.02, 0.5, "nearest")
-        assert_nearest_exact(h[pick] if False else eng.generate_host(cen, 16, 0.02, 0.5)[pick], ora, "piped host")
+        assert_nearest_exact(eng.generate_host(cen, 16, 0.02, 0.5, out=pinned.numpy())[pick], ora, "pinned host")
+        assert_nearest_exact(eng.generate_host(cen, 16, 0.02, 0.5)[pick], ora, "pageable host")
     finally:
         eng.close()
 
@@ -498,11 +505,11 @@ def test_support_last_same_images(spin, torch, prune):
 def test_heterogeneous_workers_same_images_and_trend(spin, torch):
     """Heterogeneity emulation (the paper's Type1/Type2 runs):
     slow CTAs change timing only, never images (every slowed run equals the ORACLE's images
-    of all 30,000 centres); with a quarter of the CTAs 4x slower, a
+    of all 60,000 centres, ~940 units of 64); with a quarter of the CTAs 4x slower, a
     dynamic schedule beats STATIC (ideal ratio 4 * (111 + 37/4) / 148 = 3.25, SPEC
     acceptance #5 asks >= 1.5), and the slow CTAs process fewer units under SS."""
-    P, Nn = clouds.bumpy_sphere(30000, 31)
-    cen = np.arange(30000, dtype=np.int32)
+    P, Nn = clouds.bumpy_sphere(60000, 31)
+    cen = np.arange(60000, dtype=np.int32)
     eng = spin.SpinEngine(_dev(torch, P), _dev(torch, Nn))
     try:
         d_cen = _dev(torch, cen)
@@ -686,8 +693,8 @@ def test_dense_tiles_same_images(spin, torch, mode):
     default run takes them (tiles_dense > 0) and gives the images of the compaction-only
     control (SPIN_F_NO_DENSE) bit for bit, and the oracle's on a subsample; W = 32 runs the
     512-thread G = 32 launch, W = 16 / 8 the 768-thread G = 64 one (two centres per lane)."""
-    P, Nn = clouds.bumpy_sphere(40000, 91)
-    cen = np.arange(40000, dtype=np.int32)
+    P, Nn = clouds.bumpy_sphere(100000, 91)
+    cen = np.arange(100000, dtype=np.int32)
     for W, b, c in ((32, 0.01, 0.0), (16, 0.02, 0.5), (8, 0.05, -math.inf)):
         got, st = run_gpu(spin, torch, P, Nn, cen, W, b, c, mode, stats=True)
         assert st["tiles_dense"] > 0 and st["dense_rows"] > 0, st
@@ -696,7 +703,7 @@ def test_dense_tiles_same_images(spin, torch, mode):
         assert st2["tiles_dense"] == 0
         assert st["pairs_accepted"] == st2["pairs_accepted"]
         np.testing.assert_array_equal(got, ctl, err_msg=f"dense vs compaction W={W} {mode}")
-        sub = cen[::331]
+        sub = cen[::997]
         ora, ost = oracle(P, Nn, sub, W, b, c, mode)
         check(got[sub], ora, ost, mode, f"dense W={W} {mode}")
 
