@@ -194,6 +194,31 @@ cudaError_t launch_pair_layout(const float4* pos, const float4* nrm, int64_t Npa
   return cudaGetLastError();
 }
 
+// The tcgen05 A operand (BRUTE, spin_persistent TC): per 128-point chunk c, 4 KB with row
+// r = point 128 c + r as (x_hi, y_hi, z_hi, w_hi | x_lo, y_lo, z_lo, 1), w = -|x|^2, hi =
+// x rounded to tf32, lo = x - hi truncated to tf32 (the mma.sync filter's operands, split
+// once at load time instead of per group); canonical no-swizzle K-major layout: the 16-byte
+// half kc of row r at (r & 7) * 16 + (r >> 3) * 256 + kc * 128
+__global__ void k_tf32_operand(const float4* __restrict__ pos, int64_t Npad, float* __restrict__ tfa) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= Npad) return;
+  const float4 a = pos[j];
+  const float v[3] = {a.x, a.y, a.z};
+  float* row = tfa + (j >> 7) * 1024 + ((int)(j & 7) * 16 + (int)((j & 127) >> 3) * 256) / 4;
+  auto hi = [](float x) { return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u); };
+  for (int c = 0; c < 3; ++c) {
+    const float h = hi(v[c]);
+    row[c] = h;
+    row[32 + c] = __uint_as_float(__float_as_uint(v[c] - h) & 0xffffe000u);
+  }
+  row[3] = hi(-a.w);
+  row[35] = 1.0f;
+}
+cudaError_t launch_tf32_operand(const float4* pos, int64_t Npad, float4* tfa, cudaStream_t s) {
+  k_tf32_operand<<<(unsigned)((Npad + 255) / 256), 256, 0, s>>>(pos, Npad, (float*)tfa);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_relayout(const float* pts, const float* nrm, int64_t N, int64_t Npad,
                             float4* pos, float4* nrm4, int32_t* bad, float* absmax, float* aabb,
                             cudaStream_t s) {

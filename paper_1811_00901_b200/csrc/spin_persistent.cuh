@@ -68,6 +68,14 @@
 #define SPIN_DEFER_STAGE 1    // tensor-core tiles: A fragments prefetched from tpos into registers,
                               // bulk copy into shared memory only for tiles with candidates
 #endif
+#ifndef SPIN_TC
+#define SPIN_TC 0             // BRUTE 512-thread G = 32: the sphere filter on tcgen05 (5th-gen tensor
+                              // cores).  Correct (parity tests pass) but measured slower: C4
+                              // BILINEAR 481 vs 275 ms -- the 4 KB A tile per 128-point chunk has
+                              // to stream from L2 for every group, and three buffers per
+                              // warpgroup do not cover its latency (warps wait on the MMA
+                              // barrier 37% of samples; tensor pipe 3% busy).
+#endif
 #ifndef SPIN_DENSE_ROWS
 #define SPIN_DENSE_ROWS 1     // dense tiles: live rows per step (2 measured slower: C4 275 -> 281 ms)
 #endif
@@ -222,6 +230,62 @@ __device__ __forceinline__ void mma_tf32(float& d0, float& d1, float& d2, float&
 __device__ __forceinline__ void up2u(f2 v, unsigned& lo, unsigned& hi) {
   asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
 }
+// ---- 5th-generation tensor cores (tcgen05, sm_100a): the BRUTE sphere filter of the
+// 512-thread G = 32 launch as ONE tcgen05.mma per 128-point chunk (M = 128 points, N = 32
+// centres, K = 8 tf32), operands in shared memory (no swizzle, K-major canonical layout:
+// 8-row x 16-byte core matrices, LBO = 128 B between the two K halves, SBO = 256 B between
+// 8-row groups), the fp32 margins in tensor memory, read back lane = point
+// tcgen05 pipeline depth per warpgroup: A buffers in shared memory, accumulator tiles in
+// tensor memory (4 warpgroups x 4 x 32 columns = all 512); the shared-memory carve-out of
+// the staged-tile and mask regions: A buffers, then the B operand, then 32 points per warp
+constexpr int TC_NA = 3, TC_NB = 4, TC_NBAR = TC_NA + 2 * TC_NB;
+constexpr int TC_OFF_B = 4 * TC_NA * 4096, TC_OFF_PTS = TC_OFF_B + 1024;
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned phase) {
+  unsigned done;
+  asm volatile("{\n\t.reg .pred p;\n\t"
+               "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+               "selp.u32 %0, 1, 0, p;\n\t}"
+               : "=r"(done) : "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(phase) : "memory");
+  return done != 0;
+}
+__device__ __forceinline__ uint64_t umma_desc(unsigned saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)(128u >> 4) << 16) |
+         ((uint64_t)(256u >> 4) << 32) | ((uint64_t)1 << 46);   // version 1, SWIZZLE_NONE
+}
+// instruction descriptor: D f32 (bits 4-5 = 1), A and B tf32 (bits 7-9, 10-12 = 2), both
+// K-major, N >> 3 at bit 17, M >> 4 at bit 24
+__host__ __device__ constexpr uint32_t umma_idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma_tf32(unsigned d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 0, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+               :: "r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc) : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               :: "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+// 32 consecutive tensor-memory columns of this warp's lane quarter: v[c] = column base + c
+// of lane (32 (warp % 4) + lane)
+__device__ __forceinline__ void tmem_ld32(unsigned taddr, uint32_t (&v)[32]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+               "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+               "%30, %31}, [%32];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                 "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                 "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+                 "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+                 "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 // CELLS (cylinder test): pass = (s >= c) && (|beta''| <= h) && (-q'' >= -Qt)
 __device__ __forceinline__ unsigned pair_bit_n(unsigned mask, float s, float c, float abe, float h,
                                                float qn, float nqt, unsigned bit) {
@@ -656,6 +720,29 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
   }
+  // tcgen05 filter (BRUTE, one-CTA 512-thread workers with G = 32; the planner's tf32 bound
+  // applies to it unchanged): four warpgroups, each streaming every fourth 128-point chunk
+  // through ONE tensor-core MMA into a double-buffered tensor-memory tile
+  constexpr bool TC = SPIN_TC && PRUNE == 0 && CL == 1 && NT == 512 && G == 32 && SUP != 1 &&
+                      SPIN_BRUTE_MMA && SPIN_BRUTE_TMA;
+  static_assert(!TC || TC_OFF_PTS + NWARP * 1024 <= 4096 * NWARP + 4 * 32 * (G / cb_of(G)) * NWARP,
+                "tcgen05 buffers must fit the staged-tile and mask regions");
+  __shared__ __align__(8) uint64_t s_tcbar[TC ? 4 * TC_NBAR : 1];   // per warpgroup: A full, D full, D empty
+  __shared__ unsigned s_tmem;
+  const bool tc_on = TC && p.mma && p.tfa != nullptr;
+  if (tc_on) {
+    if (tid < 4 * TC_NBAR) mbar_init(&s_tcbar[tid], (tid % TC_NBAR) >= TC_NA + TC_NB ? 4u : 1u);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
+                   :: "r"((unsigned)__cvta_generic_to_shared(&s_tmem)) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
+  unsigned tc_it = 0;   // chunks this warp's warpgroup has streamed (all groups): buffer / phase
   constexpr int QCAP = qcap_of(PRUNE, G);
   uint16_t* sQ = reinterpret_cast<uint16_t*>(smem + L.oQ) + warp * QCAP;
   // staged tile of this warp in pair layout: record r (0..3) of point pair pr (0..KP/2-1)
@@ -1458,7 +1545,161 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         __syncwarp();
       };
 
-      if (PRUNE == 0) {
+      if (TC && tc_on) {
+        // ---- B operand of the group: 32 centres x (Bx, By, Bz, 1, Bx, By, Bz, K), canonical
+        // K-major layout (core matrix = 8 centres x 4 values)
+        unsigned char* tcbase = smem + L.oTP;
+        {
+          float* sBt = reinterpret_cast<float*>(tcbase + TC_OFF_B);
+          for (int t = tid; t < G * 8; t += NT) {
+            const int n = t >> 3, k = t & 7, c = k & 3;
+            const float4 b4 = sB[n];
+            const float v = c == 0 ? b4.x : c == 1 ? b4.y : c == 2 ? b4.z : (k < 4 ? 1.0f : b4.w);
+            sBt[((n & 7) * 16 + (n >> 3) * 256 + (k >> 2) * 128) / 4 + c] = v;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncthreads();
+        }
+        const int q = warp >> 2, wq = warp & 3;       // warpgroup, tensor-memory lane quarter
+        const int nch = (p.N + 127) >> 7;             // 128-point chunks holding real points
+        const int nq = nch > q ? (nch - q + 3) >> 2 : 0;   // this warpgroup's: q, q + 4, ...
+        // per warpgroup: TC_NA A buffers (4 KB each) and TC_NB tensor-memory tiles (32 columns)
+        uint64_t* bar = s_tcbar + q * TC_NBAR;        // A full [0, NA), D full [NA, NA+NB), D empty
+        const unsigned sA0 = (unsigned)__cvta_generic_to_shared(tcbase + q * (TC_NA * 4096));
+        const uint64_t bdesc = umma_desc((unsigned)__cvta_generic_to_shared(tcbase + TC_OFF_B));
+        const unsigned tmem = s_tmem + (unsigned)(q * (TC_NB * 32));
+        constexpr uint32_t IDESC = umma_idesc_tf32(128, G);
+        float4* sPW = reinterpret_cast<float4*>(tcbase + TC_OFF_PTS) + warp * 64;   // the warp's 32 points
+        float4* sNW = sPW + 32;
+        const bool issuer = wq == 0 && lane == 0;
+        // the issuer (lane 0 of the warpgroup's first warp, itself a consumer) keeps the A
+        // ring full and issues every MMA whose A has landed and whose tensor-memory tile has
+        // been drained, without blocking except for the chunk its own warp needs next
+        int ld_n = 0, mma_n = 0;
+        auto poll = [&](int i, bool block) {
+          while (ld_n < nq && ld_n < i + TC_NA) {   // A slot of chunk ld_n - NA: its MMA completed
+            const unsigned it = tc_it + (unsigned)ld_n;
+            bulk_load(tcbase + q * (TC_NA * 4096) + (it % TC_NA) * 4096,
+                      reinterpret_cast<const unsigned char*>(p.tfa) + (size_t)(q + 4 * ld_n) * 4096, 4096u,
+                      &bar[it % TC_NA]);
+            ++ld_n;
+          }
+          while (mma_n < ld_n && mma_n < i + TC_NB) {
+            const unsigned it = tc_it + (unsigned)mma_n, a = it % TC_NA, d = it % TC_NB, ud = it / TC_NB;
+            const bool must = block && mma_n <= i;
+            if (must) {
+              mbar_wait(&bar[a], (it / TC_NA) & 1u);
+              if (ud > 0) mbar_wait(&bar[TC_NA + TC_NB + d], (ud - 1u) & 1u);
+            } else if (!mbar_test(&bar[a], (it / TC_NA) & 1u) ||
+                       (ud > 0 && !mbar_test(&bar[TC_NA + TC_NB + d], (ud - 1u) & 1u))) {
+              break;
+            }
+            tc_fence_after();
+            umma_tf32(tmem + d * 32u, umma_desc(sA0 + a * 4096u), bdesc, IDESC);
+            umma_commit(&bar[TC_NA + d]);
+            ++mma_n;
+          }
+        };
+        for (int i = 0; i < nq; ++i) {
+          const unsigned it = tc_it + (unsigned)i, d = it % TC_NB;
+          if (issuer) poll(i, true);
+          __syncwarp();
+          mbar_wait(&bar[TC_NA + d], (it / TC_NB) & 1u);
+          tc_fence_after();
+          uint32_t v[32];
+          tmem_ld32(tmem + d * 32u + ((unsigned)(32 * wq) << 16), v);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar[TC_NA + TC_NB + d]);
+          if (issuer) poll(i + 1, false);   // (chunk i's MMA completed: its A slot is free)
+          __syncwarp();
+          // every margin of this lane's point against the 32 centres, reduced to "any sign
+          // bit clear" (a margin >= +0: a candidate)
+          unsigned andv = 0xffffffffu;
+#pragma unroll
+          for (int g = 0; g < 32; g += 2) andv &= v[g] & v[g + 1];
+          if (!__any_sync(0xffffffffu, (int)andv >= 0)) continue;
+          // candidate mask of this lane's point: bit g <-> centre slot g
+          unsigned m = 0u;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) m = accept_bits4(m, v[c], v[8 + c], v[16 + c], v[24 + c], 0x01010101u << c);
+          const int cnt = __popc(m);
+          const int total = __reduce_add_sync(0xffffffffu, cnt);
+          const unsigned liveb = __ballot_sync(0xffffffffu, m != 0u);
+          const int live = __popc(liveb);
+          ct.cand += (unsigned)cnt;
+          // this warp's 32 points (chunk point 32 wq + lane = TMEM lane) into shared memory
+          {
+            const int jp = (q + 4 * i) * 128 + 32 * wq + lane;
+            sPW[lane] = __ldg(&p.pos[jp]);
+            sNW[lane] = __ldg(&p.nrm[jp]);
+          }
+          __syncwarp();
+          if (skip_accept) continue;
+          if (p.dense_min > 0 && total >= live * p.dense_min) {
+            // dense: lane = centre slot, walk the live points (broadcast reads)
+            if (lane == 0) {
+              ++dense_tiles;
+              dense_rows += (unsigned)live;
+            }
+            const float4 cP = sP[lane], cN = sN[lane];
+            const bool gl = sM[lane] >= 0;
+            const unsigned ia = (unsigned)__cvta_generic_to_shared(sImg) + 4u * (unsigned)(lane * IS);
+            unsigned lv = liveb;
+            while (lv) {
+              const int pt = __ffs(lv) - 1;
+              lv &= lv - 1u;
+              const unsigned mp = __shfl_sync(0xffffffffu, m, pt);
+              const float4 X4 = sPW[pt], NX4 = sNW[pt];
+              Dec d = decide<MODE>(p, cP, cN, X4, NX4);
+              const bool v0 = gl && ((mp >> lane) & 1u);
+              if (!v0) d.status = 0;
+              if (SUP == 2) ct.srej += (unsigned)(v0 & (d.sup_out != 0));
+              if (d.status == 2) resolve<MODE>(p, d, cP, cN, X4, NX4, ct);
+              if (d.status) {
+                ++ct.acc;
+                apply_s<MODE, G>(p, d, ia, lane, &s_carry);
+              }
+            }
+          } else {
+            // sparse: entries (point lane << 5 | centre slot) in the ring, eight centre slots
+            // (<= 256 entries) at a time, passes of 32
+            static_assert(QCAP >= 256, "ring: 32 lanes x 8 slots");
+#pragma unroll 1
+            for (int c8 = 0; c8 < 32; c8 += 8) {
+              const unsigned mb = (m >> c8) & 0xffu;
+              const int cb8 = __popc(mb);
+              int x = cb8;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+              }
+              const int tot8 = __shfl_sync(0xffffffffu, x, 31);
+              if (tot8 == 0) continue;
+              uint16_t* qd = sQ + (x - cb8);
+              for (unsigned mm = mb; mm; mm &= mm - 1u) *qd++ = (uint16_t)((lane << 5) | (c8 + __ffs(mm) - 1));
+              __syncwarp();
+              for (int base = 0; base < tot8; base += 32) {
+                if (base + lane < tot8) {
+                  const unsigned e = sQ[base + lane];
+                  const int pt = (int)(e >> 5), gs = (int)(e & 31u);
+                  const float4 P4 = sP[gs], N4 = sN[gs], X4 = sPW[pt], NX4 = sNW[pt];
+                  Dec d = decide<MODE>(p, P4, N4, X4, NX4);
+                  if (SUP == 2) ct.srej += (unsigned)(d.sup_out != 0);
+                  if (d.status == 2) resolve<MODE>(p, d, P4, N4, X4, NX4, ct);
+                  if (d.status) {
+                    ++ct.acc;
+                    apply<MODE, G>(p, d, sImg + gs * IS, gs, &s_carry);
+                  }
+                }
+              }
+              __syncwarp();
+            }
+          }
+        }
+        tc_it += (unsigned)nq;
+      } else if (PRUNE == 0) {
         for (int t = (int)crank; t < p.n_tiles; t += CL) {   // (a cluster splits the tiles)
           const int base = t * (NT * KP) + tid;
           int j[KP];
@@ -1637,6 +1878,12 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
     }
   }
 
+  if (tc_on) {
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(s_tmem) : "memory");
+  }
   // ---- a13: instrumentation
   const unsigned long long t1 = gtimer();
   atomicAdd(&s_ctr[0], (unsigned long long)ct.cand);
