@@ -534,7 +534,10 @@ def run_spin(args):
     in_sphere = None
     if prune == "cells":
         in_sphere = eng.count_in_sphere(d_cen, spin.region_radius(W, b, mode))
-    launches = 1 if prune == "brute" else 6   # CELLS: 5 centre-ordering kernels + the spin kernel
+    # per call: BRUTE the centre Morton keys, CUB's stable radix sort of them (histogram,
+    # exclusive sum, 4 onesweep passes) and the spin kernel; CELLS 5 centre-ordering kernels
+    # + the spin kernel (ncu launch lists in profiles/round2)
+    launches = 8 if prune == "brute" else 6
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--mode", default=None)
     ap.add_argument("--W", type=int, default=None)
     ap.add_argument("--schedule", default="SS")
+    ap.add_argument("--flags", type=lambda v: int(v, 0), default=0)
     a = ap.parse_args()
     import torch
     from paper_1811_00901_b200 import spin
@@ -31,7 +32,7 @@ def main():
     out = torch.empty((len(cen), W, W), dtype=torch.float32, device="cuda")
     for _ in range(2):
         _, st = eng.generate(cen, W, cfg["b"], cfg["cos_As"], mode=mode, prune=cfg["prune"],
-                             schedule=a.schedule, out=out, stats=True)
+                             schedule=a.schedule, out=out, stats=True, flags=a.flags)
     torch.cuda.synchronize()
     print(f"{cfg['name']} W={W} {mode}: {st['elapsed_ms']:.3f} ms, G={st['G']}, "
           f"cta_per_worker={st['cta_per_worker']}, candidates={st['pairs_candidate']}, "
