@@ -76,6 +76,9 @@
                               // warpgroup do not cover its latency (warps wait on the MMA
                               // barrier 37% of samples; tensor pipe 3% busy).
 #endif
+#ifndef SPIN_DENSE_QUEUE
+#define SPIN_DENSE_QUEUE 1    // BRUTE: dense tiles queued per group and drained by all warps
+#endif
 #ifndef SPIN_DENSE_ROWS
 #define SPIN_DENSE_ROWS 1     // dense tiles: live rows per step (2 measured slower: C4 275 -> 281 ms)
 #endif
@@ -778,6 +781,15 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   unsigned long long visited = 0;
   bool first = true;
 
+  // BRUTE dense-tile queue of a group (chunk indices), drained by every warp in phase 2
+  // (BILINEAR: C4 275 -> 267 ms, C2 equal; NEAREST, whose re-staging and mask recomputation
+  // cost more than the balance gains: C4 243 -> 258 ms, P6 21.9 -> 22.4 ms, so not used)
+  constexpr bool DQ = PRUNE == 0 && CL == 1 && MODE == 1 && SPIN_BRUTE_MMA && SPIN_BRUTE_TMA &&
+                      SPIN_DENSE_QUEUE;
+  constexpr int DQ_CAP = DQ ? 512 : 1;
+  __shared__ int s_dq[DQ_CAP];
+  __shared__ int s_dq_n, s_dq_head;
+  if (DQ && tid == 0) s_dq_n = s_dq_head = 0;
   __shared__ int s_wu[2];              // WF/AWF: the claimed unit range
   // AWF bookkeeping of tid 0 (in shared memory: no registers live across the loop):
   // [0] claim time, [1] chunk time so far, [2] units so far
@@ -1007,7 +1019,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       // each lane tests its own pair's bit in the mma-layout mask.  Used when the tile holds
       // at least dense_min candidates per live point, else the compaction path.
       constexpr bool DENSE = PRUNE == 0 && CL == 1 && MMA_FILTER;
-      auto run_dense = [&](unsigned mor, int mcnt) -> bool {
+      auto run_dense = [&](unsigned mor, int mcnt, int chunk, bool phase2) -> bool {
         const int total = __reduce_add_sync(0xffffffffu, mcnt);
         if (total == 0) return false;
         // live rows: OR over this lane's column blocks, then over the 4 lanes of a row group
@@ -1026,7 +1038,19 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         }
         // (a step costs one decision per centre slot of the lane: the threshold scales with
         // GS; measured C2 (G = 64): 8 per slot 3.29 ms, 16: 3.24 ms)
-        if (total < live * p.dense_min * ((G + 31) / 32)) return false;
+        if (!phase2 && total < live * p.dense_min * ((G + 31) / 32)) return false;
+        if (DQ && !phase2) {
+          // the group's dense tiles are few and land on few warps (the cloud is Morton
+          // ordered): queue the tile for the CTA-wide second phase, where every warp takes
+          // queued tiles until none are left (inline when the queue is full)
+          int slot = 0;
+          if (lane == 0) slot = atomicAdd(&s_dq_n, 1);
+          slot = __shfl_sync(0xffffffffu, slot, 0);
+          if (slot < DQ_CAP) {
+            if (lane == 0) s_dq[slot] = chunk;
+            return true;
+          }
+        }
         if (lane == 0) {
           ++dense_tiles;
           dense_rows += (unsigned)live;
@@ -1265,7 +1289,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           dst[rb] = v;
         }
       };
-      auto run_tile = [&](const int (&j)[KP], int next_chunk) {
+      auto run_tile = [&](const int (&j)[KP], int next_chunk, bool phase2) {
         // stage the tile in pair layout (the accept path's copy and the packed-fp32 filter's
         // operands), read back so each f32x2 operand arrives as an aligned register pair
         f2 X2[KP / 2], Y2[KP / 2], Z2[KP / 2], NXX2[KP / 2], NX2[KP / 2], NY2[KP / 2], NZ2[KP / 2];
@@ -1295,7 +1319,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           __syncwarp();
         };
         const bool sup_hot = SUP == 1 || (SUP == 2 && sup_on);
-        tile_mma = MMA_FILTER && p.mma && !sup_hot;
+        tile_mma = MMA_FILTER && p.mma && (!sup_hot || phase2);   // (queued tiles were mma tiles)
         // tensor-core tiles read their A fragments from registers loaded straight from tpos
         // one tile ahead (software pipeline), and stage the tile in shared memory only when
         // the pre-pass finds a candidate (most tiles of a group hold none); other tiles
@@ -1307,12 +1331,12 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         constexpr bool DEFER = PRUNE == 0 && MMA_FILTER && TMA_TILE &&
                                (SPIN_DEFER_STAGE == 2 || (SPIN_DEFER_STAGE == 1 && NT <= 512 && MODE == 0));
         constexpr bool PREFETCH = DEFER && NT <= 512;
-        if (!(DEFER && tile_mma)) stage();
+        if (!(DEFER && tile_mma) || phase2) stage();
         if (PREFETCH && !tile_mma) have_pf = false;   // (a packed-fp32 tile consumes no prefetch)
         unsigned dense_or = 0u;   // mma tiles: OR and popcount of this lane's mask words
         int dense_cnt = 0;
         bool tile_empty = false;  // mma tiles: the pre-pass found no candidate (masks not written)
-        if (MMA_FILTER && p.mma && !sup_hot) {
+        if (tile_mma) {
           // sphere margins m = B.x - |x|^2 + K of 16 points x 8 centres per HMMA:
           // A = the points as (x, y, z, -|x|^2) split into tf32 hi and lo parts (columns
           // 0-3 and 4-7; x = hi + lo + O(2^-22 |x|)), B = (Bx, By, Bz, 1) twice (B is tf32
@@ -1352,7 +1376,10 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           // record (adjacent floats) -- from the staged tile, or (DEFER) from registers
           // holding the same 8 bytes of tpos
           float2 cur[8];
-          if (DEFER && PREFETCH) {
+          if (phase2) {
+#pragma unroll
+            for (int rb = 0; rb < 8; ++rb) cur[rb] = *reinterpret_cast<const float2*>(sTf + frag_off(rb));
+          } else if (DEFER && PREFETCH) {
             if (!have_pf) load_frags(pf, j[0] >> 7);
 #pragma unroll
             for (int rb = 0; rb < 8; ++rb) cur[rb] = pf[rb];
@@ -1375,7 +1402,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           // ANDs (two LOP3 per HMMA instead of the four-instruction sign gather); with the
           // Morton-ordered cloud most tiles hold no candidate for a group and stop here
           bool tile_any = true;
-          if (SPIN_FILTER_PREPASS) {
+          if (SPIN_FILTER_PREPASS && !phase2) {
             // (one accumulator per column block, for shorter LOP3 chains, measured slower:
             // C4 filter 127 -> 146 ms)
             unsigned andv = 0xffffffffu;
@@ -1395,7 +1422,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           }
           tile_empty = !tile_any;
           if (tile_any) {
-          if (DEFER) stage();   // the candidates' points for the accept path
+          if (DEFER && !phase2) stage();   // the candidates' points for the accept path
           unsigned accm[NCB];
 #pragma unroll
           for (int w = 0; w < NCB; ++w) accm[w] = 0u;
@@ -1528,7 +1555,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         __syncwarp();
         bool done = tile_empty;
         if constexpr (DENSE) {
-          if (!done && tile_mma && p.dense_min > 0 && p.debug_skip < 2) done = run_dense(dense_or, dense_cnt);
+          if (!done && tile_mma && (phase2 || p.dense_min > 0) && p.debug_skip < 2)
+            done = run_dense(dense_or, dense_cnt, j[0] >> 7, phase2);
         }
         if (!done && p.debug_skip < 2) compact_and_accept();
         if (SUP == 2) {
@@ -1708,7 +1736,25 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
 #pragma unroll
           for (int k = 0; k < KP; ++k) j[k] = base + k * NT;
           if (TMA_TILE) j[0] = t * (NT * KP) + warp * 128;   // the warp's 128-point chunk
-          run_tile(j, t + CL < p.n_tiles ? (t + CL) * NWARP + warp : -1);
+          run_tile(j, t + CL < p.n_tiles ? (t + CL) * NWARP + warp : -1, false);
+        }
+        if (DQ) {
+          // phase 2: the group's queued dense tiles, dealt to the warps one at a time
+          __syncthreads();
+          const int nq = min(s_dq_n, DQ_CAP);
+          for (;;) {
+            int k = 0;
+            if (lane == 0) k = atomicAdd(&s_dq_head, 1);
+            k = __shfl_sync(0xffffffffu, k, 0);
+            if (k >= nq) break;
+            int j[KP];
+            j[0] = s_dq[k] * 128;
+#pragma unroll
+            for (int kk = 1; kk < KP; ++kk) j[kk] = j[0];
+            run_tile(j, -1, true);
+          }
+          __syncthreads();
+          if (tid == 0) s_dq_n = s_dq_head = 0;
         }
       } else {
         // rows of the visited box, batched ROWCAP at a time
@@ -1808,7 +1854,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
                 j[k] = p.N;  // sentinel
               }
             }
-            run_tile(j, -1);
+            run_tile(j, -1, false);
           }
           __syncthreads();
         }
