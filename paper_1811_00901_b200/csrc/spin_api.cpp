@@ -205,6 +205,7 @@ struct spin_ctx {
   float4* bpos = nullptr;   // BRUTE: the cloud in Morton order (bpos[i] = pos[perm[i]])
   float4* bnrm = nullptr;
   float4* tfa = nullptr;    // BRUTE tcgen05 A operand (2 float4 per point)
+  float4* mfrag = nullptr;  // BRUTE mma.sync A fragments (2 float4 per point)
   MortonGrid mgrid{0.f, 0.f, 0.f, 0.f};
   // Morton sort scratch (cloud at load time, centres per BRUTE call)
   uint32_t* mk0 = nullptr; int64_t mk0_cap = 0;
@@ -295,14 +296,16 @@ spin_status load_cloud(spin_ctx* h, const float* points, const float* normals, i
     if (h->bpos) cudaFree(h->bpos);
     if (h->bnrm) cudaFree(h->bnrm);
     if (h->tfa) cudaFree(h->tfa);
-    h->pos = h->nrm = h->tpos = h->bpos = h->bnrm = h->tfa = nullptr;
+    if (h->mfrag) cudaFree(h->mfrag);
+    h->pos = h->nrm = h->tpos = h->bpos = h->bnrm = h->tfa = h->mfrag = nullptr;
     h->cap = 0;
     if (cudaMalloc((void**)&h->pos, Npad * sizeof(float4)) != cudaSuccess ||
         cudaMalloc((void**)&h->nrm, Npad * sizeof(float4)) != cudaSuccess ||
         cudaMalloc((void**)&h->bpos, Npad * sizeof(float4)) != cudaSuccess ||
         cudaMalloc((void**)&h->bnrm, Npad * sizeof(float4)) != cudaSuccess ||
         cudaMalloc((void**)&h->tpos, 2 * Npad * sizeof(float4)) != cudaSuccess ||
-        cudaMalloc((void**)&h->tfa, 2 * Npad * sizeof(float4)) != cudaSuccess) {
+        cudaMalloc((void**)&h->tfa, 2 * Npad * sizeof(float4)) != cudaSuccess ||
+        cudaMalloc((void**)&h->mfrag, 2 * Npad * sizeof(float4)) != cudaSuccess) {
       cudaGetLastError();
       return fail(SPIN_E_NOMEM, "cudaMalloc of the cloud (%lld points) failed", (long long)N);
     }
@@ -346,6 +349,7 @@ spin_status load_cloud(spin_ctx* h, const float* points, const float* normals, i
     CK(launch_gather_cloud(h->mperm, (int32_t)N, Npad, h->pos, h->nrm, h->bpos, h->bnrm, s), "gather");
     CK(launch_pair_layout(h->bpos, h->bnrm, Npad, h->tpos, s), "pair layout");
     CK(launch_tf32_operand(h->bpos, Npad, h->tfa, s), "tcgen05 operand");
+    CK(launch_mma_frags(h->bpos, Npad, h->mfrag, s), "mma fragments");
     CK(cudaStreamSynchronize(s), "spin_create sync");
   }
   h->N = N;
@@ -681,7 +685,7 @@ spin_status spin_load_cloud(spin_handle h, const float* points, const float* nor
 
 void spin_destroy(spin_handle h) {
   if (!h) return;
-  void* ptrs[] = {h->pos, h->nrm, h->tpos, h->bpos, h->bnrm, h->tfa, h->mk0, h->mk1, h->mv0, h->mperm, h->mtemp, h->cell_start, h->spos, h->snrm, h->keys, h->counts,
+  void* ptrs[] = {h->pos, h->nrm, h->tpos, h->bpos, h->bnrm, h->tfa, h->mfrag, h->mk0, h->mk1, h->mv0, h->mperm, h->mtemp, h->cell_start, h->spos, h->snrm, h->keys, h->counts,
                   h->cursor, h->scan_tmp, h->ckeys, h->cstarts, h->order, h->bounds,
                   h->counter, h->stats, h->err, h->cta_t0, h->cta_t1, h->cta_units, h->cidx,
                   h->outbuf, h->stage_p, h->stage_n, h->red, h->hi_scratch, h->seg_done,
@@ -869,6 +873,7 @@ spin_status spin_generate(spin_handle h, const int32_t* d_centre_idx, int64_t M,
     p.nrm = h->bnrm;
     p.tpos = h->tpos;
     p.tfa = h->tfa;
+    p.mfrag = h->mfrag;
     p.n_tiles = (int32_t)((h->N + lc.threads * KP_POINTS - 1) / (lc.threads * KP_POINTS));
     if (!(flags & SPIN_F_NO_SORT)) {
       // a5: centres in the cloud's Morton order, so that a group's G centres are neighbours

@@ -14,6 +14,8 @@ struct KParams {
   const float4* __restrict__ nrm;   // {nx, ny, nz, 0}
   const float4* __restrict__ tpos;  // BRUTE: the cloud in 128-point warp-tile pair layout
                                     // (4 KB per chunk, the smem staging layout; TMA source)
+  const float4* __restrict__ mfrag; // BRUTE: per 128-point chunk the mma.sync A fragments (4 KB:
+                                    // uint4 (x_hi, x'_hi, x_lo, x'_lo) per row block and lane)
   const float4* __restrict__ tfa;   // BRUTE: per 128-point chunk the tcgen05 A operand (4 KB:
                                     // tf32 (x,y,z,-|x|^2) hi and (x,y,z) lo + 1, canonical layout)
   const float4* __restrict__ cpos;  // original-order copies, indexed by centre index
@@ -120,6 +122,8 @@ cudaError_t launch_spin(const LaunchCfg& lc, int mode, int prune, int grid, cons
 // cloud relayout + validation (a1)
 cudaError_t launch_pair_layout(const float4* pos, const float4* nrm, int64_t Npad, float4* tpos,
                                cudaStream_t s);
+// the mma.sync A fragments of every 128-point chunk (BRUTE; from the Morton-ordered cloud)
+cudaError_t launch_mma_frags(const float4* pos, int64_t Npad, float4* mfrag, cudaStream_t s);
 // the tcgen05 A operand of every 128-point chunk (BRUTE; from the Morton-ordered cloud)
 cudaError_t launch_tf32_operand(const float4* pos, int64_t Npad, float4* tfa, cudaStream_t s);
 cudaError_t launch_relayout(const float* pts, const float* nrm, int64_t N, int64_t Npad,

@@ -194,6 +194,36 @@ cudaError_t launch_pair_layout(const float4* pos, const float4* nrm, int64_t Npa
   return cudaGetLastError();
 }
 
+// The mma.sync A fragments (BRUTE tensor-core filter, spin_persistent FRAG): per 128-point
+// chunk c, row block rb and lane L = (gid, tig) of the m16n8k8 tf32 fragment, the uint4
+// (hi(v0), hi(v1), lo(v0), lo(v1)) with v0, v1 = component tig (x, y, z, -|x|^2) of the
+// chunk's points 32 k0 + sl and 32 (k0 + 1) + sl, k0 = 2 (rb >> 2), sl = (rb & 3) * 8 +
+// ((gid + rb) & 7) -- the rows gid and gid + 8 of row block rb in the staged pair layout;
+// hi = round to nearest tf32, lo = (v - hi) truncated to tf32 (1.0 in the w column: the
+// constant-1 column that carries K).  The split the kernel used to do per tile and group.
+__global__ void k_mma_frags(const float4* __restrict__ pos, int64_t n, uint4* __restrict__ frag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;   // n = chunks * 256
+  const int64_t c = i >> 8;
+  const int rb = (int)(i >> 5) & 7, L = (int)(i & 31), gid = L >> 2, tig = L & 3;
+  const int sl = (rb & 3) * 8 + ((gid + rb) & 7), k0 = 2 * (rb >> 2);
+  auto comp = [&](int64_t j) {
+    const float4 a = pos[j];
+    return tig == 0 ? a.x : tig == 1 ? a.y : tig == 2 ? a.z : -a.w;
+  };
+  const float v0 = comp(c * 128 + 32 * k0 + sl), v1 = comp(c * 128 + 32 * (k0 + 1) + sl);
+  auto hi = [](float x) { return (__float_as_uint(x) + 0x1000u) & 0xffffe000u; };
+  const unsigned h0 = hi(v0), h1 = hi(v1);
+  const unsigned l0 = tig == 3 ? 0x3f800000u : __float_as_uint(v0 - __uint_as_float(h0)) & 0xffffe000u;
+  const unsigned l1 = tig == 3 ? 0x3f800000u : __float_as_uint(v1 - __uint_as_float(h1)) & 0xffffe000u;
+  frag[i] = make_uint4(h0, h1, l0, l1);
+}
+cudaError_t launch_mma_frags(const float4* pos, int64_t Npad, float4* mfrag, cudaStream_t s) {
+  const int64_t n = (Npad / 128) * 256;
+  k_mma_frags<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pos, n, reinterpret_cast<uint4*>(mfrag));
+  return cudaGetLastError();
+}
+
 // The tcgen05 A operand (BRUTE, spin_persistent TC): per 128-point chunk c, 4 KB with row
 // r = point 128 c + r as (x_hi, y_hi, z_hi, w_hi | x_lo, y_lo, z_lo, 1), w = -|x|^2, hi =
 // x rounded to tf32, lo = x - hi truncated to tf32 (the mma.sync filter's operands, split

@@ -76,6 +76,9 @@
                               // warpgroup do not cover its latency (warps wait on the MMA
                               // barrier 37% of samples; tensor pipe 3% busy).
 #endif
+#ifndef SPIN_FRAG_TILE
+#define SPIN_FRAG_TILE 1      // BRUTE tensor-core tiles stage precomputed A fragments (p.mfrag)
+#endif
 #ifndef SPIN_DENSE_QUEUE
 #define SPIN_DENSE_QUEUE 1    // BRUTE: dense tiles queued per group and drained by all warps
 #endif
@@ -1293,6 +1296,15 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         // stage the tile in pair layout (the accept path's copy and the packed-fp32 filter's
         // operands), read back so each f32x2 operand arrives as an aligned register pair
         f2 X2[KP / 2], Y2[KP / 2], Z2[KP / 2], NXX2[KP / 2], NX2[KP / 2], NY2[KP / 2], NZ2[KP / 2];
+        // the tile's precomputed tf32 A fragments (FRAG): 4 KB, one uint4 per (row block, lane)
+        auto stage_frag = [&]() {
+          if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_load(sT, p.mfrag + (size_t)(j[0] >> 7) * 256, 4096u, &s_tile_bar[warp]);
+          }
+          mbar_wait(&s_tile_bar[warp], tile_phase);
+          tile_phase ^= 1u;
+        };
         auto stage = [&]() {
           if (TMA_TILE) {
             // the warp's 128 points, already in staging layout in HBM (tpos): one bulk copy
@@ -1328,10 +1340,15 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         // stage every tile: SPIN_DEFER_STAGE = 2 defers there too, loading A from tpos
         // without the prefetch, which spills)
         // (measured, C4: NEAREST 246.7 -> 242.8 ms deferred, BILINEAR 275.0 -> 279.4 ms: NEAREST only)
-        constexpr bool DEFER = PRUNE == 0 && MMA_FILTER && TMA_TILE &&
+        // FRAG: tensor-core tiles stage their precomputed A fragments (split hi/lo once at
+        // load time: 8 LDS.128 per tile instead of 8 LDS.64 and ~70 ALU / FMA operations) and
+        // the points only once the pre-pass found a candidate
+        constexpr bool FRAG = PRUNE == 0 && MMA_FILTER && TMA_TILE && SPIN_FRAG_TILE;
+        constexpr bool DEFER = !FRAG && PRUNE == 0 && MMA_FILTER && TMA_TILE &&
                                (SPIN_DEFER_STAGE == 2 || (SPIN_DEFER_STAGE == 1 && NT <= 512 && MODE == 0));
         constexpr bool PREFETCH = DEFER && NT <= 512;
-        if (!(DEFER && tile_mma) || phase2) stage();
+        if (FRAG && tile_mma) stage_frag();
+        else if (!(DEFER && tile_mma) || phase2) stage();
         if (PREFETCH && !tile_mma) have_pf = false;   // (a packed-fp32 tile consumes no prefetch)
         unsigned dense_or = 0u;   // mma tiles: OR and popcount of this lane's mask words
         int dense_cnt = 0;
@@ -1376,7 +1393,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           // record (adjacent floats) -- from the staged tile, or (DEFER) from registers
           // holding the same 8 bytes of tpos
           float2 cur[8];
-          if (phase2) {
+          if (FRAG) {
+          } else if (phase2) {
 #pragma unroll
             for (int rb = 0; rb < 8; ++rb) cur[rb] = *reinterpret_cast<const float2*>(sTf + frag_off(rb));
           } else if (DEFER && PREFETCH) {
@@ -1392,6 +1410,14 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             for (int rb = 0; rb < 8; ++rb) cur[rb] = *reinterpret_cast<const float2*>(sTf + frag_off(rb));
           }
           auto afrag = [&](int rb, unsigned& h0, unsigned& h1, unsigned& l0, unsigned& l1) {
+            if (FRAG) {
+              const uint4 fr = reinterpret_cast<const uint4*>(sT)[rb * 32 + lane];
+              h0 = fr.x;
+              h1 = fr.y;
+              l0 = fr.z;
+              l1 = fr.w;
+              return;
+            }
             const float v0 = cur[rb].x, v1 = cur[rb].y;
             h0 = (__float_as_uint(v0) + 0x1000u) & 0xffffe000u;
             h1 = (__float_as_uint(v1) + 0x1000u) & 0xffffe000u;
@@ -1454,6 +1480,10 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             sMask[w * 32 + lane] = accm[w];
             dense_or |= accm[w];
             dense_cnt += __popc(accm[w]);
+          }
+          if (FRAG) {   // the candidates' points for the accept path replace the fragments
+            __syncwarp();
+            stage();
           }
           }
         } else {
