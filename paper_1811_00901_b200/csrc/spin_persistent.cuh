@@ -79,6 +79,9 @@
 #ifndef SPIN_FRAG_TILE
 #define SPIN_FRAG_TILE 1      // BRUTE tensor-core tiles stage precomputed A fragments (p.mfrag)
 #endif
+#ifndef SPIN_PASS1
+#define SPIN_PASS1 1          // BRUTE tensor-core tiles: pre-pass phase with prefetched fragment tiles
+#endif
 #ifndef SPIN_DENSE_QUEUE
 #define SPIN_DENSE_QUEUE 1    // BRUTE: dense tiles queued per group and drained by all warps
 #endif
@@ -787,8 +790,16 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
   // BRUTE dense-tile queue of a group (chunk indices), drained by every warp in phase 2
   // (BILINEAR: C4 275 -> 267 ms, C2 equal; NEAREST, whose re-staging and mask recomputation
   // cost more than the balance gains: C4 243 -> 258 ms, P6 21.9 -> 22.4 ms, so not used)
-  constexpr bool DQ = PRUNE == 0 && CL == 1 && MODE == 1 && SPIN_BRUTE_MMA && SPIN_BRUTE_TMA &&
-                      SPIN_DENSE_QUEUE;
+  // PASS1 (with the precomputed fragments): phase 1 only runs the pre-pass, streaming the
+  // fragment tiles through ONE buffer per warp with the next tile's copy in flight, and
+  // queues every tile that holds a candidate; phase 2 re-stages and decides the queued tiles
+  // (measured: 768-thread CTAs C2 BILINEAR 3.18 -> 3.06 ms, NEAREST 2.90 -> 2.83 ms, P6
+  // 20.31 -> 20.43 ms; 512-thread CTAs slower, C4 BILINEAR 251.7 -> 257.4 ms, NEAREST 229.5
+  // -> 232.8 ms: 768-thread CTAs only, SPIN_PASS1 = 2 forces it everywhere)
+  constexpr bool PASS1 = PRUNE == 0 && CL == 1 && SPIN_BRUTE_MMA && SPIN_BRUTE_TMA && SPIN_FRAG_TILE &&
+                         (SPIN_PASS1 == 2 || (SPIN_PASS1 == 1 && NT > 512));
+  constexpr bool DQ = PASS1 || (PRUNE == 0 && CL == 1 && MODE == 1 && SPIN_BRUTE_MMA && SPIN_BRUTE_TMA &&
+                                SPIN_DENSE_QUEUE);
   constexpr int DQ_CAP = DQ ? 512 : 1;
   __shared__ int s_dq[DQ_CAP];
   __shared__ int s_dq_n, s_dq_head;
@@ -1041,8 +1052,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         }
         // (a step costs one decision per centre slot of the lane: the threshold scales with
         // GS; measured C2 (G = 64): 8 per slot 3.29 ms, 16: 3.24 ms)
-        if (!phase2 && total < live * p.dense_min * ((G + 31) / 32)) return false;
-        if (DQ && !phase2) {
+        if ((PASS1 || !phase2) && total < live * p.dense_min * ((G + 31) / 32)) return false;
+        if (DQ && !PASS1 && !phase2) {
           // the group's dense tiles are few and land on few warps (the cloud is Morton
           // ordered): queue the tile for the CTA-wide second phase, where every warp takes
           // queued tiles until none are left (inline when the queue is full)
@@ -1585,7 +1596,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         __syncwarp();
         bool done = tile_empty;
         if constexpr (DENSE) {
-          if (!done && tile_mma && (phase2 || p.dense_min > 0) && p.debug_skip < 2)
+          if (!done && tile_mma && p.dense_min > 0 && p.debug_skip < 2)
             done = run_dense(dense_or, dense_cnt, j[0] >> 7, phase2);
         }
         if (!done && p.debug_skip < 2) compact_and_accept();
@@ -1760,16 +1771,89 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         }
         tc_it += (unsigned)nq;
       } else if (PRUNE == 0) {
+        // PASS1 state: the next tile's fragment copy is in flight into the warp's buffer
+        bool pf_inflight = false;
+        unsigned pb0[PASS1 ? NCB : 1], pb1[PASS1 ? NCB : 1];   // B fragments of the group
+        if (PASS1) {
+          const int gid = lane >> 2, tig = lane & 3;
+          const float* sBf = reinterpret_cast<const float*>(sB);
+#pragma unroll
+          for (int cb = 0; cb < NCB; ++cb) {
+            const int sb = gid * NCB + cb;
+            float b1 = sBf[(G >= 8 || sb < G ? sb : 0) * 4 + tig];
+            float b0 = tig == 3 ? 1.0f : b1;
+            if (G < 8 && sb >= G) {
+              b0 = 0.0f;
+              b1 = tig == 3 ? -INFINITY : 0.0f;
+            }
+            pb0[cb] = __float_as_uint(b0);
+            pb1[cb] = __float_as_uint(b1);
+          }
+        }
+        auto frag_copy = [&](int chunk) {
+          if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_load(sT, p.mfrag + (size_t)chunk * 256, 4096u, &s_tile_bar[warp]);
+          }
+        };
         for (int t = (int)crank; t < p.n_tiles; t += CL) {   // (a cluster splits the tiles)
           const int base = t * (NT * KP) + tid;
           int j[KP];
 #pragma unroll
           for (int k = 0; k < KP; ++k) j[k] = base + k * NT;
           if (TMA_TILE) j[0] = t * (NT * KP) + warp * 128;   // the warp's 128-point chunk
-          run_tile(j, t + CL < p.n_tiles ? (t + CL) * NWARP + warp : -1, false);
+          const int next = t + CL < p.n_tiles ? (t + CL) * NWARP + warp : -1;
+          const bool sup_hot1 = SUP == 1 || (SUP == 2 && sup_on);
+          if (PASS1 && p.mma && !sup_hot1) {
+            // ---- phase 1: the pre-pass of the tile from its staged fragments
+            const int chunk = j[0] >> 7;
+            if (!pf_inflight) frag_copy(chunk);
+            mbar_wait(&s_tile_bar[warp], tile_phase);
+            tile_phase ^= 1u;
+            pf_inflight = false;
+            uint4 fr[8];
+#pragma unroll
+            for (int rb = 0; rb < 8; ++rb) fr[rb] = reinterpret_cast<const uint4*>(sT)[rb * 32 + lane];
+            __syncwarp();
+            // prefetch the next tile's fragments into the (now free) buffer while the HMMAs
+            // run, unless the queue is nearly full (a tile with a candidate then has to be
+            // decided inline, in this buffer)
+            int room = 0;
+            if (lane == 0) room = *reinterpret_cast<volatile int*>(&s_dq_n) < DQ_CAP - NWARP;
+            room = __shfl_sync(0xffffffffu, room, 0);
+            if (next >= 0 && room) {
+              frag_copy(next);
+              pf_inflight = true;
+            }
+            unsigned andv = 0xffffffffu;
+#pragma unroll
+            for (int rb = 0; rb < 8; ++rb) {
+#pragma unroll
+              for (int cb = 0; cb < NCB; ++cb) {
+                float d0, d1, d2, d3;
+                mma_tf32(d0, d1, d2, d3, fr[rb].x, fr[rb].y, fr[rb].z, fr[rb].w, pb0[cb], pb1[cb], 0.0f, 0.0f);
+                andv &= __float_as_uint(d0) & __float_as_uint(d1);
+                andv &= __float_as_uint(d2) & __float_as_uint(d3);
+              }
+            }
+            if (__any_sync(0xffffffffu, (int)andv >= 0)) {
+              if (pf_inflight) {
+                if (lane == 0) s_dq[atomicAdd(&s_dq_n, 1)] = chunk;   // room was reserved
+              } else {
+                run_tile(j, -1, true);   // queue nearly full: re-stage and decide inline
+              }
+            }
+          } else {
+            if (PASS1 && pf_inflight) {   // (a packed-fp32 tile: drain the prefetch first)
+              mbar_wait(&s_tile_bar[warp], tile_phase);
+              tile_phase ^= 1u;
+              pf_inflight = false;
+            }
+            run_tile(j, next, false);
+          }
         }
         if (DQ) {
-          // phase 2: the group's queued dense tiles, dealt to the warps one at a time
+          // phase 2: the group's queued tiles, dealt to the warps one at a time
           __syncthreads();
           const int nq = min(s_dq_n, DQ_CAP);
           for (;;) {
