@@ -566,8 +566,12 @@ def run_spin(args):
                                 "hi/lo split)" if st0.get("filter_mma") else
                                 "packed fp32 (FFMA2)"),
                      "note": "frac = pair throughput in the paper formulation's flops "
-                             "(20 per pair) over the FP32 peak (north-star metric); the "
-                             "kernel itself is issue/ALU-pipe bound (DESIGN.md 7.2)",
+                             "(20 per pair) over the FP32 peak (north-star metric).  It can "
+                             "exceed 1: BRUTE evaluates every pair's sphere margin on the "
+                             "tensor cores, most tiles end after a sign-AND pre-pass, and "
+                             "only candidates reach the FP32 decision, so the FP32 pipe "
+                             "executes far fewer than 20 flop per pair; the kernel itself is "
+                             "issue / latency bound (ncu in profiles/round2, DESIGN.md 7.2)",
                      "flop_per_pair": FLOP_PER_PAIR,
                      "peak_source": "derived 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md); "
                                     "FFMA microbenchmark measured 72.5 TFLOP/s",
