@@ -92,6 +92,24 @@
 #define SPIN_FILTER_PREPASS 1 // tensor-core filter: AND the margins' sign bits first, gather only
                               // tiles holding a candidate
 #endif
+#ifndef SPIN_FRAG_REG
+#define SPIN_FRAG_REG 0       // 512-thread BRUTE tensor-core tiles: A fragments straight from L2 into
+                              // registers (half a tile at a time, the next half's loads in flight during
+                              // the HMMAs) instead of a bulk copy the warp waits for.  Parity-clean,
+                              // measured slower (C4 filter 106 -> 130 ms, BILINEAR 245 -> 269 ms: the
+                              // per-lane loads go through L1 / LSU, the bulk copy does not): off
+#endif
+#ifndef SPIN_EXP_FRAG_BYTES
+#define SPIN_EXP_FRAG_BYTES 4096u   // measurement only: bytes of the fragment tile actually copied
+#endif
+#ifndef SPIN_PIN_IMG
+#define SPIN_PIN_IMG 1        // dense walks: the lane's image address pinned in a register
+#endif
+#ifndef SPIN_CELLS_HALVES
+#define SPIN_CELLS_HALVES 1   // CELLS: a tile that overflows the ring is compacted in two halves
+                              // (1: NEAREST only -- C5 152.3 -> 150.0 ms, W = 24 556 -> 545 ms; BILINEAR,
+                              // two candidates per lane per pass, measured slower: C3 41.8 -> 43.3 ms)
+#endif
 #ifndef SPIN_QCAP_CELLS
 #define SPIN_QCAP_CELLS 1024  // CELLS per-warp candidate ring (entries)
 #endif
@@ -956,6 +974,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       unsigned qhead = 0, qtail = 0;
       float2 pf[8];            // DEFER: A-fragment pairs of this warp's next tile (prefetched)
       bool have_pf = false;
+      uint4 pfr[4];            // FRAGREG: row blocks 0-3 of the next tile's fragments (prefetched)
+      bool have_pfr = false;
       constexpr int NWD = G / CB;                      // mask words per lane per tile
       // candidate operands: centre slot gs, point (source lane, k) from the staged tile
       // entry = (mask word w << 10) | (source lane << 5) | mask bit (k << 3 | c)
@@ -1085,7 +1105,10 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           cN[s] = sN[g];
           glive |= (unsigned)(lane + 32 * s < G && sM[g] >= 0) << s;
         }
-        const unsigned img0 = (unsigned)__cvta_generic_to_shared(sImg);
+        unsigned img0 = (unsigned)__cvta_generic_to_shared(sImg);
+        // (opaque to the compiler, which otherwise rematerialises the shared-window base --
+        // an S2R and four dependent instructions -- inside the row loop)
+        if (SPIN_PIN_IMG) asm volatile("mov.u32 %0, %0;" : "+r"(img0));
         // live rows by bit scan, two per step where the word holds two (two independent
         // decisions in flight; 768-thread CTAs, with 80 registers, one).  (A row list in the
         // entry ring measured slower: C4 NEAREST 243 -> 276 ms)
@@ -1142,22 +1165,14 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         }
         return true;
       };
-      auto compact_and_accept = [&]() {
-        int cnt = 0;
-        unsigned wm = 0u;   // this lane's nonzero mask words
+      // entries of mask words [w0, w1) of the tile: cnt = this lane's bits in them, x = the
+      // inclusive lane prefix of cnt, total = the warp's
+      auto compact_range = [&](const int w0, const int w1, const int cnt, const int x, const int total) {
+        unsigned wm = 0u;   // this lane's nonzero mask words (BRUTE flat loop)
+        if (PRUNE == 0) {
 #pragma unroll
-        for (int w = 0; w < NWD; ++w) {
-          const unsigned mw = sMask[w * 32 + lane];
-          cnt += __popc(mw);
-          wm |= (unsigned)(mw != 0u) << w;
+          for (int w = 0; w < NWD; ++w) wm |= (unsigned)(sMask[w * 32 + lane] != 0u) << w;
         }
-        int x = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, x, o);
-          if (lane >= o) x += y;
-        }
-        const int total = __shfl_sync(0xffffffffu, x, 31);
         if (total == 0) return;
         qhead = qtail = 0u;   // the ring is empty between tiles
         // common case: the whole tile fits the ring and one scan places every entry;
@@ -1166,8 +1181,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         constexpr int CHB = QCAP >= 64 + 512 ? 16 : QCAP >= 64 + 256 ? 8 : 4;
         static_assert(QCAP >= 64 + 32 * CHB, "ring too small for the dense path");
         const bool dense = total > QCAP - 64;
-        const int nchunks = dense ? (32 / CHB) * NWD : 1;
-        for (int ci = 0;;) {
+        const int nchunks = dense ? (32 / CHB) * w1 : (32 / CHB) * w0 + 1;
+        for (int ci = (32 / CHB) * w0;;) {
           if (ci < nchunks) {
             if (!dense) {
               // no wrap: total <= QCAP - 64 entries from slot 0
@@ -1190,8 +1205,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
                 }
               } else {
                 // dense (CELLS): word by word
-#pragma unroll
-                for (int w = 0; w < NWD; ++w) {
+#pragma unroll 1
+                for (int w = w0; w < w1; ++w) {
                   unsigned m = sMask[w * 32 + lane];
                   const unsigned eb = ((unsigned)w << 10) | ((unsigned)lane << 5);
                   while (m) {
@@ -1286,6 +1301,40 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           if (!more) break;
         }
       };
+      // CELLS tiles (20% of the pairs are candidates; a tile of 4096 pairs often exceeds the
+      // ring): a tile whose entries do not fit the ring is compacted and accepted in two
+      // halves of its mask words, each placed by ONE scan from slot 0 (the two halves' counts
+      // share the scan, 16 bits each), instead of the chunked ring path per mask word
+      constexpr bool HALVES = PRUNE == 1 && (SPIN_CELLS_HALVES == 2 || (SPIN_CELLS_HALVES == 1 && MODE == 0)) && NWD >= 2 && NWD % 2 == 0;
+      auto compact_and_accept = [&]() {
+        unsigned cnt = 0u;
+#pragma unroll
+        for (int w = 0; w < NWD; ++w)
+          cnt += (unsigned)__popc(sMask[w * 32 + lane]) << (HALVES && w >= NWD / 2 ? 16 : 0);
+        unsigned x = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        const unsigned tot = __shfl_sync(0xffffffffu, x, 31);
+        if (tot == 0u) return;
+        const int total = HALVES ? (int)(tot & 0xffffu) + (int)(tot >> 16) : (int)tot;
+        const bool split = HALVES && total > QCAP - 64;
+        // (one call site: the accept passes are inlined once)
+#pragma unroll 1
+        for (int hh = 0; hh < (split ? 2 : 1); ++hh) {
+          const int sh = 16 * hh;
+          const int w0 = split ? hh * (NWD / 2) : 0, w1 = split ? w0 + NWD / 2 : NWD;
+          const int c = split ? (int)((cnt >> sh) & 0xffffu)
+                              : HALVES ? (int)(cnt & 0xffffu) + (int)(cnt >> 16) : (int)cnt;
+          const int xx = split ? (int)((x >> sh) & 0xffffu)
+                               : HALVES ? (int)(x & 0xffffu) + (int)(x >> 16) : (int)x;
+          const int tt = split ? (int)((tot >> sh) & 0xffffu) : total;
+          if (hh) __syncwarp();   // the first half's entries were read before they are overwritten
+          compact_range(w0, w1, c, xx, tt);
+        }
+      };
       // the 8-byte A-fragment pair of row block rb of thread (gid, tig) within a 128-point
       // chunk in pair layout (the same offset in the staged tile and in tpos)
       auto frag_off = [&](int rb) {
@@ -1311,7 +1360,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         auto stage_frag = [&]() {
           if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            bulk_load(sT, p.mfrag + (size_t)(j[0] >> 7) * 256, 4096u, &s_tile_bar[warp]);
+            bulk_load(sT, p.mfrag + (size_t)(j[0] >> 7) * 256, SPIN_EXP_FRAG_BYTES, &s_tile_bar[warp]);
           }
           mbar_wait(&s_tile_bar[warp], tile_phase);
           tile_phase ^= 1u;
@@ -1358,9 +1407,25 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         constexpr bool DEFER = !FRAG && PRUNE == 0 && MMA_FILTER && TMA_TILE &&
                                (SPIN_DEFER_STAGE == 2 || (SPIN_DEFER_STAGE == 1 && NT <= 512 && MODE == 0));
         constexpr bool PREFETCH = DEFER && NT <= 512;
-        if (FRAG && tile_mma) stage_frag();
+        // FRAGREG: the fragments go from L2 to registers, row blocks 0-3 prefetched during the
+        // previous tile and 4-7 during this tile's first HMMAs; the warp never waits for a whole
+        // 4 KB copy, and shared memory is touched only by tiles with a candidate (their points)
+        constexpr bool FRAGREG = FRAG && SPIN_FRAG_REG && NT <= 512 && !PASS1 && SPIN_EXP_FRAG_BYTES == 4096u;
+        static_assert(!FRAGREG || SPIN_FILTER_PREPASS, "FRAGREG loads its fragments in the pre-pass");
+        const bool fragreg = FRAGREG && tile_mma && !phase2;
+        uint4 fa[4], fb[4];
+        auto ldfrag4 = [&](uint4 (&dst)[4], int chunk, int half) {
+          const uint4* src = reinterpret_cast<const uint4*>(p.mfrag) + (size_t)chunk * 256 + half * 128 + lane;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(dst[i].x), "=r"(dst[i].y), "=r"(dst[i].z), "=r"(dst[i].w) : "l"(src + i * 32));
+        };
+        if (fragreg) {
+        } else if (FRAG && tile_mma) stage_frag();
         else if (!(DEFER && tile_mma) || phase2) stage();
         if (PREFETCH && !tile_mma) have_pf = false;   // (a packed-fp32 tile consumes no prefetch)
+        if (FRAGREG && !fragreg) have_pfr = false;
         unsigned dense_or = 0u;   // mma tiles: OR and popcount of this lane's mask words
         int dense_cnt = 0;
         bool tile_empty = false;  // mma tiles: the pre-pass found no candidate (masks not written)
@@ -1421,8 +1486,16 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             for (int rb = 0; rb < 8; ++rb) cur[rb] = *reinterpret_cast<const float2*>(sTf + frag_off(rb));
           }
           auto afrag = [&](int rb, unsigned& h0, unsigned& h1, unsigned& l0, unsigned& l1) {
+            if (FRAGREG && fragreg) {
+              const uint4 fr = rb < 4 ? fa[rb & 3] : fb[rb & 3];
+              h0 = fr.x;
+              h1 = fr.y;
+              l0 = fr.z;
+              l1 = fr.w;
+              return;
+            }
             if (FRAG) {
-              const uint4 fr = reinterpret_cast<const uint4*>(sT)[rb * 32 + lane];
+              const uint4 fr = reinterpret_cast<const uint4*>(sT)[(SPIN_EXP_FRAG_BYTES < 4096u ? (rb & 3) : rb) * 32 + lane];
               h0 = fr.x;
               h1 = fr.y;
               l0 = fr.z;
@@ -1443,8 +1516,18 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             // (one accumulator per column block, for shorter LOP3 chains, measured slower:
             // C4 filter 127 -> 146 ms)
             unsigned andv = 0xffffffffu;
+            if (FRAGREG && fragreg) {
+              if (!have_pfr) ldfrag4(pfr, j[0] >> 7, 0);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) fa[i] = pfr[i];
+              ldfrag4(fb, j[0] >> 7, 1);
+            }
 #pragma unroll
             for (int rb = 0; rb < 8; ++rb) {
+              if (FRAGREG && fragreg && rb == 4) {   // row blocks 0-3 of the next tile
+                have_pfr = next_chunk >= 0;
+                if (have_pfr) ldfrag4(pfr, next_chunk, 0);
+              }
               unsigned h0, h1, l0, l1;
               afrag(rb, h0, h1, l0, l1);
 #pragma unroll
@@ -1460,6 +1543,12 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           tile_empty = !tile_any;
           if (tile_any) {
           if (DEFER && !phase2) stage();   // the candidates' points for the accept path
+          if (FRAGREG && fragreg) {
+            // (rare: row blocks 0-3 again, an L2 hit; the prefetch is dropped so that its
+            // registers are free during the tile's accept path)
+            ldfrag4(fa, j[0] >> 7, 0);
+            have_pfr = false;
+          }
           unsigned accm[NCB];
 #pragma unroll
           for (int w = 0; w < NCB; ++w) accm[w] = 0u;
