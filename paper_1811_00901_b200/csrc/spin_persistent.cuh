@@ -92,6 +92,12 @@
 #define SPIN_FILTER_PREPASS 1 // tensor-core filter: AND the margins' sign bits first, gather only
                               // tiles holding a candidate
 #endif
+#ifndef SPIN_CELLS_LAYOUT2
+#define SPIN_CELLS_LAYOUT2 1  // CELLS: component-major staged tile and entries that decode with two shifts
+#endif
+#ifndef SPIN_SELF_RESOLVE
+#define SPIN_SELF_RESOLVE 1   // NEAREST: the self pair is recognised in resolve(), not in every decision
+#endif
 #ifndef SPIN_FRAG_REG
 #define SPIN_FRAG_REG 0       // 512-thread BRUTE tensor-core tiles: A fragments straight from L2 into
                               // registers (half a tile at a time, the next half's loads in flight during
@@ -491,7 +497,9 @@ __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const f
   const float wval = q * p.inv_b2;                                   // (alpha/b)^2
   // fp32 verdicts need the certified domain (|d| <= D) and |u| < 2^21 (magic rounding)
   // (SPIN_F_NO_FAST_CERT arrives as D2g = -1: every candidate is uncertain)
-  const bool unc0 = !(ds > p.Es_a) | !(dd <= p.D2g) |
+  // (NEAREST: dd == 0 -- the self pair, a duplicate point, or an underflow -- goes to resolve(),
+  // which knows the self pair's bin without arithmetic; keeps ~7 instructions out of every decision)
+  const bool unc0 = !(ds > p.Es_a) | !(dd <= p.D2g) | (SPIN_SELF_RESOLVE && MODE == 0 && !(dd > 0.0f)) |
                     !(fabsf(uval) < 2097152.0f);
   Dec r;
   r.a = 0.f;
@@ -503,7 +511,7 @@ __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const f
   r.far = (dd > p.D2g) & (p.D2g >= 0.0f);
   if (MODE == 0) {
     // the self pair (d == 0): beta = q = 0 exactly, k = ceil(W/2) (or floor), l = 0 (#8)
-    const bool self = (fabsf(d0) + fabsf(d1) + fabsf(d2) == 0.f) & (p.self_fast != 0);
+    const bool self = !SPIN_SELF_RESOLVE && (fabsf(d0) + fabsf(d1) + fabsf(d2) == 0.f) & (p.self_fast != 0);
     // row k = ceil(u) (or floor): certified when u is farther than Eu from an integer;
     // |u| < 2^22 inside the certified domain (dd <= D2g), garbage is ignored outside it
     const float rr = rint_magic(uval);
@@ -561,6 +569,17 @@ __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const f
 template <int MODE>
 __device__ __forceinline__ void resolve(const KParams& p, Dec& d, const float4 P4, const float4 N4,
                                         const float4 X4, const float4 NX4, Ctr& ct) {
+  if (SPIN_SELF_RESOLVE && MODE == 0 && p.self_fast &&
+      fabsf(X4.x - P4.x) + fabsf(X4.y - P4.y) + fabsf(X4.z - P4.z) == 0.f) {
+    // the self pair (d == 0 exactly): beta = q = 0, k = ceil(W/2) (or floor), l = 0 (#8); only
+    // its support test (|n|^2 against cos A_s) needs a certain verdict
+    const float s = fmaf(N4.x, NX4.x, fmaf(N4.y, NX4.y, N4.z * NX4.z));
+    if (s - p.c_f > p.Es_a) {
+      d.status = p.self_k >= 0;
+      d.bin = p.self_k * p.W + p.self_l;
+      return;
+    }
+  }
   ++ct.f64;
   const SlowOut r = slow_pair(P4, N4, X4, NX4, p.W, p.A, p.b, p.cos_As, p.has_support, p.literal,
                               p.floor_bins, MODE);
@@ -986,8 +1005,16 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       // point (rb>>2)*2 + (r>>3).  (Slots and rows are spread so that one lane's
       // candidates read different shared-memory banks in the accept passes.)
       bool tile_mma = false;
+      // CELLS (CL2: component-major staged tile, entries with the centre slot in bits 0-4 and
+      // the point lane * 4 + k in bits 5-11): see stage() and enc_entry below
+      // (groups of 8, 16 or 32 centres: a 5-bit centre slot, 8 centres per mask word)
+      constexpr bool CL2 = PRUNE == 1 && SPIN_CELLS_LAYOUT2 && G <= 32 && CB == 8;
       auto decode_entry = [&](unsigned e, int& gs, int& sl, int& kk) {
-        if (MMA_FILTER && tile_mma) {
+        if (CL2) {
+          gs = (int)(e & 31u);
+          sl = (int)(e >> 7);
+          kk = (int)(e >> 5) & 3;
+        } else if (MMA_FILTER && tile_mma) {
           const int bit = (int)(e & 31u), ln = (int)(e >> 5) & 31;
           const int cbk = (int)(e >> 10), rb = bit & 7, jv = bit >> 3;
           gs = (2 * (ln & 3) + (jv & 1)) * NCB + cbk;
@@ -1001,6 +1028,16 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         }
       };
       auto load_entry = [&](unsigned e, int& gs, float4& P4, float4& N4, float4& X4, float4& NX4) {
+        if (CL2) {
+          // component c of point (lane sl, k) at float c * 128 + sl * 4 + k = c * 128 + (e >> 5)
+          gs = (int)(e & 31u);
+          P4 = sP[gs];
+          N4 = sN[gs];
+          const float* rec = reinterpret_cast<const float*>(sT) + (e >> 5);
+          X4 = make_float4(rec[0], rec[128], rec[256], 0.f);
+          NX4 = make_float4(rec[512], rec[640], rec[768], 0.f);
+          return;
+        }
         int sl, kk;
         decode_entry(e, gs, sl, kk);
         P4 = sP[gs];
@@ -1165,6 +1202,14 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         }
         return true;
       };
+      // entry of mask bit `raw` (= k * 8 + c) of this lane's mask word w.  CL2: centre slot
+      // w * 8 + c | (lane * 4 + k) << 5 = base + raw + 24 k; else (w, lane, raw) fields
+      auto enc_base = [&](unsigned w) -> unsigned {
+        return CL2 ? (w << 3) | ((unsigned)lane << 7) : (w << 10) | ((unsigned)lane << 5);
+      };
+      auto enc_entry = [&](unsigned eb, unsigned raw) -> unsigned {
+        return CL2 ? eb + raw + 3u * (raw & 0x18u) : eb | raw;
+      };
       // entries of mask words [w0, w1) of the tile: cnt = this lane's bits in them, x = the
       // inclusive lane prefix of cnt, total = the warp's
       auto compact_range = [&](const int w0, const int w1, const int cnt, const int x, const int total) {
@@ -1208,11 +1253,11 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
 #pragma unroll 1
                 for (int w = w0; w < w1; ++w) {
                   unsigned m = sMask[w * 32 + lane];
-                  const unsigned eb = ((unsigned)w << 10) | ((unsigned)lane << 5);
+                  const unsigned eb = enc_base((unsigned)w);
                   while (m) {
                     const unsigned bit = msb(m);
                     m ^= 1u << bit;
-                    *q++ = (uint16_t)(eb | bit);
+                    *q++ = (uint16_t)enc_entry(eb, bit);
                   }
                 }
               }
@@ -1247,11 +1292,11 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
                 const int tw = __shfl_sync(0xffffffffu, xw, 31);
                 if (tw <= QCAP - 64) {
                   unsigned pos = qtail + (unsigned)(xw - cw);
-                  const unsigned eb = ((unsigned)(ci / CPW) << 10) | ((unsigned)lane << 5);
+                  const unsigned eb = enc_base((unsigned)(ci / CPW));
                   while (mw) {
                     const unsigned bit = msb(mw);
                     mw ^= 1u << bit;
-                    sQ[pos & (QCAP - 1)] = (uint16_t)(eb | bit);
+                    sQ[pos & (QCAP - 1)] = (uint16_t)enc_entry(eb, bit);
                     ++pos;
                   }
                   qtail += (unsigned)tw;
@@ -1271,11 +1316,11 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
               const int t2 = __shfl_sync(0xffffffffu, x2, 31);
               unsigned pos = qtail + (unsigned)(x2 - c2);
               // entry = (word, lane, raw mask bit CHB * sub + b)
-              const unsigned eb = ((unsigned)(ci / CPW) << 10) | ((unsigned)lane << 5) | (unsigned)(CHB * sub);
+              const unsigned eb = enc_base((unsigned)(ci / CPW));
               while (m) {
                 const unsigned bit = msb(m);
                 m ^= 1u << bit;
-                sQ[pos & (QCAP - 1)] = (uint16_t)(eb | bit);
+                sQ[pos & (QCAP - 1)] = (uint16_t)enc_entry(eb, (unsigned)(CHB * sub) + bit);
                 ++pos;
               }
               qtail += (unsigned)t2;
@@ -1378,8 +1423,26 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             if (!SPIN_TMA_WAIT_ALL) __syncwarp();   // lane 0 acquired the phase; the warp barrier orders the rest
             tile_phase ^= 1u;
           }
+          if (CL2) {
+            // component-major: float4 c of lane l = component c of the lane's four points
+            // (x, y, z, -|x|^2, nx, ny, nz): the packed-fp32 operands of point pairs (0,1) and
+            // (2,3) are its two halves, and an accept-path operand sits at c * 128 + l * 4 + k
+            float4 a[KP], b[KP];
 #pragma unroll
-          for (int k = 0; !TMA_TILE && k < KP; k += 2) {
+            for (int k = 0; k < KP; ++k) {
+              a[k] = __ldg(&p.pos[j[k]]);
+              b[k] = __ldg(&p.nrm[j[k]]);
+            }
+            sT[0 * 32 + lane] = make_float4(a[0].x, a[1].x, a[2].x, a[3].x);
+            sT[1 * 32 + lane] = make_float4(a[0].y, a[1].y, a[2].y, a[3].y);
+            sT[2 * 32 + lane] = make_float4(a[0].z, a[1].z, a[2].z, a[3].z);
+            sT[3 * 32 + lane] = make_float4(-a[0].w, -a[1].w, -a[2].w, -a[3].w);
+            sT[4 * 32 + lane] = make_float4(b[0].x, b[1].x, b[2].x, b[3].x);
+            sT[5 * 32 + lane] = make_float4(b[0].y, b[1].y, b[2].y, b[3].y);
+            sT[6 * 32 + lane] = make_float4(b[0].z, b[1].z, b[2].z, b[3].z);
+          }
+#pragma unroll
+          for (int k = 0; !TMA_TILE && !CL2 && k < KP; k += 2) {
             const float4 a0 = __ldg(&p.pos[j[k]]), a1 = __ldg(&p.pos[j[k + 1]]);
             const float4 b0 = __ldg(&p.nrm[j[k]]), b1 = __ldg(&p.nrm[j[k + 1]]);
             const int pr = k / 2;
@@ -1587,8 +1650,20 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           }
           }
         } else {
+        if (CL2) {
+          f2 r[14];
 #pragma unroll
-        for (int pr = 0; pr < KP / 2; ++pr) {
+          for (int c = 0; c < 7; ++c)
+            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r[2 * c]), "=l"(r[2 * c + 1])
+                         : "r"((unsigned)__cvta_generic_to_shared(sT + c * 32 + lane)));
+#pragma unroll
+          for (int pr = 0; pr < 2; ++pr) {
+            X2[pr] = r[0 + pr]; Y2[pr] = r[2 + pr]; Z2[pr] = r[4 + pr]; NXX2[pr] = r[6 + pr];
+            NX2[pr] = r[8 + pr]; NY2[pr] = r[10 + pr]; NZ2[pr] = r[12 + pr];
+          }
+        }
+#pragma unroll
+        for (int pr = 0; !CL2 && pr < KP / 2; ++pr) {
           f2 r[8];
           const float4* base = sT + pr * 32 + lane;
           asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(r[0]), "=l"(r[1]) : "r"((unsigned)__cvta_generic_to_shared(base)));
