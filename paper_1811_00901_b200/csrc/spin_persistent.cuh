@@ -95,6 +95,9 @@
 #ifndef SPIN_CELLS_LAYOUT2
 #define SPIN_CELLS_LAYOUT2 1  // CELLS: component-major staged tile and entries that decode with two shifts
 #endif
+#ifndef SPIN_CELLS_PIN
+#define SPIN_CELLS_PIN 1      // CELLS accept passes: shared-window addresses pinned in registers
+#endif
 #ifndef SPIN_SELF_RESOLVE
 #define SPIN_SELF_RESOLVE 1   // NEAREST: the self pair is recognised in resolve(), not in every decision
 #endif
@@ -520,9 +523,10 @@ __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const f
     float kf = rr + (du > 0.f ? 1.0f : 0.0f) - p.floor_f;
     // column l = ceil(sqrt(w)) (or floor): certified when w is farther than Ew from
     // every perfect square (fl^2 is exact); sqrt only proposes fl, the squares decide
-    const float wc = fmaxf(wval, 0.0f);
+    // (w below 1e-30, negative included, proposes fl = 0 like the exact zero)
+    const float wc = fmaxf(wval, 1e-30f);
     float rs;
-    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(fmaxf(wc, 1e-30f)));
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(wc));
     const float fl = rint_magic(fmaf(wc, rs, -0.5f));
     const float dlo = fmaf(-fl, fl, wval), dhi = fmaf(fl + 1.0f, fl + 1.0f, -wval);
     const bool wneg = wval < -p.Ew_a;
@@ -1009,6 +1013,36 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
       // the point lane * 4 + k in bits 5-11): see stage() and enc_entry below
       // (groups of 8, 16 or 32 centres: a 5-bit centre slot, 8 centres per mask word)
       constexpr bool CL2 = PRUNE == 1 && SPIN_CELLS_LAYOUT2 && G <= 32 && CB == 8;
+      // CL2: shared-window addresses of the centre constants, the warp's staged tile, its ring
+      // and the images, opaque to the compiler (which otherwise rematerialises the window base
+      // -- an S2R and its dependants -- and the warp offset in every accept pass)
+      unsigned pin_c = 0u, pin_t = 0u, pin_q = 0u;
+      if (CL2 && SPIN_CELLS_PIN) {
+        pin_c = (unsigned)__cvta_generic_to_shared(sP);
+        pin_t = (unsigned)__cvta_generic_to_shared(sT);
+        pin_q = (unsigned)__cvta_generic_to_shared(sQ);
+        asm volatile("mov.u32 %0, %0;" : "+r"(pin_c));
+        asm volatile("mov.u32 %0, %0;" : "+r"(pin_t));
+        asm volatile("mov.u32 %0, %0;" : "+r"(pin_q));
+      }
+      auto lds_f4 = [](unsigned a) {
+        float4 v;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+        return v;
+      };
+      auto lds_f = [](unsigned a) {
+        float v;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+        return v;
+      };
+      auto load_q = [&](unsigned i) -> unsigned {   // ring / queue entry i of this warp
+        if (CL2 && SPIN_CELLS_PIN) {
+          unsigned short v;
+          asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(pin_q + 2u * i));
+          return (unsigned)v;
+        }
+        return (unsigned)sQ[i];
+      };
       auto decode_entry = [&](unsigned e, int& gs, int& sl, int& kk) {
         if (CL2) {
           gs = (int)(e & 31u);
@@ -1031,6 +1065,14 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         if (CL2) {
           // component c of point (lane sl, k) at float c * 128 + sl * 4 + k = c * 128 + (e >> 5)
           gs = (int)(e & 31u);
+          if (SPIN_CELLS_PIN) {
+            const unsigned ca = pin_c + 16u * (e & 31u), ra = pin_t + ((e >> 3) & 0x1ffcu);
+            P4 = lds_f4(ca);
+            N4 = lds_f4(ca + (unsigned)(L.oN - L.oP));
+            X4 = make_float4(lds_f(ra), lds_f(ra + 512u), lds_f(ra + 1024u), 0.f);
+            NX4 = make_float4(lds_f(ra + 2048u), lds_f(ra + 2560u), lds_f(ra + 3072u), 0.f);
+            return;
+          }
           P4 = sP[gs];
           N4 = sN[gs];
           const float* rec = reinterpret_cast<const float*>(sT) + (e >> 5);
@@ -1074,11 +1116,15 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         if (d0.status) {
           ++ct.acc;
           if constexpr (CL > 1) apply_cl<MODE, G, CL>(d0, sImg, IS, g0);
+          else if (CL2 && SPIN_CELLS_PIN)
+            apply_s<MODE, G>(p, d0, pin_c + (unsigned)(L.oImg - L.oP) + 4u * (unsigned)(g0 * IS), g0, &s_carry);
           else apply<MODE, G>(p, d0, sImg + g0 * IS, g0, &s_carry);
         }
         if (APL == 2 && d1.status) {
           ++ct.acc;
           if constexpr (CL > 1) apply_cl<MODE, G, CL>(d1, sImg, IS, g1);
+          else if (CL2 && SPIN_CELLS_PIN)
+            apply_s<MODE, G>(p, d1, pin_c + (unsigned)(L.oImg - L.oP) + 4u * (unsigned)(g1 * IS), g1, &s_carry);
           else apply<MODE, G>(p, d1, sImg + g1 * IS, g1, &s_carry);
         }
       };
@@ -1270,8 +1316,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
                 for (int base = 0; base < total; base += PASS) {
                   const int i0 = base + lane;
                   const bool v0 = i0 < total, v1 = APL == 2 && i0 + 32 < total;
-                  const unsigned e0 = v0 ? (unsigned)sQ[i0] : 0u;
-                  const unsigned e1 = v1 ? (unsigned)sQ[i0 + 32] : 0u;
+                  const unsigned e0 = v0 ? load_q((unsigned)i0) : 0u;
+                  const unsigned e1 = v1 ? load_q((unsigned)i0 + 32u) : 0u;
                   if (v0) process_pair(e0, v0, e1, v1);
                 }
                 return;
@@ -1337,8 +1383,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             if (avail == 0u || (avail < PASS && more)) break;
             const unsigned n = min(PASS, avail);
             const bool v0 = (unsigned)lane < n, v1 = APL == 2 && (unsigned)lane + 32u < n;
-            const unsigned e0 = sQ[(qhead + lane) & (QCAP - 1)];
-            const unsigned e1 = APL == 2 ? sQ[(qhead + 32u + lane) & (QCAP - 1)] : 0u;
+            const unsigned e0 = load_q((qhead + lane) & (QCAP - 1));
+            const unsigned e1 = APL == 2 ? load_q((qhead + 32u + lane) & (QCAP - 1)) : 0u;
             __syncwarp();
             qhead += n;
             if (v0 && !skip_accept) process_pair(v0 ? e0 : 0u, v0, v1 ? e1 : 0u, v1);
