@@ -453,6 +453,8 @@ void plan_thresholds(const spin_ctx* h, int32_t W, double b, double cos_As, bool
   p.Wf = (float)W;
   p.Au = (flags & SPIN_F_LITERAL_HALF_WIDTH) ? (float)(p.A / b) : (float)p.A;
   p.floor_f = (flags & SPIN_F_FLOOR_BINS) ? 1.0f : 0.0f;
+  p.Wff = (float)W + p.floor_f;
+  p.bin_magic = 8388608.0f - p.floor_f * ((float)W + 1.0f);
   p.Es_a = f32_up(Es_a);
   p.Eu_a = f32_up(Eu_a);
   p.Ew_a = f32_up(Ew_a);

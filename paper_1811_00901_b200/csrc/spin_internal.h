@@ -66,6 +66,7 @@ struct KParams {
   float Wf;                  // (float)W
   float Au;                  // u = fma(-beta, inv_b, Au): W/2 (scaled) or fl32(W/(2b)) (literal)
   float floor_f;             // 1.0 for SPIN_F_FLOOR_BINS, else 0.0
+  float Wff, bin_magic;      // W + floor_f; 2^23 - floor_f (W + 1) (NEAREST bin index, decide)
   float self_kf;             // (float)self_k
   float Es_a, Eu_a, Ew_a, D2g;
   int32_t literal, floor_bins, no_fast_cert;

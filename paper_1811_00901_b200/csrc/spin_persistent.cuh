@@ -95,6 +95,19 @@
 #ifndef SPIN_CELLS_LAYOUT2
 #define SPIN_CELLS_LAYOUT2 1  // CELLS: component-major staged tile and entries that decode with two shifts
 #endif
+#ifndef SPIN_CELLS_CULL
+#define SPIN_CELLS_CULL 0     // CELLS: warp tiles of 128 consecutive points; centre batches whose regions
+                              // cannot reach the tile's bounding box skip the pair test.  Parity-clean and
+                              // the cull fires (26% of the batches on C5, 6% on C3: SPIN_CULL_DIAG), but
+                              // the consecutive tiles cost what it saves (their candidates collide in
+                              // the image adds): C5 132.5 -> 133.1 ms, C3 40.1 -> 41.6 ms: off
+#endif
+#ifndef SPIN_CULL_DIAG
+#define SPIN_CULL_DIAG 0      // diagnostic builds: culled / tested centre batches in tiles_dense / dense_rows
+#endif
+#ifndef SPIN_CAND_PER_TILE
+#define SPIN_CAND_PER_TILE 0  // 1: candidates counted once per compacted tile (measured equal to slightly slower: C2 2.92 -> 3.00 ms)
+#endif
 #ifndef SPIN_CELLS_PIN
 #define SPIN_CELLS_PIN 1      // CELLS accept passes: shared-window addresses pinned in registers
 #endif
@@ -520,7 +533,10 @@ __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const f
     const float rr = rint_magic(uval);
     const float du = uval - rr;                                      // exact
     bool ku = !(fabsf(du) > p.Eu_a);
-    float kf = rr + (du > 0.f ? 1.0f : 0.0f) - p.floor_f;
+    // (kf and lf carry the floor-reading shift floor_f, taken out once in the bin index: k and
+    // l are small integers, every sum below is exact)
+    const float ff = p.floor_f, Wff = p.Wff;
+    float kf = rr + (du > 0.f ? 1.0f : 0.0f);
     // column l = ceil(sqrt(w)) (or floor): certified when w is farther than Ew from
     // every perfect square (fl^2 is exact); sqrt only proposes fl, the squares decide
     // (w below 1e-30, negative included, proposes fl = 0 like the exact zero)
@@ -531,11 +547,12 @@ __device__ __forceinline__ Dec decide(const KParams& p, const float4 P4, const f
     const float dlo = fmaf(-fl, fl, wval), dhi = fmaf(fl + 1.0f, fl + 1.0f, -wval);
     const bool wneg = wval < -p.Ew_a;
     bool lu = !(wneg | ((dlo > p.Ew_a) & (dhi > p.Ew_a)));
-    float lf = wneg ? 0.0f : fl + 1.0f - p.floor_f;
-    if (self) { kf = p.self_kf; lf = 0.0f; ku = false; lu = false; }
-    const bool out = (!ku & ((kf < 0.0f) | (kf >= Wf))) | (!lu & (lf >= Wf));
+    float lf = wneg ? ff : fl + 1.0f;
+    if (self) { kf = p.self_kf + ff; lf = ff; ku = false; lu = false; }
+    const bool out = (!ku & ((kf < ff) | (kf >= Wff))) | (!lu & (lf >= Wff));
     r.status = (sup_out | (!unc0 & out)) ? 0 : ((unc0 | ku | lu) ? 2 : 1);
-    r.bin = bin_index(kf, lf, Wf);
+    // (k - ff) W + (l - ff) + 2^23
+    r.bin = (int)(__float_as_uint(__fadd_rn(__fmaf_rn(kf, Wf, lf), p.bin_magic)) & 0x7fffffu);
   } else {
     // BILINEAR region 0 <= u < W-1, w < (W-1)^2  (#12); the self pair (u = W/2, w = 0)
     // is interior for W >= 3 and needs no special case
@@ -1109,7 +1126,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           if (!v1) d1.status = 0;
         }
         if (!v0) d0.status = 0;
-        ct.cand += (unsigned)v0 + (APL == 2 ? (unsigned)v1 : 0u);
+        if (!SPIN_CAND_PER_TILE) ct.cand += (unsigned)v0 + (APL == 2 ? (unsigned)v1 : 0u);
         if (SUP == 2) ct.srej += (unsigned)(v0 & (d0.sup_out != 0));
         if (d0.status == 2) resolve<MODE>(p, d0, P0, N0, X0, NX0, ct);
         if (APL == 2 && d1.status == 2) resolve<MODE>(p, d1, P1, N1, X1, NX1, ct);
@@ -1265,6 +1282,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
           for (int w = 0; w < NWD; ++w) wm |= (unsigned)(sMask[w * 32 + lane] != 0u) << w;
         }
         if (total == 0) return;
+        if (SPIN_CAND_PER_TILE) ct.cand += (unsigned)cnt;   // (this lane's share of the tile's candidates)
         qhead = qtail = 0u;   // the ring is empty between tiles
         // common case: the whole tile fits the ring and one scan places every entry;
         // dense tiles go CHB bits of a mask word (<= 32 * CHB entries) at a time, each
@@ -1447,6 +1465,9 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         // stage the tile in pair layout (the accept path's copy and the packed-fp32 filter's
         // operands), read back so each f32x2 operand arrives as an aligned register pair
         f2 X2[KP / 2], Y2[KP / 2], Z2[KP / 2], NXX2[KP / 2], NX2[KP / 2], NY2[KP / 2], NZ2[KP / 2];
+        // CELLS cull: centre slots whose region can reach this warp tile's bounding box
+        constexpr bool CULL = CL2 && SPIN_CELLS_CULL;
+        unsigned act = 0xffffffffu;
         // the tile's precomputed tf32 A fragments (FRAG): 4 KB, one uint4 per (row block, lane)
         auto stage_frag = [&]() {
           if (lane == 0) {
@@ -1486,6 +1507,47 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             sT[4 * 32 + lane] = make_float4(b[0].x, b[1].x, b[2].x, b[3].x);
             sT[5 * 32 + lane] = make_float4(b[0].y, b[1].y, b[2].y, b[3].y);
             sT[6 * 32 + lane] = make_float4(b[0].z, b[1].z, b[2].z, b[3].z);
+            if (CULL) {
+              // bounding box of the tile's points (sentinels excluded), reduced over the warp in
+              // the order-preserving integer image of the floats (one REDUX per bound)
+              float lo3[3] = {INFINITY, INFINITY, INFINITY}, hi3[3] = {-INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+              for (int k = 0; k < KP; ++k) {
+                if (j[k] < p.N) {
+                  lo3[0] = fminf(lo3[0], a[k].x); hi3[0] = fmaxf(hi3[0], a[k].x);
+                  lo3[1] = fminf(lo3[1], a[k].y); hi3[1] = fmaxf(hi3[1], a[k].y);
+                  lo3[2] = fminf(lo3[2], a[k].z); hi3[2] = fmaxf(hi3[2], a[k].z);
+                }
+              }
+              auto ford = [](float x) { const int i = __float_as_int(x); return i ^ ((i >> 31) & 0x7fffffff); };
+              auto finv = [](int i) { return __int_as_float(i ^ ((i >> 31) & 0x7fffffff)); };
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                lo3[c] = finv(__reduce_min_sync(0xffffffffu, ford(lo3[c])));
+                hi3[c] = finv(__reduce_max_sync(0xffffffffu, ford(hi3[c])));
+              }
+              // lane = centre slot: every point X of the box has a_i <= X_i - P_i <= b_i, so
+              // |X - P|^2 >= sum max(0, a_i, -b_i)^2 and n.(X - P) lies in [bmin, bmax]; the region
+              // needs |X - P| <= R and |n.(X - P) - mid| <= h (h_test also covers the hot filter's
+              // rounding; sl the rounding here: <= 4u of the summed magnitudes)
+              bool may = false;
+              if (lane < G) {
+                const float4 P4 = sP[lane], N4 = sN[lane];
+                const float ax = lo3[0] - P4.x, bx = hi3[0] - P4.x, ay = lo3[1] - P4.y, by = hi3[1] - P4.y;
+                const float az = lo3[2] - P4.z, bz = hi3[2] - P4.z;
+                const float dx = fmaxf(0.f, fmaxf(ax, -bx)), dy = fmaxf(0.f, fmaxf(ay, -by));
+                const float dz = fmaxf(0.f, fmaxf(az, -bz));
+                const float dist2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                const float bmin = fminf(N4.x * ax, N4.x * bx) + fminf(N4.y * ay, N4.y * by) + fminf(N4.z * az, N4.z * bz);
+                const float bmax = fmaxf(N4.x * ax, N4.x * bx) + fmaxf(N4.y * ay, N4.y * by) + fmaxf(N4.z * az, N4.z * bz);
+                const float sl = 2e-6f * (fabsf(ax) + fabsf(bx) + fabsf(ay) + fabsf(by) + fabsf(az) + fabsf(bz)) +
+                                 1e-5f * p.h_test + 1e-30f;
+                const float midf = (float)p.mid, hs = p.h_test + sl;
+                may = sM[lane] >= 0 && dist2 * 0.99999f <= p.R_up * p.R_up * 1.00001f &&
+                      bmin - midf <= hs && bmax - midf >= -hs;
+              }
+              act = __ballot_sync(0xffffffffu, may);
+            }
           }
 #pragma unroll
           for (int k = 0; !TMA_TILE && !CL2 && k < KP; k += 2) {
@@ -1771,6 +1833,12 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         } else {
 #pragma unroll 1
           for (int cb = 0; cb < cb_end; cb += CB) {
+            if (SPIN_CULL_DIAG && lane == 0) ++dense_rows;
+            if (CULL && ((act >> cb) & ((1u << CB) - 1u)) == 0u) {   // no centre of the batch reaches the tile
+              if (SPIN_CULL_DIAG && lane == 0) ++dense_tiles;
+              sMask[(cb / CB) * 32 + lane] = 0u;
+              continue;
+            }
             unsigned mask = 0u;
 #pragma unroll
             for (int c = 0; c < CB; ++c) {
@@ -2159,7 +2227,8 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             int j[KP];
 #pragma unroll
             for (int k = 0; k < KP; ++k) {
-              const int f = f0 + tid + k * NT;
+              // (CULL: a warp's 128 points are consecutive in the gathered order, a compact box)
+              const int f = CL2 && SPIN_CELLS_CULL ? f0 + warp * (32 * KP) + k * 32 + lane : f0 + tid + k * NT;
               if (f < T) {
                 // largest r with sRowO[r] <= f: gallop from the previous point's row, then
                 // bisect
