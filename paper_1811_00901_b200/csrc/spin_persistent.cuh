@@ -121,6 +121,11 @@
                               // measured slower (C4 filter 106 -> 130 ms, BILINEAR 245 -> 269 ms: the
                               // per-lane loads go through L1 / LSU, the bulk copy does not): off
 #endif
+#ifndef SPIN_EXP_ABL
+#define SPIN_EXP_ABL 0        // measurement only (wrong images): pre-pass ablations, bit 0: no HMMAs, bit 1: no
+                              // fragment copy, bit 2: no AND chain, bit 3: no tile ever holds a candidate,
+                              // bit 5: candidate tiles do not stage their points, bit 6: nor compute masks
+#endif
 #ifndef SPIN_EXP_FRAG_BYTES
 #define SPIN_EXP_FRAG_BYTES 4096u   // measurement only: bytes of the fragment tile actually copied
 #endif
@@ -1470,6 +1475,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         unsigned act = 0xffffffffu;
         // the tile's precomputed tf32 A fragments (FRAG): 4 KB, one uint4 per (row block, lane)
         auto stage_frag = [&]() {
+          if (SPIN_EXP_ABL & 2) return;
           if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             bulk_load(sT, p.mfrag + (size_t)(j[0] >> 7) * 256, SPIN_EXP_FRAG_BYTES, &s_tile_bar[warp]);
@@ -1704,12 +1710,22 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
 #pragma unroll
               for (int cb = 0; cb < NCB; ++cb) {
                 float d0, d1, d2, d3;
-                mma_tf32(d0, d1, d2, d3, h0, h1, l0, l1, bu0[cb], bu1[cb], 0.0f, 0.0f);
-                andv &= __float_as_uint(d0) & __float_as_uint(d1);
-                andv &= __float_as_uint(d2) & __float_as_uint(d3);
+                if (SPIN_EXP_ABL & 1) {
+                  d0 = __uint_as_float(h0 ^ bu0[cb]); d1 = __uint_as_float(h1 ^ bu1[cb]);
+                  d2 = __uint_as_float(l0 ^ bu0[cb]); d3 = __uint_as_float(l1 ^ bu1[cb]);
+                } else {
+                  mma_tf32(d0, d1, d2, d3, h0, h1, l0, l1, bu0[cb], bu1[cb], 0.0f, 0.0f);
+                }
+                if (SPIN_EXP_ABL & 4) {
+                  if (rb == 7 && cb == NCB - 1) andv = __float_as_uint(d0) & __float_as_uint(d1) & __float_as_uint(d2) & __float_as_uint(d3);
+                } else {
+                  andv &= __float_as_uint(d0) & __float_as_uint(d1);
+                  andv &= __float_as_uint(d2) & __float_as_uint(d3);
+                }
               }
             }
             tile_any = __any_sync(0xffffffffu, (int)andv >= 0);
+            if (SPIN_EXP_ABL & 8) tile_any = false;
           }
           tile_empty = !tile_any;
           if (tile_any) {
@@ -1724,7 +1740,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
 #pragma unroll
           for (int w = 0; w < NCB; ++w) accm[w] = 0u;
 #pragma unroll
-          for (int rb = 0; rb < 8; ++rb) {
+          for (int rb = 0; rb < ((SPIN_EXP_ABL & 64) ? 0 : 8); ++rb) {
             unsigned h0, h1, l0, l1;
             afrag(rb, h0, h1, l0, l1);
             // up to MB products of the row block in flight before their sign gather (all of
@@ -1752,7 +1768,7 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
             dense_or |= accm[w];
             dense_cnt += __popc(accm[w]);
           }
-          if (FRAG) {   // the candidates' points for the accept path replace the fragments
+          if (FRAG && !(SPIN_EXP_ABL & 32)) {   // the candidates' points for the accept path replace the fragments
             __syncwarp();
             stage();
           }
