@@ -15,6 +15,7 @@ seeded images per config are compared with the oracle's: region mismatches must 
 NEAREST bins identical, BILINEAR interior-edge flips counted and reported (log_parity).
 Definition checked: Alg. 1, under DESIGN.md §3's readings.
 """
+import os
 import numpy as np
 import pytest
 
@@ -187,3 +188,19 @@ def test_p6_paper_shape(spin, torch):
         r.flips()
     finally:
         r.close()
+
+
+@pytest.mark.skipif(os.environ.get("SPIN_WIDE") != "1", reason="one-off wide campaign (SPIN_WIDE=1)")
+def test_wide_campaign(spin, torch):
+    """One-off wider oracle samples on a build (not part of the default suite: ~10 minutes of
+    oracle time): 20,000 seeded images each of C4 (both modes), C3 (both prunings), C5 W = 8
+    and P6 against oracle-BRUTE; logged through SPIN_PARITY_LOG like the default checks."""
+    n = int(os.environ.get("SPIN_WIDE_IMAGES", "20000"))
+    for cfg_id, mode, prune, seed in ((4, "bilinear", None, 404), (4, "nearest", None, 405),
+                                      (3, "bilinear", "cells", 403), (3, "nearest", "brute", 406),
+                                      (5, "nearest", "cells", 407), (6, "nearest", None, 408)):
+        r = Run(spin, torch, cfg_id, mode, prune=prune)
+        try:
+            r.check(clouds.subsample(len(r.cen), n, seed), f"wide: seeded {n}-image subsample")
+        finally:
+            r.close()
