@@ -1217,7 +1217,9 @@ __global__ void __launch_bounds__(NT, 1) spin_persistent(const __grid_constant__
         // live rows by bit scan, two per step where the word holds two (two independent
         // decisions in flight; 768-thread CTAs, with 80 registers, one).  (A row list in the
         // entry ring measured slower: C4 NEAREST 243 -> 276 ms)
-        constexpr int DR = NT <= 512 ? SPIN_DENSE_ROWS : 1;
+        // (NEAREST on the 512-thread launch takes two: C4 NEAREST 213.2 -> 209.8 ms; BILINEAR, with its
+        // longer splat, 245.2 -> 246.3 ms and keeps one)
+        constexpr int DR = NT <= 512 ? (SPIN_DENSE_ROWS == 1 && MODE == 0 ? 2 : SPIN_DENSE_ROWS) : 1;
         unsigned w0 = lw[0], w1 = lw[1], w2 = lw[2], w3 = lw[3];
         auto row_point = [&](int i, int bq, float4& X4, float4& NX4) {
           const int gid = 2 * i + (bq >> 4), half = (bq >> 3) & 1, rb = bq & 7;
